@@ -1,0 +1,156 @@
+/*
+ * sincfft_b200.h -- C ABI of the B200-native NNFFT / fast sinc transform.
+ *
+ * This is the drop-in boundary for the hot path named by BASELINE.json's
+ * north star.  The reference (arXiv 2107.02671, package `sincfft`) is pure
+ * Python and has no FFI; its "operator API" is a handful of Python
+ * functions.  Every entry point below replaces one of them and is bound from
+ * Python through ctypes (paper_2107_02671_b200/_lib.py); INTEGRATION.md shows
+ * the binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - complex arrays are interleaved (re, im) doubles, i.e. numpy complex128;
+ *   - a batch of B coefficient vectors is an (M1, B) row-major array
+ *     (column b of F is F[:, b]); outputs are (M2, B) row-major;
+ *   - `ptr_kind` says whether user pointers are host (SINCFFT_PTR_HOST,
+ *     copied inside the call) or device (SINCFFT_PTR_DEVICE) memory;
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); all work of
+ *     one call is ordered on it, and host-pointer calls synchronize it before
+ *     returning;
+ *   - every function returns a status code; on failure
+ *     sincfft_last_error() returns a thread-local message.
+ *   - plans are immutable after creation; concurrent execute calls on one
+ *     plan are allowed (scratch memory is stream-ordered per call), matching
+ *     the reference contract.
+ */
+#ifndef SINCFFT_B200_H
+#define SINCFFT_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SINCFFT_API __attribute__((visibility("default")))
+#else
+#define SINCFFT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python shim maps them to the reference's exception
+ * classes (ref: pkg/src/sincfft/errors.py:4-13) */
+#define SINCFFT_OK 0
+#define SINCFFT_EPARAM 1       /* -> sincfft.errors.ParameterError        */
+#define SINCFFT_EPOSITIVITY 2  /* -> sincfft.errors.PositivityError       */
+#define SINCFFT_ECUDA 3        /* CUDA runtime failure (RuntimeError)     */
+#define SINCFFT_ENOMEM 4       /* device allocation failed (MemoryError)  */
+#define SINCFFT_EUNSUPPORTED 5 /* outside the implemented envelope        */
+
+#define SINCFFT_PTR_HOST 0
+#define SINCFFT_PTR_DEVICE 1
+
+typedef struct sincfft_nnfft_plan_s *sincfft_nnfft_plan;
+typedef struct sincfft_sinc_plan_s *sincfft_sinc_plan;
+
+/* Geometry of a plan (ref: NnfftGeometry, pkg/src/sincfft/nnfft.py:30-89). */
+typedef struct {
+  int64_t N, M1, M2, N1, K, N2;
+  int32_t m1, m2;
+  double sigma1, sigma2, a, beta1, beta2;
+  /* FFT realisation: pruned Bluestein of length L = L1*L2 over the
+   * Kout = s_hi - s_lo + 1 outputs the gather reads */
+  int64_t L, L1, L2, Kout, s_lo;
+} sincfft_geometry;
+
+/* Thread-local description of the last failure ("" if none). */
+SINCFFT_API const char *sincfft_last_error(void);
+
+/* ABI version (major*10000 + minor*100 + patch). */
+SINCFFT_API int sincfft_version(void);
+
+/* Number of visible CUDA devices (0 if none / no driver). */
+SINCFFT_API int sincfft_device_count(void);
+
+/* --- NNFFT (Algorithm 2.1) ---------------------------------------------
+ * Replaces sincfft.nnfft.nnfft_plan (pkg/src/sincfft/nnfft.py:131-207).
+ * N is the (already rescaled) bandwidth N*, v[M1] frequencies with
+ * |v| <= 1/(2a) (+1e-12; clipped), x[M2] nodes in [-1/2, 1/2] (+1e-12;
+ * clipped).  Only the sinh window is implemented (north star); m1, m2 in
+ * [2, 16].  Validation follows nnfft.py:51-89,152-183 and fails with
+ * SINCFFT_EPARAM / SINCFFT_EPOSITIVITY. */
+SINCFFT_API int sincfft_nnfft_plan_create(sincfft_nnfft_plan *plan, int64_t N, int64_t M1, int64_t M2,
+                              double sigma1, double sigma2, int32_t m1, int32_t m2,
+                              const double *v, const double *x, int32_t ptr_kind,
+                              int32_t device, void *stream);
+
+SINCFFT_API int sincfft_nnfft_plan_destroy(sincfft_nnfft_plan plan);
+
+SINCFFT_API int sincfft_nnfft_plan_geometry(sincfft_nnfft_plan plan, sincfft_geometry *geo);
+
+/* Replaces sincfft.nnfft.nnfft_trafo (nnfft.py:210-243), extended to B
+ * columns sharing one plan (the reference applied column by column).
+ * f: (M1, batch) complex, out: (M2, batch) complex. */
+SINCFFT_API int sincfft_nnfft_execute(sincfft_nnfft_plan plan, const double *f, double *out,
+                          int64_t batch, int32_t ptr_kind, void *stream);
+
+/* Split execute for source-sharded multi-GPU runs: step 1 only (spread onto
+ * the K-grid, device buffer grid[batch][K] complex, overwritten), and steps
+ * 2-4 (deconvolution + FFT + gather) from a caller-supplied (e.g. all-reduced)
+ * device grid.  execute == spread followed by finish. */
+SINCFFT_API int sincfft_nnfft_spread(sincfft_nnfft_plan plan, const double *f, double *grid_dev,
+                         int64_t batch, int32_t ptr_kind, void *stream);
+SINCFFT_API int sincfft_nnfft_finish(sincfft_nnfft_plan plan, const double *grid_dev, double *out,
+                         int64_t batch, int32_t ptr_kind, void *stream);
+
+/* Observability: one execute with DEVICE pointers and CUDA events recorded
+ * on `stream` between the stages; returns after synchronizing the stream
+ * with stage_ms[0..3] = spread (incl. grid zeroing), FFT (deconvolution +
+ * pruned Bluestein), gather, whole call, in milliseconds. */
+SINCFFT_API int sincfft_nnfft_execute_profiled(sincfft_nnfft_plan plan, const double *f,
+                                               double *out, int64_t batch, void *stream,
+                                               double *stage_ms);
+
+/* Number of kernel launches one execute issues (for launch accounting). */
+SINCFFT_API int sincfft_nnfft_launches_per_execute(sincfft_nnfft_plan plan);
+
+/* Materialise the reference's step-0 tables (NnfftPlan.spread_idx/_val,
+ * gather_idx/_val, hat1, hat2; nnfft.py:92-107,175-205) into HOST buffers,
+ * in the reference's layout, from the device-side plan.  Any pointer may be
+ * NULL to skip that table.  Used by drop-in callers that inspect plans and by
+ * the parity tests of the window evaluation. */
+SINCFFT_API int sincfft_nnfft_export_tables(sincfft_nnfft_plan plan, int64_t *spread_idx, double *spread_val,
+                                int64_t *gather_idx, double *gather_val, double *hat1,
+                                double *hat2);
+
+/* --- fast sinc transform (Algorithm 6.3, GENERAL mode) ------------------
+ * Replaces sincfft.fast_sinc.sinc_plan (fast_sinc.py:123-223) for the
+ * GENERAL layout.  The caller supplies the Clenshaw-Curtis points z[n+1]
+ * and weights w[n+1] (host plan-time data, sinc_approx.py:97-106) and the
+ * rescaled bandwidth n_star (fast_sinc.py:97-107); the two inner NNFFT plans
+ * are (n_star, a*N/n_star, z/2) and (n_star, -(N/n_star) z/2, b)
+ * (fast_sinc.py:205-220). */
+SINCFFT_API int sincfft_sinc_plan_create(sincfft_sinc_plan *plan, int64_t N, int64_t n_star, int64_t L1,
+                             int64_t L2, int64_t n, const double *z, const double *w,
+                             const double *a, const double *b, double sigma1, double sigma2,
+                             int32_t m1, int32_t m2, int32_t ptr_kind, int32_t device,
+                             void *stream);
+
+SINCFFT_API int sincfft_sinc_plan_destroy(sincfft_sinc_plan plan);
+
+/* Geometry of the two inner plans (stage 1: sources -> Chebyshev nodes,
+ * stage 3: Chebyshev nodes -> targets). */
+SINCFFT_API int sincfft_sinc_plan_geometry(sincfft_sinc_plan plan, sincfft_geometry *stage1,
+                               sincfft_geometry *stage3);
+
+/* Replaces sincfft.fast_sinc.fast_sinc_transform (fast_sinc.py:226-249).
+ * c: L1 coefficients, complex (c_is_real = 0) or real fp64 (c_is_real = 1,
+ * the reference promotes real input to complex128); out: L2 complex. */
+SINCFFT_API int sincfft_sinc_execute(sincfft_sinc_plan plan, const double *c, int32_t c_is_real,
+                         double *out, int32_t ptr_kind, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SINCFFT_B200_H */

@@ -1,0 +1,27 @@
+"""B200-native NNFFT and fast sinc transform (arXiv 2107.02671).
+
+Drop-in for the hot path of the reference package ``sincfft``: the names,
+signatures, defaults and exception classes of ``sincfft.nnfft`` and
+``sincfft.fast_sinc`` (reference ``pkg/src/sincfft/__init__.py:17-47``), backed
+by hand-written sm_100a CUDA kernels behind the C ABI in
+``include/sincfft_b200.h``.  Importing the package loads that library and
+fails loudly if it has not been built; there is no CPU fallback.
+"""
+
+from . import bounds
+from .errors import ParameterError, PositivityError
+from .fast_sinc import SincMode, SincPlan, fast_sinc_transform, sinc_plan
+from .nnfft import (NnfftGeometry, NnfftPlan, WindowSpec, nnfft_plan, nnfft_trafo,
+                    rescale_frequencies)
+from .quadrature import CcQuadrature, cc_quadrature, cc_weights_direct, cc_weights_fast
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ParameterError", "PositivityError",
+    "WindowSpec", "NnfftGeometry", "NnfftPlan", "nnfft_plan", "nnfft_trafo",
+    "rescale_frequencies",
+    "CcQuadrature", "cc_quadrature", "cc_weights_direct", "cc_weights_fast",
+    "SincMode", "SincPlan", "sinc_plan", "fast_sinc_transform",
+    "bounds", "__version__",
+]

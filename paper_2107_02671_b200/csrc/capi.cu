@@ -1,0 +1,491 @@
+// capi.cu -- the extern "C" drop-in boundary (include/sincfft_b200.h).
+//
+// Each entry point replaces one function of the reference's Python API
+// (pkg/src/sincfft/nnfft.py, fast_sinc.py); the ctypes shim in
+// paper_2107_02671_b200/_lib.py binds them and maps status codes to the
+// reference's exception classes (errors.py:4-13).
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "../../include/sincfft_b200.h"
+#include "nnfft_impl.cuh"
+
+struct sincfft_nnfft_plan_s {
+  sfb::NnfftPlanImpl impl;
+};
+
+struct sincfft_sinc_plan_s {
+  sfb::NnfftPlanImpl st1, st3;
+  int64_t N = 0, n_star = 0, L1 = 0, L2 = 0, n = 0;
+  int device = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    g_last_error.clear();
+    f();
+    return SINCFFT_OK;
+  } catch (const sfb::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return SINCFFT_ENOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SINCFFT_ECUDA;
+  }
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+void check_ptr_kind(int32_t k) {
+  if (k != SINCFFT_PTR_HOST && k != SINCFFT_PTR_DEVICE) sfb::fail(1, "ptr_kind must be 0 (host) or 1 (device)");
+}
+
+// device copy of caller data (host -> device, or device alias)
+struct InBuf {
+  std::unique_ptr<sfb::Scratch> tmp;
+  const void* ptr = nullptr;
+  InBuf(const void* user, size_t bytes, int32_t kind, cudaStream_t s) {
+    if (kind == SINCFFT_PTR_DEVICE) {
+      ptr = user;
+    } else {
+      tmp.reset(new sfb::Scratch(bytes, s));
+      if (bytes) SF_CUDA(cudaMemcpyAsync(tmp->p, user, bytes, cudaMemcpyHostToDevice, s));
+      ptr = tmp->p;
+    }
+  }
+};
+
+void set_device(int dev) {
+  int cur = -1;
+  SF_CUDA(cudaGetDevice(&cur));
+  if (cur != dev) SF_CUDA(cudaSetDevice(dev));
+}
+
+__global__ void k_scale_copy(const double* in, double* out, int64_t n, double s) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = s * in[i];
+}
+
+void fill_geometry(const sfb::NnfftPlanImpl& p, sincfft_geometry* g) {
+  g->N = p.g.N;
+  g->M1 = p.g.M1;
+  g->M2 = p.g.M2;
+  g->N1 = p.g.N1;
+  g->K = p.g.K;
+  g->N2 = p.g.N2;
+  g->m1 = p.g.m1;
+  g->m2 = p.g.m2;
+  g->sigma1 = p.g.sigma1;
+  g->sigma2 = p.g.sigma2;
+  g->a = p.g.a;
+  g->beta1 = p.g.beta1;
+  g->beta2 = p.g.beta2;
+  g->L = p.fft.L;
+  g->L1 = p.fft.L1;
+  g->L2 = p.fft.L2;
+  g->Kout = p.fft.Kout;
+  g->s_lo = p.fft.s_lo;
+}
+
+// reference-layout step-0 tables (nnfft.py:185-205) from the device plan
+template <int M>
+__global__ void k_export_spread(const double* v, int64_t n, double N1, int64_t K, sfb::WinCoef C,
+                                int64_t* idx, double* val) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double pos = N1 * v[i];
+  const double c = floor(pos);
+  double w[2 * M];
+  sfb::window_taps<M>(C, pos - c, w);
+  for (int t = 0; t < 2 * M; ++t) {
+    int64_t sp = (int64_t)c + (t + 1 - M) + K / 2;
+    double vv = w[t];
+    if (sp < 0 || sp >= K) {
+      vv = 0.0;
+      sp = sp < 0 ? 0 : K - 1;
+    }
+    idx[i * 2 * M + t] = sp;
+    val[i * 2 * M + t] = vv;
+  }
+}
+
+template <int M>
+__global__ void k_export_gather(const double* x, int64_t n, double ratio, double N2d, int64_t N2,
+                                double Nd, double beta1, int m1, int64_t N1, sfb::WinCoef C,
+                                int64_t* idx, double* val, double* hat1) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double pos = N2d * (x[j] * ratio);
+  const double c = floor(pos);
+  double w[2 * M];
+  sfb::window_taps<M>(C, pos - c, w);
+  for (int t = 0; t < 2 * M; ++t) {
+    int64_t sp = ((int64_t)c + (t + 1 - M)) % N2;
+    if (sp < 0) sp += N2;
+    idx[j * 2 * M + t] = sp;
+    val[j * 2 * M + t] = w[t];
+  }
+  hat1[j] = sfb::phi_hat_sinh(beta1, m1, N1, Nd * x[j]);
+}
+
+template <int M>
+void export_spread_m(const sfb::NnfftPlanImpl& p, int64_t* idx, double* val, cudaStream_t s) {
+  k_export_spread<M><<<(unsigned)sfb::ceil_div(p.g.M1, 256), 256, 0, s>>>(
+      p.v_clip.p, p.g.M1, (double)p.g.N1, p.g.K, p.c1, idx, val);
+  SF_LAUNCH_CHECK();
+}
+
+template <int M>
+void export_gather_m(const sfb::NnfftPlanImpl& p, int64_t* idx, double* val, double* hat1,
+                     cudaStream_t s) {
+  k_export_gather<M><<<(unsigned)sfb::ceil_div(p.g.M2, 256), 256, 0, s>>>(
+      p.x_clip.p, p.g.M2, (double)p.g.N / (double)p.g.N1, (double)p.g.N2, p.g.N2, (double)p.g.N,
+      p.g.beta1, p.g.m1, p.g.N1, p.c2, idx, val, hat1);
+  SF_LAUNCH_CHECK();
+}
+
+#define SF_DISPATCH_M(m, CALL)                                                        \
+  switch (m) {                                                                        \
+    case 2: CALL(2); break;                                                           \
+    case 3: CALL(3); break;                                                           \
+    case 4: CALL(4); break;                                                           \
+    case 5: CALL(5); break;                                                           \
+    case 6: CALL(6); break;                                                           \
+    case 7: CALL(7); break;                                                           \
+    case 8: CALL(8); break;                                                           \
+    case 9: CALL(9); break;                                                           \
+    case 10: CALL(10); break;                                                         \
+    case 11: CALL(11); break;                                                         \
+    case 12: CALL(12); break;                                                         \
+    case 13: CALL(13); break;                                                         \
+    case 14: CALL(14); break;                                                         \
+    case 15: CALL(15); break;                                                         \
+    case 16: CALL(16); break;                                                         \
+    default: sfb::fail(5, "unsupported window cut-off");                              \
+  }
+
+void build_nnfft(sfb::NnfftPlanImpl& p, int64_t N, int64_t M1, int64_t M2, double sigma1,
+                 double sigma2, int m1, int m2, const double* v_dev, const double* x_dev,
+                 int device, cudaStream_t s) {
+  p.g = sfb::make_geometry(N, M1, M2, sigma1, sigma2, m1, m2);
+  p.device = device;
+  sfb::build_plan(p, v_dev, x_dev, s);
+}
+
+}  // namespace
+
+namespace sfb {
+
+void run_execute(const NnfftPlanImpl& p, const double2* f, double2* out, int batch,
+                 cudaStream_t s) {
+  Scratch grid(sizeof(double2) * (size_t)p.g.K * batch, s);
+  Scratch work(p.fft.single ? 0 : sizeof(double2) * (size_t)p.fft.L * batch, s);
+  Scratch h(sizeof(double2) * (size_t)p.fft.Kout * batch, s);
+  run_spread(p, f, grid.as<double2>(), batch, s);
+  run_fft(p, grid.as<double2>(), h.as<double2>(), work.as<double2>(), batch, s);
+  run_gather(p, h.as<double2>(), out, batch, s);
+}
+
+}  // namespace sfb
+
+extern "C" {
+
+const char* sincfft_last_error(void) { return g_last_error.c_str(); }
+
+int sincfft_version(void) { return 100; }
+
+int sincfft_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int sincfft_nnfft_plan_create(sincfft_nnfft_plan* plan, int64_t N, int64_t M1, int64_t M2,
+                              double sigma1, double sigma2, int32_t m1, int32_t m2,
+                              const double* v, const double* x, int32_t ptr_kind, int32_t device,
+                              void* stream) {
+  return guarded([&] {
+    if (!plan) sfb::fail(1, "plan pointer is NULL");
+    *plan = nullptr;
+    check_ptr_kind(ptr_kind);
+    if (!v || !x) sfb::fail(1, "nnfft_plan: v and x must be non-NULL");
+    // geometry first: its errors must not depend on the data or the device
+    (void)sfb::make_geometry(N, M1, M2, sigma1, sigma2, m1, m2);
+    set_device(device);
+    cudaStream_t s = as_stream(stream);
+    auto* h = new sincfft_nnfft_plan_s();
+    try {
+      InBuf vb(v, sizeof(double) * M1, ptr_kind, s), xb(x, sizeof(double) * M2, ptr_kind, s);
+      build_nnfft(h->impl, N, M1, M2, sigma1, sigma2, m1, m2, (const double*)vb.ptr,
+                  (const double*)xb.ptr, device, s);
+      SF_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *plan = h;
+  });
+}
+
+int sincfft_nnfft_plan_destroy(sincfft_nnfft_plan plan) {
+  return guarded([&] {
+    if (!plan) return;
+    set_device(plan->impl.device);
+    delete plan;
+  });
+}
+
+int sincfft_nnfft_plan_geometry(sincfft_nnfft_plan plan, sincfft_geometry* geo) {
+  return guarded([&] {
+    if (!plan || !geo) sfb::fail(1, "NULL argument");
+    fill_geometry(plan->impl, geo);
+  });
+}
+
+int sincfft_nnfft_execute(sincfft_nnfft_plan plan, const double* f, double* out, int64_t batch,
+                          int32_t ptr_kind, void* stream) {
+  return guarded([&] {
+    if (!plan || !f || !out) sfb::fail(1, "NULL argument");
+    check_ptr_kind(ptr_kind);
+    if (batch < 1 || batch > 65535) sfb::fail(1, "batch must be in [1, 65535]");
+    const sfb::NnfftPlanImpl& p = plan->impl;
+    set_device(p.device);
+    cudaStream_t s = as_stream(stream);
+    const size_t fb = sizeof(double2) * (size_t)p.g.M1 * batch;
+    const size_t ob = sizeof(double2) * (size_t)p.g.M2 * batch;
+    InBuf fin(f, fb, ptr_kind, s);
+    if (ptr_kind == SINCFFT_PTR_DEVICE) {
+      sfb::run_execute(p, (const double2*)fin.ptr, (double2*)out, (int)batch, s);
+    } else {
+      sfb::Scratch o(ob, s);
+      sfb::run_execute(p, (const double2*)fin.ptr, o.as<double2>(), (int)batch, s);
+      SF_CUDA(cudaMemcpyAsync(out, o.p, ob, cudaMemcpyDeviceToHost, s));
+      SF_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+int sincfft_nnfft_spread(sincfft_nnfft_plan plan, const double* f, double* grid_dev,
+                         int64_t batch, int32_t ptr_kind, void* stream) {
+  return guarded([&] {
+    if (!plan || !f || !grid_dev) sfb::fail(1, "NULL argument");
+    check_ptr_kind(ptr_kind);
+    if (batch < 1 || batch > 65535) sfb::fail(1, "batch must be in [1, 65535]");
+    const sfb::NnfftPlanImpl& p = plan->impl;
+    set_device(p.device);
+    cudaStream_t s = as_stream(stream);
+    InBuf fin(f, sizeof(double2) * (size_t)p.g.M1 * batch, ptr_kind, s);
+    sfb::run_spread(p, (const double2*)fin.ptr, (double2*)grid_dev, (int)batch, s);
+    if (ptr_kind == SINCFFT_PTR_HOST) SF_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int sincfft_nnfft_finish(sincfft_nnfft_plan plan, const double* grid_dev, double* out,
+                         int64_t batch, int32_t ptr_kind, void* stream) {
+  return guarded([&] {
+    if (!plan || !grid_dev || !out) sfb::fail(1, "NULL argument");
+    check_ptr_kind(ptr_kind);
+    if (batch < 1 || batch > 65535) sfb::fail(1, "batch must be in [1, 65535]");
+    const sfb::NnfftPlanImpl& p = plan->impl;
+    set_device(p.device);
+    cudaStream_t s = as_stream(stream);
+    sfb::Scratch work(p.fft.single ? 0 : sizeof(double2) * (size_t)p.fft.L * batch, s);
+    sfb::Scratch h(sizeof(double2) * (size_t)p.fft.Kout * batch, s);
+    sfb::run_fft(p, (const double2*)grid_dev, h.as<double2>(), work.as<double2>(), (int)batch, s);
+    const size_t ob = sizeof(double2) * (size_t)p.g.M2 * batch;
+    if (ptr_kind == SINCFFT_PTR_DEVICE) {
+      sfb::run_gather(p, h.as<double2>(), (double2*)out, (int)batch, s);
+    } else {
+      sfb::Scratch o(ob, s);
+      sfb::run_gather(p, h.as<double2>(), o.as<double2>(), (int)batch, s);
+      SF_CUDA(cudaMemcpyAsync(out, o.p, ob, cudaMemcpyDeviceToHost, s));
+      SF_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+int sincfft_nnfft_execute_profiled(sincfft_nnfft_plan plan, const double* f, double* out,
+                                   int64_t batch, void* stream, double* stage_ms) {
+  return guarded([&] {
+    if (!plan || !f || !out || !stage_ms) sfb::fail(1, "NULL argument");
+    if (batch < 1 || batch > 65535) sfb::fail(1, "batch must be in [1, 65535]");
+    const sfb::NnfftPlanImpl& p = plan->impl;
+    set_device(p.device);
+    cudaStream_t s = as_stream(stream);
+    sfb::Scratch grid(sizeof(double2) * (size_t)p.g.K * batch, s);
+    sfb::Scratch work(p.fft.single ? 0 : sizeof(double2) * (size_t)p.fft.L * batch, s);
+    sfb::Scratch h(sizeof(double2) * (size_t)p.fft.Kout * batch, s);
+    cudaEvent_t ev[4];
+    for (auto& e : ev) SF_CUDA(cudaEventCreate(&e));
+    SF_CUDA(cudaEventRecord(ev[0], s));
+    sfb::run_spread(p, (const double2*)f, grid.as<double2>(), (int)batch, s);
+    SF_CUDA(cudaEventRecord(ev[1], s));
+    sfb::run_fft(p, grid.as<double2>(), h.as<double2>(), work.as<double2>(), (int)batch, s);
+    SF_CUDA(cudaEventRecord(ev[2], s));
+    sfb::run_gather(p, h.as<double2>(), (double2*)out, (int)batch, s);
+    SF_CUDA(cudaEventRecord(ev[3], s));
+    SF_CUDA(cudaEventSynchronize(ev[3]));
+    float t;
+    for (int i = 0; i < 3; ++i) {
+      SF_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+      stage_ms[i] = t;
+    }
+    SF_CUDA(cudaEventElapsedTime(&t, ev[0], ev[3]));
+    stage_ms[3] = t;
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
+int sincfft_nnfft_launches_per_execute(sincfft_nnfft_plan plan) {
+  if (!plan) return -1;
+  // memset node (counted as a launch) + spread + FFT (1 or 3) + gather
+  return 1 + 1 + (plan->impl.fft.single ? 1 : 3) + 1;
+}
+
+int sincfft_nnfft_export_tables(sincfft_nnfft_plan plan, int64_t* spread_idx, double* spread_val,
+                                int64_t* gather_idx, double* gather_val, double* hat1,
+                                double* hat2) {
+  return guarded([&] {
+    if (!plan) sfb::fail(1, "NULL plan");
+    const sfb::NnfftPlanImpl& p = plan->impl;
+    set_device(p.device);
+    cudaStream_t s = nullptr;
+    const int64_t n1 = p.g.M1 * 2 * p.g.m1, n2 = p.g.M2 * 2 * p.g.m2;
+    {
+      sfb::Scratch di(sizeof(int64_t) * n1, s), dv(sizeof(double) * n1, s);
+#define SF_EXP_S(MM) export_spread_m<MM>(p, di.as<int64_t>(), dv.as<double>(), s)
+      SF_DISPATCH_M(p.g.m1, SF_EXP_S);
+#undef SF_EXP_S
+      if (spread_idx)
+        SF_CUDA(cudaMemcpyAsync(spread_idx, di.p, sizeof(int64_t) * n1, cudaMemcpyDeviceToHost, s));
+      if (spread_val)
+        SF_CUDA(cudaMemcpyAsync(spread_val, dv.p, sizeof(double) * n1, cudaMemcpyDeviceToHost, s));
+      SF_CUDA(cudaStreamSynchronize(s));
+    }
+    {
+      sfb::Scratch di(sizeof(int64_t) * n2, s), dv(sizeof(double) * n2, s),
+          dh(sizeof(double) * p.g.M2, s);
+#define SF_EXP_G(MM) export_gather_m<MM>(p, di.as<int64_t>(), dv.as<double>(), dh.as<double>(), s)
+      SF_DISPATCH_M(p.g.m2, SF_EXP_G);
+#undef SF_EXP_G
+      if (gather_idx)
+        SF_CUDA(cudaMemcpyAsync(gather_idx, di.p, sizeof(int64_t) * n2, cudaMemcpyDeviceToHost, s));
+      if (gather_val)
+        SF_CUDA(cudaMemcpyAsync(gather_val, dv.p, sizeof(double) * n2, cudaMemcpyDeviceToHost, s));
+      if (hat1)
+        SF_CUDA(cudaMemcpyAsync(hat1, dh.p, sizeof(double) * p.g.M2, cudaMemcpyDeviceToHost, s));
+      SF_CUDA(cudaStreamSynchronize(s));
+    }
+    if (hat2)
+      SF_CUDA(cudaMemcpy(hat2, p.hat2.p, sizeof(double) * p.g.K, cudaMemcpyDeviceToHost));
+  });
+}
+
+// ------------------------------------------------------------- fast sinc
+int sincfft_sinc_plan_create(sincfft_sinc_plan* plan, int64_t N, int64_t n_star, int64_t L1,
+                             int64_t L2, int64_t n, const double* z, const double* w,
+                             const double* a, const double* b, double sigma1, double sigma2,
+                             int32_t m1, int32_t m2, int32_t ptr_kind, int32_t device,
+                             void* stream) {
+  return guarded([&] {
+    if (!plan) sfb::fail(1, "plan pointer is NULL");
+    *plan = nullptr;
+    check_ptr_kind(ptr_kind);
+    if (!z || !w || !a || !b) sfb::fail(1, "sinc_plan: NULL node/weight array");
+    if (N <= 0 || n_star < N || n < 2 || L1 <= 0 || L2 <= 0)
+      sfb::fail(1, "sinc_plan: invalid sizes");
+    set_device(device);
+    cudaStream_t s = as_stream(stream);
+    auto* h = new sincfft_sinc_plan_s();
+    try {
+      h->N = N, h->n_star = n_star, h->L1 = L1, h->L2 = L2, h->n = n, h->device = device;
+      const int64_t nz = n + 1;
+      InBuf zb(z, sizeof(double) * nz, ptr_kind, s), wb(w, sizeof(double) * nz, ptr_kind, s),
+          ab(a, sizeof(double) * L1, ptr_kind, s), bb(b, sizeof(double) * L2, ptr_kind, s);
+      const double scale = (double)N / (double)n_star;  // fast_sinc.py:198
+      sfb::Scratch v1(sizeof(double) * L1, s), x1(sizeof(double) * nz, s),
+          v3(sizeof(double) * nz, s);
+      const unsigned g1 = (unsigned)sfb::ceil_div(L1, 256), gz = (unsigned)sfb::ceil_div(nz, 256);
+      k_scale_copy<<<g1, 256, 0, s>>>((const double*)ab.ptr, v1.as<double>(), L1, scale);
+      k_scale_copy<<<gz, 256, 0, s>>>((const double*)zb.ptr, x1.as<double>(), nz, 0.5);
+      k_scale_copy<<<gz, 256, 0, s>>>((const double*)zb.ptr, v3.as<double>(), nz, -0.5 * scale);
+      SF_LAUNCH_CHECK();
+      // plan1 = nnfft_plan(n_star, a*scale, z/2)      (fast_sinc.py:205-209)
+      build_nnfft(h->st1, n_star, L1, nz, sigma1, sigma2, m1, m2, v1.as<double>(),
+                  x1.as<double>(), device, s);
+      // alpha = w * g fused into stage-1's gather scale (fast_sinc.py:246)
+      sfb::fuse_target_weights(h->st1, (const double*)wb.ptr, s);
+      // plan3 = nnfft_plan(n_star, -(scale/2) z, b)   (fast_sinc.py:216-220)
+      build_nnfft(h->st3, n_star, nz, L2, sigma1, sigma2, m1, m2, v3.as<double>(),
+                  (const double*)bb.ptr, device, s);
+      SF_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *plan = h;
+  });
+}
+
+int sincfft_sinc_plan_destroy(sincfft_sinc_plan plan) {
+  return guarded([&] {
+    if (!plan) return;
+    set_device(plan->device);
+    delete plan;
+  });
+}
+
+int sincfft_sinc_plan_geometry(sincfft_sinc_plan plan, sincfft_geometry* stage1,
+                               sincfft_geometry* stage3) {
+  return guarded([&] {
+    if (!plan) sfb::fail(1, "NULL plan");
+    if (stage1) fill_geometry(plan->st1, stage1);
+    if (stage3) fill_geometry(plan->st3, stage3);
+  });
+}
+
+int sincfft_sinc_execute(sincfft_sinc_plan plan, const double* c, int32_t c_is_real, double* out,
+                         int32_t ptr_kind, void* stream) {
+  return guarded([&] {
+    if (!plan || !c || !out) sfb::fail(1, "NULL argument");
+    check_ptr_kind(ptr_kind);
+    set_device(plan->device);
+    cudaStream_t s = as_stream(stream);
+    const sfb::NnfftPlanImpl& p1 = plan->st1;
+    const sfb::NnfftPlanImpl& p3 = plan->st3;
+    const size_t cb = (c_is_real ? sizeof(double) : sizeof(double2)) * (size_t)plan->L1;
+    InBuf cin(c, cb, ptr_kind, s);
+    sfb::Scratch g1(sizeof(double2) * (size_t)p1.g.K, s);
+    sfb::Scratch w1(p1.fft.single ? 0 : sizeof(double2) * (size_t)p1.fft.L, s);
+    sfb::Scratch h1(sizeof(double2) * (size_t)p1.fft.Kout, s);
+    sfb::Scratch alpha(sizeof(double2) * (size_t)p1.g.M2, s);
+    if (c_is_real) sfb::run_spread_real(p1, (const double*)cin.ptr, g1.as<double2>(), s);
+    else sfb::run_spread(p1, (const double2*)cin.ptr, g1.as<double2>(), 1, s);
+    sfb::run_fft(p1, g1.as<double2>(), h1.as<double2>(), w1.as<double2>(), 1, s);
+    sfb::run_gather(p1, h1.as<double2>(), alpha.as<double2>(), 1, s);
+    const size_t ob = sizeof(double2) * (size_t)plan->L2;
+    if (ptr_kind == SINCFFT_PTR_DEVICE) {
+      sfb::run_execute(p3, alpha.as<double2>(), (double2*)out, 1, s);
+    } else {
+      sfb::Scratch o(ob, s);
+      sfb::run_execute(p3, alpha.as<double2>(), o.as<double2>(), 1, s);
+      SF_CUDA(cudaMemcpyAsync(out, o.p, ob, cudaMemcpyDeviceToHost, s));
+      SF_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+}  // extern "C"

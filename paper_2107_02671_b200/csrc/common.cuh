@@ -1,0 +1,94 @@
+// common.cuh -- shared helpers for the B200 NNFFT library (sm_100a, fp64).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace sfb {
+
+// Error carrying one of the SINCFFT_* status codes (see include/sincfft_b200.h).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define SF_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      if (e_ == cudaErrorMemoryAllocation)                                              \
+        ::sfb::fail(4, std::string("CUDA out of memory at " #call ": ") +               \
+                           cudaGetErrorString(e_));                                     \
+      ::sfb::fail(3, std::string("CUDA error at " #call ": ") + cudaGetErrorString(e_)); \
+    }                                                                                   \
+  } while (0)
+
+#define SF_LAUNCH_CHECK() SF_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------- complex fp64
+__host__ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__host__ __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__host__ __device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__host__ __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__host__ __device__ __forceinline__ double2 cscale(double2 a, double s) {
+  return make_double2(a.x * s, a.y * s);
+}
+// a * (-i)
+__host__ __device__ __forceinline__ double2 cmul_mi(double2 a) { return make_double2(a.y, -a.x); }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Stream-ordered scratch buffer (cudaMallocAsync pool); freed on the stream.
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  Scratch() = default;
+  Scratch(size_t bytes, cudaStream_t st) : s(st) {
+    if (bytes) SF_CUDA(cudaMallocAsync(&p, bytes, st));
+  }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Owning device allocation (plan-lifetime tables).
+template <class T>
+struct DevArray {
+  T* p = nullptr;
+  int64_t n = 0;
+  DevArray() = default;
+  explicit DevArray(int64_t count) { alloc(count); }
+  void alloc(int64_t count) {
+    release();
+    n = count;
+    if (count > 0) SF_CUDA(cudaMalloc(&p, sizeof(T) * (size_t)count));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevArray() { release(); }
+  DevArray(const DevArray&) = delete;
+  DevArray& operator=(const DevArray&) = delete;
+  DevArray(DevArray&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+};
+
+}  // namespace sfb

@@ -1,0 +1,205 @@
+// fft.cuh -- fp64 complex FFT building blocks in shared memory (sm_100a).
+//
+// Step 3 of Algorithm 2.1 is one forward DFT of length N2 (ref:
+// pkg/src/sincfft/nnfft.py:239 -> fft_core.py:24-25, scipy/pocketfft).  N2 is
+// dictated by the reference's geometry and is never a power of two (its
+// factors include the primes 11, 19, 41, 79, 257, 2341, 65537),
+// and parity needs that exact N2.  Only K = N1 + 2 m1 inputs are nonzero and
+// the gather reads only the Kout ~ N2/sigma1 outputs around s = 0, so the
+// DFT is realised as a PRUNED Bluestein chirp-z transform over a 7-smooth
+// length L >= K + Kout - 1 ~ N2 (fft.cu), whose two FFTs of length L are
+// built from the in-place mixed-radix (2,3,4,5,7,8) routines below.
+//
+// Layout conventions
+//   * a transform of length n in shared memory occupies elements e in
+//     [0, n*nb): element i of batch b is e = i*nb + b (nb interleaved
+//     transforms, b fastest so consecutive lanes touch consecutive words);
+//   * physical slot spad(e) = e + e/8 pads one slot per 8 to break the
+//     power-of-two strides of the late stages (16-byte elements);
+//   * DIF maps natural order -> digit-reversed order, DIT maps digit-reversed
+//     order -> natural order, both in place and with forward sign
+//     exp(-2 pi i/n); inverse transforms use conj(FFT(conj(x))).
+#pragma once
+
+#include "common.cuh"
+#include "fft_consts.cuh"
+
+namespace sfb {
+
+constexpr int kMaxStages = 24;
+
+struct FftStages {
+  int n;
+  int nst;
+  int rad[kMaxStages];  // DIF order; product == n
+};
+
+__device__ __forceinline__ int spad(int e) { return e + (e >> 3); }
+
+// ------------------------------------------------------------ radix kernels
+template <int R>
+struct Dft;
+
+template <>
+struct Dft<2> {
+  static __device__ __forceinline__ void run(double2* x) {
+    const double2 a = x[0], b = x[1];
+    x[0] = cadd(a, b);
+    x[1] = csub(a, b);
+  }
+};
+
+template <>
+struct Dft<4> {
+  static __device__ __forceinline__ void run(double2* x) {
+    const double2 t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]);
+    const double2 t2 = cadd(x[1], x[3]), t3 = cmul_mi(csub(x[1], x[3]));
+    x[0] = cadd(t0, t2);
+    x[2] = csub(t0, t2);
+    x[1] = cadd(t1, t3);
+    x[3] = csub(t1, t3);
+  }
+};
+
+template <>
+struct Dft<8> {
+  static __device__ __forceinline__ void run(double2* x) {
+    const double h = 0.70710678118654752440;  // sqrt(1/2)
+    double2 a[4], b[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      a[r] = cadd(x[r], x[r + 4]);
+      b[r] = csub(x[r], x[r + 4]);
+    }
+    // b_r *= W8^r : W8 = (1 - i)/sqrt2, W8^2 = -i, W8^3 = -(1 + i)/sqrt2
+    b[1] = make_double2(h * (b[1].x + b[1].y), h * (b[1].y - b[1].x));
+    b[2] = cmul_mi(b[2]);
+    b[3] = make_double2(h * (b[3].y - b[3].x), -h * (b[3].x + b[3].y));
+    Dft<4>::run(a);
+    Dft<4>::run(b);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      x[2 * r] = a[r];
+      x[2 * r + 1] = b[r];
+    }
+  }
+};
+
+// generic odd radix via the symmetric real-pair formulation
+template <int R>
+struct DftOdd {
+  static __device__ __forceinline__ void run(double2* x) {
+    constexpr int H = (R - 1) / 2;
+    double2 s[H + 1], d[H + 1];
+    double2 x0 = x[0];
+    double2 sum = x0;
+#pragma unroll
+    for (int r = 1; r <= H; ++r) {
+      s[r] = cadd(x[r], x[R - r]);
+      d[r] = csub(x[r], x[R - r]);
+      sum = cadd(sum, s[r]);
+    }
+    double2 out[R];
+    out[0] = sum;
+#pragma unroll
+    for (int k = 1; k <= H; ++k) {
+      double2 A = x0, B = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int r = 1; r <= H; ++r) {
+        const double c = RadixConst<R>::c((r * k) % R);
+        const double sn = RadixConst<R>::s((r * k) % R);
+        A.x = fma(s[r].x, c, A.x);
+        A.y = fma(s[r].y, c, A.y);
+        B.x = fma(d[r].x, sn, B.x);
+        B.y = fma(d[r].y, sn, B.y);
+      }
+      // X_k = A - i B, X_{R-k} = A + i B
+      out[k] = make_double2(A.x + B.y, A.y - B.x);
+      out[R - k] = make_double2(A.x - B.y, A.y + B.x);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = out[r];
+  }
+};
+template <>
+struct Dft<3> : DftOdd<3> {};
+template <>
+struct Dft<5> : DftOdd<5> {};
+template <>
+struct Dft<7> : DftOdd<7> {};
+
+// -------------------------------------------------------------- one stage
+// DIF stage (natural -> reversed): twiddle after the butterfly.
+// DIT stage (reversed -> natural): twiddle before the butterfly.
+// Butterfly q = g*S + j touches elements g*R*S + j + r*S, r < R; its twiddle
+// for leg r is W_n^{r*j*G} with G = n/(R*S).
+template <int R, bool DIT>
+__device__ __forceinline__ void fft_stage(double2* s, int nb_log2, int S, int G,
+                                          const double2* __restrict__ tw, int tid, int nthr) {
+  const int nb = 1 << nb_log2;
+  const int nbf = (G * S) << nb_log2;
+  for (int idx = tid; idx < nbf; idx += nthr) {
+    const int b = idx & (nb - 1);
+    const int q = idx >> nb_log2;
+    const int g = q / S;
+    const int j = q - g * S;
+    const int base = g * R * S + j;
+    double2 x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = s[spad(((base + r * S) << nb_log2) + b)];
+    if (DIT && j != 0) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) x[r] = cmul(x[r], __ldg(tw + r * j * G));
+    }
+    Dft<R>::run(x);
+    if (!DIT && j != 0) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) x[r] = cmul(x[r], __ldg(tw + r * j * G));
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[spad(((base + r * S) << nb_log2) + b)] = x[r];
+  }
+}
+
+template <bool DIT>
+__device__ __forceinline__ void fft_stage_dispatch(int R, double2* s, int nb_log2, int S, int G,
+                                                   const double2* __restrict__ tw, int tid,
+                                                   int nthr) {
+  switch (R) {
+    case 2: fft_stage<2, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
+    case 3: fft_stage<3, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
+    case 4: fft_stage<4, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
+    case 5: fft_stage<5, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
+    case 7: fft_stage<7, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
+    case 8: fft_stage<8, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
+    default: break;
+  }
+}
+
+// Full in-place transforms of nb interleaved length-n vectors in smem.
+// Caller must __syncthreads() before (data loaded); these end synchronized.
+__device__ __forceinline__ void fft_dif(double2* s, int nb_log2, const FftStages& st,
+                                        const double2* __restrict__ tw) {
+  int G = 1, S = st.n;
+  for (int q = 0; q < st.nst; ++q) {
+    const int R = st.rad[q];
+    S /= R;
+    fft_stage_dispatch<false>(R, s, nb_log2, S, G, tw, threadIdx.x, blockDim.x);
+    __syncthreads();
+    G *= R;
+  }
+}
+
+__device__ __forceinline__ void fft_dit(double2* s, int nb_log2, const FftStages& st,
+                                        const double2* __restrict__ tw) {
+  int S = 1, G = st.n;
+  for (int q = st.nst - 1; q >= 0; --q) {
+    const int R = st.rad[q];
+    G /= R;
+    fft_stage_dispatch<true>(R, s, nb_log2, S, G, tw, threadIdx.x, blockDim.x);
+    __syncthreads();
+    S *= R;
+  }
+}
+
+}  // namespace sfb

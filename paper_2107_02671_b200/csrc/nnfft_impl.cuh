@@ -1,0 +1,108 @@
+// nnfft_impl.cuh -- device-resident NNFFT plan (Algorithm 2.1) and its stages.
+//
+// Reference mapping (pkg/src/sincfft/nnfft.py):
+//   geometry            :51-89   -> Geometry (computed on the host, plan.cu)
+//   step 0 tables       :131-207 -> SpreadPlan / GatherPlan / FftPlan: nodes are
+//                                   binned & sorted on the device; window values
+//                                   are NOT tabulated but evaluated per node from
+//                                   per-tap polynomials (window.cuh)
+//   step 1 spread       :229-233 -> spread.cu  (k_spread)
+//   step 2 deconv+embed :235-238 -> folded into the Bluestein pre-chirp table P
+//   step 3 FFT          :239     -> fft.cu     (pruned Bluestein, 1 or 3 kernels)
+//   step 4 gather       :241-243 -> gather.cu  (k_gather, 1/phi_hat_1 fused)
+#pragma once
+
+#include <mutex>
+
+#include "common.cuh"
+#include "fft.cuh"
+#include "window.cuh"
+
+namespace sfb {
+
+struct Geometry {
+  int64_t N, M1, M2, N1, K, N2;
+  int m1, m2;
+  double sigma1, sigma2, a, beta1, beta2;
+};
+
+// Sources, sorted by cell c = floor(N1 v) + K/2 and grouped into "chunks" of
+// at most kChunk sources of one cell.  Chunks of a tile of kTile cells are
+// ordered rank-major (chunk rank within its cell, then cell), so a warp's 32
+// consecutive chunks almost always have pairwise distinct cells.  Work units
+// (one CTA each) are ranges of at most kUnitChunks chunks of one tile.
+constexpr int kTile = 256;
+constexpr int kChunk = 4;
+constexpr int kUnitChunks = 1024;
+constexpr int kSpreadThreads = 256;
+
+struct SpreadPlan {
+  DevArray<double> pos;   // fl(N1 * v), sorted by cell     [M1]
+  DevArray<int> perm;     // original source index          [M1]
+  DevArray<int2> chunks;  // {first sorted index, (local cell << 8) | count}
+  DevArray<int4> units;   // {tile, chunk begin, chunk end, 0}
+  int64_t n_chunks = 0, n_units = 0;
+};
+
+// Targets sorted by fl(N2 * xs); scale = 1/phi_hat_1(N x_j) in sorted order
+// (optionally times an external per-target weight, used by the fast sinc
+// transform to fuse alpha = w * g into stage 1).
+struct GatherPlan {
+  DevArray<double> pos;
+  DevArray<int> perm;
+  DevArray<double> scale;
+};
+
+// Pruned Bluestein: h_{s_lo + k'} = Q[k'] * sum_l (g_l P_l) b_{k'-l},
+// k' in [0, Kout), l in [0, K), realised as a cyclic convolution of length
+// L = L1 * L2 (7-smooth) via FFT.  Bhat = FFT_L(b)/L stored in the four-step
+// "digit-reversed" layout the forward kernels produce.
+struct FftPlan {
+  int64_t L = 0, L1 = 0, L2 = 0, Kout = 0, s_lo = 0;
+  int C = 1, C_log2 = 0;  // columns per CTA in the column kernels
+  bool single = true;     // L fits one CTA
+  FftStages st1{}, st2{}; // L1 (rows / single) and L2 (columns)
+  DevArray<double2> tw1, tw2, tw_lo, tw_hi;
+  DevArray<int> rev2;
+  DevArray<double2> P, Q, Bhat;
+};
+
+struct NnfftPlanImpl {
+  Geometry g{};
+  int device = 0;
+  WinCoef c1{}, c2{};
+  SpreadPlan sp;
+  GatherPlan gp;
+  FftPlan fft;
+  DevArray<double> v_clip, x_clip;  // original order, for export_tables
+  DevArray<double> hat2;            // phi_hat_2 at l - K/2          [K]
+};
+
+// ----- plan.cu
+Geometry make_geometry(int64_t N, int64_t M1, int64_t M2, double sigma1, double sigma2, int m1,
+                       int m2);
+// v, x are device pointers (original order, unclipped) on `stream`.
+void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cudaStream_t stream);
+// multiply the gather scale by per-target weights (device, original order)
+void fuse_target_weights(NnfftPlanImpl& p, const double* w_dev, cudaStream_t stream);
+
+// ----- fft.cu
+void build_fft(NnfftPlanImpl& p, cudaStream_t stream);
+// grid[batch][K] -> h[batch][Kout] (work: batch*L complex scratch)
+void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work, int batch,
+             cudaStream_t stream);
+
+// ----- spread.cu / gather.cu
+// f: (M1, batch) row-major; grid[batch][K] is zeroed and accumulated.
+void run_spread(const NnfftPlanImpl& p, const double2* f, double2* grid, int batch,
+                cudaStream_t stream);
+// real-valued coefficients (fast sinc input), batch 1
+void run_spread_real(const NnfftPlanImpl& p, const double* f, double2* grid, cudaStream_t stream);
+void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batch,
+                cudaStream_t stream);
+
+// whole transform with device pointers (scratch allocated stream-ordered)
+void run_execute(const NnfftPlanImpl& p, const double2* f, double2* out, int batch,
+                 cudaStream_t stream);
+
+}  // namespace sfb

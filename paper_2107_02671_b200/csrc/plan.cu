@@ -1,0 +1,400 @@
+// plan.cu -- step 0 of Algorithm 2.1 on the device (ref: pkg/src/sincfft/
+// nnfft.py:131-207): validation, clipping, node binning/sorting, the phi_hat
+// tables and the FFT tables.  Window values are not tabulated (the reference
+// stores M x 2m tables, nnfft.py:188-205); kernels evaluate them from the
+// per-tap polynomials instead, so a plan holds O(M1 + M2 + K + L) data.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <string>
+
+#include "nnfft_impl.cuh"
+
+namespace sfb {
+
+// --------------------------------------------------------------- geometry
+// ref: NnfftGeometry.from_parameters, nnfft.py:51-89 (same rules & order)
+Geometry make_geometry(int64_t N, int64_t M1, int64_t M2, double sigma1, double sigma2, int m1,
+                       int m2) {
+  if (N <= 0) fail(1, "N must be a positive integer");
+  if (M1 <= 0) fail(1, "M1 must be a positive integer");
+  if (M2 <= 0) fail(1, "M2 must be a positive integer");
+  if (m1 < 2) fail(1, "m1 must be an integer >= 2");
+  if (m2 < 2) fail(1, "m2 must be an integer >= 2");
+  if (!(sigma1 > 1.0) || !(sigma2 > 1.0)) fail(1, "sigma1 and sigma2 must be > 1");
+  const double n1f = sigma1 * (double)N;
+  const int64_t N1 = (int64_t)std::llround(n1f);
+  if (std::fabs(n1f - (double)N1) > 1e-9 || (N1 % 2) != 0)
+    fail(1, "sigma1*N must be an even integer, got " + std::to_string(n1f));
+  if (2 * m1 > N1 / 2)
+    fail(1, "need 2*m1 <= N1/2, got 2*" + std::to_string(m1) + " > " + std::to_string(N1 / 2));
+  const int64_t K = N1 + 2 * m1;
+  const double n2f = sigma2 * (double)K;
+  // Python round() is round-half-even; n2f is never a half-integer tie that
+  // matters here, but mirror it exactly anyway
+  double r = std::nearbyint(n2f);
+  int64_t N2 = (int64_t)r;
+  if (std::fabs(n2f - (double)N2) > 1e-9) N2 = (int64_t)std::ceil(n2f);
+  if (N2 % 2) N2 += 1;
+  const double sigma2_eff = (double)N2 / (double)K;
+  if ((double)(2 * m2) > (1.0 - (double)N / (double)N1) * (double)N2 + 1e-9)
+    fail(1, "need 2*m2 <= (1 - 1/sigma1)*N2, got 2*" + std::to_string(m2) + " > " +
+                std::to_string((1.0 - (double)N / (double)N1) * (double)N2));
+  if (m1 > kMaxM || m2 > kMaxM)
+    fail(5, "window cut-offs above 16 are not supported by the B200 kernels");
+  if (K >= (int64_t)1 << 30 || N2 >= (int64_t)1 << 30 || M1 >= (int64_t)1 << 31 ||
+      M2 >= (int64_t)1 << 31)
+    fail(5, "problem size exceeds the 2^30-point grid / 2^31-node envelope");
+  Geometry g{};
+  g.N = N;
+  g.M1 = M1;
+  g.M2 = M2;
+  g.N1 = N1;
+  g.K = K;
+  g.N2 = N2;
+  g.m1 = m1;
+  g.m2 = m2;
+  g.sigma1 = (double)N1 / (double)N;
+  g.sigma2 = sigma2_eff;
+  g.a = (double)K / (double)N1;
+  const double pi = 3.141592653589793238462643383279502884;
+  // ref: windows.py:77-80 -- sinh requires 5/4 <= sigma <= 2 (+-1e-9)
+  if (!(1.25 - 1e-9 <= g.sigma1 && g.sigma1 <= 2.0 + 1e-9))
+    fail(1, "sinh window requires 5/4 <= sigma <= 2, got sigma=" + std::to_string(g.sigma1));
+  if (!(1.25 - 1e-9 <= g.sigma2 && g.sigma2 <= 2.0 + 1e-9))
+    fail(1, "sinh window requires 5/4 <= sigma <= 2, got sigma=" + std::to_string(g.sigma2));
+  g.beta1 = 2.0 * pi * m1 * (1.0 - 1.0 / (2.0 * g.sigma1));  // windows.py:94-95
+  g.beta2 = 2.0 * pi * m2 * (1.0 - 1.0 / (2.0 * g.sigma2));
+  return g;
+}
+
+// ---------------------------------------------------------------- kernels
+__global__ void k_absmax(const double* a, int64_t n, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = fabs(a[i]);
+    m = (v > m || v != v) ? v : m;  // NaN propagates
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double t = __shfl_xor_sync(0xffffffffu, m, o);
+    m = (t > m || t != t) ? t : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void k_clip(const double* in, double* out, int64_t n, double lim) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = fmin(fmax(in[i], -lim), lim);
+}
+
+// source keys: cell index floor(N1 v) + K/2 (nnfft.py:188-190)
+__global__ void k_src_keys(const double* v, int64_t n, double N1, int64_t halfK, unsigned* key,
+                           int* idx) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double pos = N1 * v[i];
+  key[i] = (unsigned)((int64_t)floor(pos) + halfK);
+  idx[i] = (int)i;
+}
+
+__global__ void k_take_scaled(const double* v, const int* perm, int64_t n, double scale,
+                              double* out) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) out[j] = scale * v[perm[j]];
+}
+
+// first index with key >= c, for c in [0, ncell]
+__global__ void k_lower_bound(const unsigned* key, int64_t n, int64_t ncell, int* start) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c > ncell) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)key[mid] < c) lo = mid + 1;
+    else hi = mid;
+  }
+  start[c] = (int)lo;
+}
+
+__global__ void k_chunk_counts(const int* start, int64_t ncell, int* nch) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= ncell) return;
+  nch[c] = (start[c + 1] - start[c] + kChunk - 1) / kChunk;
+}
+
+__global__ void k_chunk_emit(const int* start, const int* nch, const int* off, int64_t ncell,
+                             unsigned long long* key, int2* desc) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= ncell) return;
+  const int n = start[c + 1] - start[c];
+  const int k = nch[c];
+  const int o = off[c];
+  const unsigned long long tile = (unsigned long long)(c / kTile);
+  const int lc = (int)(c % kTile);
+  for (int r = 0; r < k; ++r) {
+    key[o + r] = (tile << 40) | ((unsigned long long)r << 8) | (unsigned long long)lc;
+    const int cnt = min(kChunk, n - r * kChunk);
+    desc[o + r] = make_int2(start[c] + r * kChunk, (lc << 8) | cnt);
+  }
+}
+
+__global__ void k_tile_bounds(const unsigned long long* key, int64_t n, int64_t ntile,
+                              int* tstart) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > ntile) return;
+  const unsigned long long target = (unsigned long long)t << 40;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (key[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  tstart[t] = (int)lo;
+}
+
+__global__ void k_unit_counts(const int* tstart, int64_t ntile, int* nu) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= ntile) return;
+  nu[t] = (tstart[t + 1] - tstart[t] + kUnitChunks - 1) / kUnitChunks;
+}
+
+__global__ void k_unit_emit(const int* tstart, const int* nu, const int* off, int64_t ntile,
+                            int4* units) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= ntile) return;
+  for (int u = 0; u < nu[t]; ++u) {
+    const int b = tstart[t] + u * kUnitChunks;
+    units[off[t] + u] = make_int4((int)t, b, min(b + kUnitChunks, tstart[t + 1]), 0);
+  }
+}
+
+// target keys: floor(N2 * xs) + N2 with xs = x * (N/N1)  (nnfft.py:200-201)
+__global__ void k_tgt_keys(const double* x, int64_t n, double ratio, double N2d, int64_t N2,
+                           unsigned* key, int* idx) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double xs = x[i] * ratio;
+  key[i] = (unsigned)((int64_t)floor(N2d * xs) + N2);
+  idx[i] = (int)i;
+}
+
+// sorted target positions and 1/phi_hat_1(N x) (nnfft.py:175, 243)
+__global__ void k_tgt_tables(const double* x, const int* perm, int64_t n, double ratio, double N2d,
+                             double Nd, double beta1, int m1, int64_t N1, double* pos,
+                             double* scale, unsigned long long* min_hat_bits) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double xv = x[perm[j]];
+  pos[j] = N2d * (xv * ratio);
+  const double hat = phi_hat_sinh(beta1, m1, N1, Nd * xv);
+  scale[j] = 1.0 / hat;
+  if (!(hat > 0.0)) atomicAdd(min_hat_bits, 1ull);
+}
+
+__global__ void k_hat2(double* hat2, int64_t K, double beta2, int m2, int64_t N2,
+                       unsigned long long* bad) {
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (l >= K) return;
+  const double h = phi_hat_sinh(beta2, m2, N2, (double)(l - K / 2));
+  hat2[l] = h;
+  if (!(h > 0.0)) atomicAdd(bad, 1ull);
+}
+
+__global__ void k_mul_scale(double* scale, const int* perm, const double* w, int64_t n) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) scale[j] *= w[perm[j]];
+}
+
+// ------------------------------------------------------------ host helpers
+namespace {
+
+inline unsigned blocks(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, ceil_div(n, t)); }
+
+double device_absmax(const double* a, int64_t n, cudaStream_t s) {
+  Scratch r(sizeof(unsigned long long), s);
+  SF_CUDA(cudaMemsetAsync(r.p, 0, sizeof(unsigned long long), s));
+  k_absmax<<<std::min<unsigned>(blocks(n), 1024), 256, 0, s>>>(a, n, r.as<unsigned long long>());
+  SF_LAUNCH_CHECK();
+  unsigned long long bits = 0;
+  SF_CUDA(cudaMemcpyAsync(&bits, r.p, sizeof(bits), cudaMemcpyDeviceToHost, s));
+  SF_CUDA(cudaStreamSynchronize(s));
+  double m;
+  std::memcpy(&m, &bits, sizeof(m));
+  return m;
+}
+
+int key_bits(uint64_t maxkey) {
+  int b = 1;
+  while (b < 64 && (maxkey >> b) != 0) ++b;
+  return b;
+}
+
+template <class T>
+T read1(const T* dev, cudaStream_t s) {
+  T v;
+  SF_CUDA(cudaMemcpyAsync(&v, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
+  SF_CUDA(cudaStreamSynchronize(s));
+  return v;
+}
+
+// exclusive scan of n ints into off[0..n], returns total
+int64_t exclusive_scan(const int* in, int* off, int64_t n, cudaStream_t s) {
+  size_t tb = 0;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, off, (int)n + 1, s));
+  Scratch t(tb, s);
+  // in has n entries; scan n+1 using a padded copy so off[n] is the total
+  Scratch pad(sizeof(int) * (n + 1), s);
+  SF_CUDA(cudaMemsetAsync(pad.p, 0, sizeof(int) * (n + 1), s));
+  SF_CUDA(cudaMemcpyAsync(pad.p, in, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, pad.as<int>(), off, (int)n + 1, s));
+  return (int64_t)read1(off + n, s);
+}
+
+}  // namespace
+
+void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cudaStream_t s) {
+  const Geometry& g = p.g;
+  // --- domain checks and clipping (nnfft.py:162-170)
+  const double vlim = 0.5 / g.a;
+  const double vmax = device_absmax(v_dev, g.M1, s);
+  if (!(vmax <= vlim + 1e-12)) {
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "nnfft_plan: frequencies exceed 1/(2a) = %.6g; apply rescale_frequencies to map "
+             "[-1/2, 1/2] data into the band",
+             vlim);
+    fail(1, buf);
+  }
+  const double xmax = device_absmax(x_dev, g.M2, s);
+  if (!(xmax <= 0.5 + 1e-12)) fail(1, "nnfft_plan: spatial nodes must lie in [-1/2, 1/2]");
+  p.v_clip.alloc(g.M1);
+  p.x_clip.alloc(g.M2);
+  k_clip<<<blocks(g.M1), 256, 0, s>>>(v_dev, p.v_clip.p, g.M1, vlim);
+  k_clip<<<blocks(g.M2), 256, 0, s>>>(x_dev, p.x_clip.p, g.M2, 0.5);
+  SF_LAUNCH_CHECK();
+
+  // --- window polynomials (window.cu); sigma of window 2 is N2/K (nnfft.py:173)
+  p.c1 = fit_window(g.m1, g.beta1);
+  p.c2 = fit_window(g.m2, g.beta2);
+
+  // --- phi_hat_2 at l - K/2 (nnfft.py:180-183)
+  p.hat2.alloc(g.K);
+  {
+    Scratch bad(sizeof(unsigned long long), s);
+    SF_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
+    k_hat2<<<blocks(g.K), 256, 0, s>>>(p.hat2.p, g.K, g.beta2, g.m2, g.N2,
+                                       bad.as<unsigned long long>());
+    SF_LAUNCH_CHECK();
+    if (read1(bad.as<unsigned long long>(), s))
+      fail(2, "nnfft_plan: phi_hat_2 must be strictly positive on the coarse grid");
+  }
+
+  // --- sources: sort by cell, chunk, tile into work units
+  {
+    const int64_t M1 = g.M1, K = g.K;
+    Scratch kin(sizeof(unsigned) * M1, s), kout(sizeof(unsigned) * M1, s);
+    Scratch iin(sizeof(int) * M1, s);
+    p.sp.perm.alloc(M1);
+    k_src_keys<<<blocks(M1), 256, 0, s>>>(p.v_clip.p, M1, (double)g.N1, K / 2, kin.as<unsigned>(),
+                                          iin.as<int>());
+    SF_LAUNCH_CHECK();
+    size_t tb = 0;
+    const int bits = key_bits((uint64_t)K);
+    SF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.as<unsigned>(), kout.as<unsigned>(),
+                                            iin.as<int>(), p.sp.perm.p, (int)M1, 0, bits, s));
+    {
+      Scratch t(tb, s);
+      SF_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kin.as<unsigned>(), kout.as<unsigned>(),
+                                              iin.as<int>(), p.sp.perm.p, (int)M1, 0, bits, s));
+    }
+    p.sp.pos.alloc(M1);
+    k_take_scaled<<<blocks(M1), 256, 0, s>>>(p.v_clip.p, p.sp.perm.p, M1, (double)g.N1,
+                                             p.sp.pos.p);
+    SF_LAUNCH_CHECK();
+    Scratch cstart(sizeof(int) * (K + 1), s), nch(sizeof(int) * K, s),
+        coff(sizeof(int) * (K + 1), s);
+    k_lower_bound<<<blocks(K + 1), 256, 0, s>>>(kout.as<unsigned>(), M1, K, cstart.as<int>());
+    k_chunk_counts<<<blocks(K), 256, 0, s>>>(cstart.as<int>(), K, nch.as<int>());
+    SF_LAUNCH_CHECK();
+    const int64_t nchunks = exclusive_scan(nch.as<int>(), coff.as<int>(), K, s);
+    p.sp.n_chunks = nchunks;
+    Scratch ckey(sizeof(unsigned long long) * nchunks, s), cdesc(sizeof(int2) * nchunks, s);
+    Scratch ckey2(sizeof(unsigned long long) * nchunks, s);
+    p.sp.chunks.alloc(nchunks);
+    k_chunk_emit<<<blocks(K), 256, 0, s>>>(cstart.as<int>(), nch.as<int>(), coff.as<int>(), K,
+                                           ckey.as<unsigned long long>(), cdesc.as<int2>());
+    SF_LAUNCH_CHECK();
+    const int64_t ntile = ceil_div(K, kTile);
+    const int kb = 40 + key_bits((uint64_t)ntile);
+    tb = 0;
+    SF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ckey.as<unsigned long long>(),
+                                            ckey2.as<unsigned long long>(), cdesc.as<int2>(),
+                                            p.sp.chunks.p, (int)nchunks, 0, kb, s));
+    {
+      Scratch t(tb, s);
+      SF_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, ckey.as<unsigned long long>(),
+                                              ckey2.as<unsigned long long>(), cdesc.as<int2>(),
+                                              p.sp.chunks.p, (int)nchunks, 0, kb, s));
+    }
+    Scratch tstart(sizeof(int) * (ntile + 1), s), nu(sizeof(int) * ntile, s),
+        uoff(sizeof(int) * (ntile + 1), s);
+    k_tile_bounds<<<blocks(ntile + 1), 256, 0, s>>>(ckey2.as<unsigned long long>(), nchunks, ntile,
+                                                    tstart.as<int>());
+    k_unit_counts<<<blocks(ntile), 256, 0, s>>>(tstart.as<int>(), ntile, nu.as<int>());
+    SF_LAUNCH_CHECK();
+    p.sp.n_units = exclusive_scan(nu.as<int>(), uoff.as<int>(), ntile, s);
+    p.sp.units.alloc(p.sp.n_units);
+    k_unit_emit<<<blocks(ntile), 256, 0, s>>>(tstart.as<int>(), nu.as<int>(), uoff.as<int>(), ntile,
+                                              p.sp.units.p);
+    SF_LAUNCH_CHECK();
+    SF_CUDA(cudaStreamSynchronize(s));
+  }
+
+  // --- targets: sort by fine-grid cell, 1/phi_hat_1, output window [s_lo, s_hi]
+  {
+    const int64_t M2 = g.M2;
+    const double ratio = (double)g.N / (double)g.N1;  // x/sigma1 (nnfft.py:200)
+    Scratch kin(sizeof(unsigned) * M2, s), kout(sizeof(unsigned) * M2, s);
+    Scratch iin(sizeof(int) * M2, s);
+    p.gp.perm.alloc(M2);
+    k_tgt_keys<<<blocks(M2), 256, 0, s>>>(p.x_clip.p, M2, ratio, (double)g.N2, g.N2,
+                                          kin.as<unsigned>(), iin.as<int>());
+    SF_LAUNCH_CHECK();
+    size_t tb = 0;
+    const int bits = key_bits((uint64_t)(2 * g.N2 + 2));
+    SF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.as<unsigned>(), kout.as<unsigned>(),
+                                            iin.as<int>(), p.gp.perm.p, (int)M2, 0, bits, s));
+    {
+      Scratch t(tb, s);
+      SF_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kin.as<unsigned>(), kout.as<unsigned>(),
+                                              iin.as<int>(), p.gp.perm.p, (int)M2, 0, bits, s));
+    }
+    p.gp.pos.alloc(M2);
+    p.gp.scale.alloc(M2);
+    Scratch bad(sizeof(unsigned long long), s);
+    SF_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
+    k_tgt_tables<<<blocks(M2), 256, 0, s>>>(p.x_clip.p, p.gp.perm.p, M2, ratio, (double)g.N2,
+                                            (double)g.N, g.beta1, g.m1, g.N1, p.gp.pos.p,
+                                            p.gp.scale.p, bad.as<unsigned long long>());
+    SF_LAUNCH_CHECK();
+    if (read1(bad.as<unsigned long long>(), s))
+      fail(2, "nnfft_plan: phi_hat_1(N x_j) must be strictly positive at every node");
+    const double plo = read1(p.gp.pos.p, s);
+    const double phi = read1(p.gp.pos.p + (M2 - 1), s);
+    const int64_t s_lo = (int64_t)std::floor(plo) + 1 - g.m2;
+    const int64_t s_hi = (int64_t)std::floor(phi) + g.m2;
+    p.fft.s_lo = s_lo;
+    p.fft.Kout = std::min<int64_t>(s_hi - s_lo + 1, g.N2);
+  }
+
+  build_fft(p, s);
+  SF_CUDA(cudaStreamSynchronize(s));
+}
+
+void fuse_target_weights(NnfftPlanImpl& p, const double* w_dev, cudaStream_t s) {
+  k_mul_scale<<<blocks(p.g.M2), 256, 0, s>>>(p.gp.scale.p, p.gp.perm.p, w_dev, p.g.M2);
+  SF_LAUNCH_CHECK();
+}
+
+}  // namespace sfb

@@ -1,0 +1,107 @@
+// window.cuh -- the sinh-type window of arXiv 2107.02671 on the device.
+//
+// Reference: omega(x) = sinh(beta sqrt(1-x^2)) / sinh(beta) on |x| < 1, zero
+// outside, beta = 2 pi m (1 - 1/(2 sigma)) (pkg/src/sincfft/windows.py:94-95,
+// 109-124), applied on a grid as phi(t) = omega(n_grid t / m) (windows.py:
+// 212-214); its Fourier transform through I1 (windows.py:143-160, 217-220).
+//
+// On the NNFFT path every window value has the form
+//     g_t(d) = omega((t - d)/m),   t in [1-m, m],  d in [0, 1)
+// where d is the fractional grid offset of a node (spread: d = N1 v -
+// floor(N1 v), nnfft.py:188-191; gather: d = N2 xs - floor(N2 xs),
+// nnfft.py:200-204; omega is even so the sign of the argument is irrelevant).
+//
+// Instead of sqrt + exp + expm1 per tap (the reference's form; ~40 fp64 ops)
+// each tap is a degree-P polynomial in u = 2d - 1, fitted at plan time in
+// 80-bit long double and validated against the exact window to <= 5e-15
+// absolute (|omega| <= 1).  Two symmetries halve the work:
+//   * g_{1-t}(u) = g_t(-u): tap pair (t, 1-t) shares the even part E(u^2) and
+//     the odd part u*O(u^2) of one polynomial: g_t = E + uO, g_{1-t} = E - uO;
+//   * the two edge taps t = m, 1-m carry the sqrt branch point of omega at
+//     |x| = 1: g_m(d) = sqrt(d) H(u), g_{1-m}(d) = sqrt(1-d) H(-u) with H
+//     analytic, so they are exactly zero where the reference's are (d = 0).
+// Cost: about m*(P+1) DFMA + 2 sqrt per node for all 2m taps.
+#pragma once
+
+#include <cmath>
+
+#include "common.cuh"
+
+namespace sfb {
+
+constexpr int kMaxM = 16;   // largest supported window cut-off m
+constexpr int kMaxNE = 9;   // even coefficients for P <= 16
+constexpr int kMaxNO = 8;   // odd coefficients for P <= 16
+
+// polynomial degree per cut-off, chosen from a long-double fit study so the
+// worst tap error is <= 1e-15 for every sigma in [5/4, 2]
+__host__ __device__ constexpr int window_degree(int m) {
+  return m <= 2 ? 16 : m <= 3 ? 15 : m <= 6 ? 14 : m <= 9 ? 13 : 12;
+}
+
+// Coefficients for the m tap pairs; pair q < m-1 is the inner pair
+// (t = q+1, 1-t), pair m-1 the edge pair.  Passed to kernels by value, so the
+// coefficients live in the constant bank and feed DFMA operands directly.
+struct WinCoef {
+  double e[kMaxM][kMaxNE];
+  double o[kMaxM][kMaxNO];
+};
+
+// All 2M tap values w[i] = g_{i+1-M}(d) for one node.  Host and device use
+// the same instruction sequence (host validation emulates the kernel).
+template <int M>
+__host__ __device__ __forceinline__ void window_taps(const WinCoef& C, double d, double* w) {
+  constexpr int P = window_degree(M);
+  constexpr int NE = P / 2 + 1;
+  constexpr int NO = (P + 1) / 2;
+  const double u = 2.0 * d - 1.0;
+  const double u2 = u * u;
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    double E = C.e[q][NE - 1];
+#pragma unroll
+    for (int k = NE - 2; k >= 0; --k) E = fma(E, u2, C.e[q][k]);
+    double O = C.o[q][NO - 1];
+#pragma unroll
+    for (int k = NO - 2; k >= 0; --k) O = fma(O, u2, C.o[q][k]);
+    const double hi = fma(u, O, E);
+    const double lo = fma(-u, O, E);
+    if (q < M - 1) {
+      w[M + q] = hi;
+      w[M - 1 - q] = lo;
+    } else {
+      w[2 * M - 1] = sqrt(d) * hi;
+      w[0] = sqrt(1.0 - d) * lo;
+    }
+  }
+}
+
+// Fourier transform of the sinh shape function, omega_hat(v)
+// (windows.py:143-160), all three branches; on the NNFFT path only the
+// w > 1e-3 branch is reachable.
+__device__ inline double omega_hat_sinh(double beta, double v) {
+  const double pi = 3.141592653589793238462643383279502884;
+  const double one_m = -expm1(-2.0 * beta);
+  const double w = beta * beta - 4.0 * pi * pi * v * v;
+  if (w > 1e-3) {
+    const double z = sqrt(w);
+    return 2.0 * pi * beta * cyl_bessel_i1(z) * exp(-beta) / (one_m * z);
+  }
+  const double pref = 2.0 * pi * beta * exp(-beta) / one_m;
+  if (w >= -1e-3) return pref * (0.5 + w / 16.0 + w * w / 384.0 + w * w * w / 18432.0);
+  const double zn = sqrt(-w);
+  return pref * j1(zn) / zn;
+}
+
+// phi_hat(v) = (m/n_grid) omega_hat(v m / n_grid)   (windows.py:217-220)
+__device__ inline double phi_hat_sinh(double beta, int m, int64_t n_grid, double v) {
+  const double sc = (double)m / (double)n_grid;
+  return sc * omega_hat_sinh(beta, v * sc);
+}
+
+// Host: fit + validate the coefficients for cut-off m and shape beta.
+// Throws Error(SINCFFT_EUNSUPPORTED) if m is outside [2, kMaxM] or the
+// validation bound fails.  Defined in window.cu.
+WinCoef fit_window(int m, double beta, double* max_err_out = nullptr);
+
+}  // namespace sfb
