@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 NNFFT hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config 3|1|2|4|5]
+
+A "step" is one NNFFT execute (Algorithm 2.1 steps 1-4, ``nnfft_trafo``) over
+the workload's nodes with the plan (step 0) built beforehand, exactly how the
+reference is used (plan once, transform many).  Default workload: config 3 of
+BASELINE.json (N = 2^20, M1 = M2 = 2^24, m1 = m2 = 8, sigma = 2, clustered
+nodes 0.5 cos(pi u), complex128) -- the largest single-GPU configuration and
+the one the north star's scaling target names.
+
+* ``value``: (M1 + M2) nodes/s over K device-timed steps, inputs resident in
+  HBM, CUDA events on the launching stream, max over ranks.
+* ``e2e``: same metric through the C ABI with pinned HOST buffers (H2D of f
+  and D2H of the output inside the timed region).
+* ``roofline``: algorithmic bytes of the dominant kernel over
+  its CUDA-event duration measured live, against MEASURED_PEAKS.json.
+* ``cpu_baseline``: the CPU oracle (a restatement of the reference; the
+  reference itself is pure single-threaded numpy/scipy) on a bounded sample.
+
+N > 1 (torchrun): the one config-3 problem is split -- each rank spreads
+M1/N sources and gathers M2/N targets; the partial K-grids are summed with
+one NCCL all-reduce (the path's only exchange step); the FFT is
+replicated.  ``scaling`` is "strong".
+"""
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "NNFFT (M1+M2) nodes/sec fp64 at 1/2/4/8 B200; % of HBM roofline"
+
+CONFIGS = {
+    "1": dict(N=256, M1=1024, M2=1024, m=4, clustered=False, batch=0,
+              desc="config1: NNFFT N=256, M1=M2=1024, m1=m2=4, sigma=2, uniform nodes"),
+    "2": dict(N=4096, M1=65536, M2=65536, m=8, clustered=False, batch=0,
+              desc="config2: NNFFT N=4096, M1=M2=65536, m1=m2=8, sigma=2, uniform nodes"),
+    "3": dict(N=1 << 20, M1=1 << 24, M2=1 << 24, m=8, clustered=True, batch=0,
+              desc="config3: NNFFT N=2^20, M1=M2=2^24, m1=m2=8, sigma=2, clustered nodes "
+                   "0.5cos(pi u), complex128"),
+    "4": dict(N=65536, M1=1 << 20, M2=1 << 20, m=6, clustered=False, batch=256,
+              desc="config4: batched NNFFT N=65536, M1=M2=2^20, 256 columns, m1=m2=6"),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """Polls NVML during the timed region (sm clock, max clock, throttle reasons)."""
+
+    REASONS = {
+        "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4, "sync_boost": 0x10,
+    }
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_inputs(cfg, seed=0):
+    from tests.inputs import nodes_and_coeffs
+    return nodes_and_coeffs(seed, cfg["M1"], cfg["M2"], clustered=cfg["clustered"],
+                            batch=cfg["batch"])
+
+
+def cpu_sample_rate(cfg, steps=1, warmup=0, sample_nodes=1 << 22):
+    """Time the CPU oracle's trafo (single-threaded numpy/scipy, like the
+    reference) on a bounded sample: the workload's geometry (N, m) with
+    sample_nodes sources and targets drawn the same way."""
+    from oracle import sincfft_oracle as O
+    M = min(sample_nodes, cfg["M1"])
+    sub = dict(cfg, M1=M, M2=M, batch=0)
+    v, x, f = make_inputs(sub, seed=1)
+    n_star, vs = O.rescale_frequencies(cfg["N"], v, 2.0, cfg["m"])
+    t0 = time.perf_counter()
+    tab = O.plan(n_star, vs, x, m1=cfg["m"], m2=cfg["m"])
+    t_plan = time.perf_counter() - t0
+    for _ in range(warmup):
+        O.trafo(tab, f)
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.trafo(tab, f)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    return {"value": 2 * M / t, "unit": "nodes/s", "cores": 1, "kind": "port",
+            "sample": f"oracle trafo, N={cfg['N']}, m={cfg['m']}, M1=M2={M} "
+                      f"({'clustered' if cfg['clustered'] else 'uniform'}), median of {steps}, "
+                      f"plan {t_plan:.1f}s untimed",
+            "seconds_per_step": t}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # bound the whole K+W run to ~2.5 min of single-core work: per-step cost of
+    # the oracle trafo is ~0.85 s (FFT at N=2^20) + ~0.5 us per node
+    budget = 150.0 / (args.steps + args.warmup)
+    M = 1 << 22
+    while M > 1 << 14 and 0.85 + 2 * M * 0.5e-6 > budget:
+        M >>= 1
+    base = cpu_sample_rate(cfg, steps=args.steps, warmup=args.warmup, sample_nodes=M)
+    line = {"metric": METRIC, "value": base["value"], "unit": "nodes/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": base["seconds_per_step"] * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "sample": base["sample"]},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": base["value"], "unit": "nodes/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, cfg):
+    import torch
+    import paper_2107_02671_b200 as sf
+    from paper_2107_02671_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    sh = C.c_void_p(stream.cuda_stream)
+
+    v, x, f = make_inputs(cfg)
+    m = cfg["m"]
+    n_star, vs = sf.rescale_frequencies(cfg["N"], v, 2.0, m)
+    # shard sources and targets (contiguous index ranges)
+    s0, s1 = rank * cfg["M1"] // world, (rank + 1) * cfg["M1"] // world
+    t0_, t1_ = rank * cfg["M2"] // world, (rank + 1) * cfg["M2"] // world
+    torch.cuda.synchronize()
+    tp = time.perf_counter()
+    plan = sf.nnfft_plan(n_star, vs[s0:s1], x[t0_:t1_], m1=m, m2=m, device=local)
+    torch.cuda.synchronize()
+    plan_ms = (time.perf_counter() - tp) * 1e3
+    geo = plan.backend_geometry
+    B = max(cfg["batch"], 1)
+    fshard = np.ascontiguousarray(f[s0:s1])
+    d_f = torch.from_numpy(fshard).to(dev)
+    d_out = torch.empty((t1_ - t0_,) + ((B,) if cfg["batch"] else ()), dtype=torch.complex128,
+                        device=dev)
+    d_grid = torch.empty((B, geo["K"]), dtype=torch.complex128, device=dev)
+    L = _lib.lib
+    ph = plan.handle
+
+    def step():
+        if world == 1:
+            _lib.check(L.sincfft_nnfft_execute(ph, d_f.data_ptr(), d_out.data_ptr(), B,
+                                               _lib.PTR_DEVICE, sh))
+        else:
+            _lib.check(L.sincfft_nnfft_spread(ph, d_f.data_ptr(), d_grid.data_ptr(), B,
+                                              _lib.PTR_DEVICE, sh))
+            dist.all_reduce(torch.view_as_real(d_grid))
+            _lib.check(L.sincfft_nnfft_finish(ph, d_grid.data_ptr(), d_out.data_ptr(), B,
+                                              _lib.PTR_DEVICE, sh))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        ev1.synchronize()
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    total_nodes = (cfg["M1"] + cfg["M2"]) * B
+    value = total_nodes / (ms * 1e-3)
+
+    # per-stage device times (spread / fft / gather), live, same stream
+    stage = np.zeros(4)
+    buf = (C.c_double * 4)()
+    nprof = max(3, min(args.steps, 20))
+    for _ in range(nprof):
+        _lib.check(L.sincfft_nnfft_execute_profiled(ph, d_f.data_ptr(), d_out.data_ptr(), B, sh,
+                                                    buf))
+        stage += np.array(buf[:])
+    stage /= nprof
+    names = ["spread", "fft", "gather"]
+    K, N2, Ms, Mt = geo["K"], geo["N2"], s1 - s0, t1_ - t0_
+    alg = {"spread": 8 * Ms + B * (16 * Ms + 16 * K),
+           "fft": B * (16 * K + 16 * N2),
+           "gather": 8 * Mt + B * (16 * N2 + 16 * Mt)}
+    dom = names[int(np.argmax(stage[:3]))]
+    t_dom = stage[names.index(dom)] * 1e-3
+    peak, peak_kind = peaks()
+    achieved = alg[dom] / t_dom / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        with open(tf) as fh:
+            traffic = json.load(fh).get(f"config{args.config}", {}).get(dom)
+
+    # end to end through the C ABI with pinned host buffers
+    h_f = torch.from_numpy(fshard).pin_memory()
+    h_out = torch.empty(tuple(d_out.shape), dtype=torch.complex128).pin_memory()
+    h2d = h_f.numel() * 16
+    d2h = h_out.numel() * 16
+
+    def e2e_step():
+        if world == 1:
+            _lib.check(L.sincfft_nnfft_execute(ph, h_f.data_ptr(), h_out.data_ptr(), B,
+                                               _lib.PTR_HOST, sh))
+        else:
+            _lib.check(L.sincfft_nnfft_spread(ph, h_f.data_ptr(), d_grid.data_ptr(), B,
+                                              _lib.PTR_HOST, sh))
+            dist.all_reduce(torch.view_as_real(d_grid))
+            _lib.check(L.sincfft_nnfft_finish(ph, d_grid.data_ptr(), h_out.data_ptr(), B,
+                                              _lib.PTR_HOST, sh))
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    e2e_val = total_nodes / (e2e_ms * 1e-3)
+    # the e2e output must agree with the device-resident one (grid flushes use
+    # fp64 atomics, so summation order -- and the last bits -- may differ)
+    dev_out = d_out.cpu().numpy()
+    assert np.max(np.abs(h_out.numpy() - dev_out)) <= 1e-13 * np.abs(fshard).sum(), \
+        "e2e and device outputs differ"
+
+    launches = L.sincfft_nnfft_launches_per_execute(ph) * args.steps
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_sample_rate(cfg)
+        cpu.pop("seconds_per_step", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "N": cfg["N"], "M1": cfg["M1"], "M2": cfg["M2"],
+                       "m1": m, "m2": m, "sigma1": 2.0, "sigma2": 2.0, "batch": B,
+                       "N_star": n_star, "N1": geo["N1"], "K": K, "N2": N2,
+                       "fft_length_L": geo["L"], "l2": "inputs larger than L2 "
+                       "(f and out 256 MiB each per column vs 126 MB L2)",
+                       "parallelism": f"sources+targets sharded x{world}" +
+                       (", NCCL all-reduce of the K-grid" if world > 1 else "")},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "alg_bytes_per_launch": alg[dom],
+                         "launch_ms": t_dom * 1e3},
+            "stage_ms": {n: float(stage[i]) for i, n in enumerate(names)},
+            "plan_ms": plan_ms,
+            "e2e": {"value": e2e_val, "unit": "nodes/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="3")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

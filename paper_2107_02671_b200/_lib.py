@@ -12,7 +12,8 @@ import os
 
 from .errors import ParameterError, PositivityError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libsincfft_b200.so")
+LIB_PATH = os.environ.get("SINCFFT_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "libsincfft_b200.so")
 
 OK, EPARAM, EPOSITIVITY, ECUDA, ENOMEM, EUNSUPPORTED = range(6)
 PTR_HOST, PTR_DEVICE = 0, 1

@@ -69,6 +69,17 @@ void set_device(int dev) {
   int cur = -1;
   SF_CUDA(cudaGetDevice(&cur));
   if (cur != dev) SF_CUDA(cudaSetDevice(dev));
+  // keep freed stream-ordered scratch cached in the device pool (the default
+  // release threshold 0 would hand it back to the driver at every sync and
+  // turn each execute's scratch into fresh cudaMalloc calls)
+  static bool configured[64] = {};
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaMemPool_t pool;
+    SF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;
+    SF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    configured[dev] = true;
+  }
 }
 
 __global__ void k_scale_copy(const double* in, double* out, int64_t n, double s) {
@@ -351,8 +362,8 @@ int sincfft_nnfft_execute_profiled(sincfft_nnfft_plan plan, const double* f, dou
 
 int sincfft_nnfft_launches_per_execute(sincfft_nnfft_plan plan) {
   if (!plan) return -1;
-  // memset node (counted as a launch) + spread + FFT (1 or 3) + gather
-  return 1 + 1 + (plan->impl.fft.single ? 1 : 3) + 1;
+  // memset node (counted as a launch) + spread + FFT (1 or 3) + gather + unpermute
+  return 1 + 1 + (plan->impl.fft.single ? 1 : 3) + 2;
 }
 
 int sincfft_nnfft_export_tables(sincfft_nnfft_plan plan, int64_t* spread_idx, double* spread_val,

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(256) k_colfwd(FftArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(512) k_rowmul(FftArgs a, int spectrum) {
+__global__ void __launch_bounds__(256) k_rowmul(FftArgs a, int spectrum) {
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int64_t p = blockIdx.x;
@@ -259,7 +259,8 @@ FftStages make_stages(int64_t n) {
   st.n = (int)n;
   int64_t r = n;
   std::vector<int> rad;
-  while (r % 8 == 0) rad.push_back(8), r /= 8;
+  while (r % 16 == 0) rad.push_back(16), r /= 16;
+  if (r % 8 == 0) rad.push_back(8), r /= 8;
   if (r % 4 == 0) rad.push_back(4), r /= 4;
   if (r % 2 == 0) rad.push_back(2), r /= 2;
   for (int p : {7, 5, 3})
@@ -291,17 +292,34 @@ std::vector<int> digit_reverse(const FftStages& st) {
   return rev;
 }
 
+// Relative cost of one length-n smem FFT per point: every stage is one
+// shared-memory round trip (~4 DFMA-equivalents per point) plus its
+// butterfly arithmetic per point (radix 16/8/4/2 are cheap, odd radices not).
+double stage_cost(int64_t n) {
+  double c = 0;
+  const FftStages st = make_stages(n);
+  for (int i = 0; i < st.nst; ++i) {
+    switch (st.rad[i]) {
+      case 16: c += 4 + 6.5; break;
+      case 8: c += 4 + 5.5; break;
+      case 4: c += 4 + 4.5; break;
+      case 2: c += 4 + 3.0; break;
+      case 3: c += 4 + 7.0; break;
+      case 5: c += 4 + 10.0; break;
+      case 7: c += 4 + 14.0; break;
+    }
+  }
+  return c;
+}
+
 double cost(int64_t L1, int64_t L2) {
-  // smem-pass dominated: penalise odd radices and large rows (low occupancy)
-  auto c1 = [](int64_t n) {
-    double c = 0;
-    int64_t r = n;
-    for (int p : {7, 5, 3})
-      while (r % p == 0) c += 0.15, r /= p;
-    return c;
-  };
-  double c = (double)(L1 * L2) * (1.0 + c1(L1) * 0.1 + c1(L2) * 0.1);
-  if (L1 > 4096) c *= 1.08;
+  double c = (double)(L1 * L2) * (2.0 * stage_cost(L1) + 2.0 * stage_cost(L2) + 12.0);
+  if (L1 > 4096) c *= 1.05;  // one CTA per SM for the longest rows
+  // column kernels move C contiguous elements (16*C bytes) per row: fewer than
+  // 8 columns per CTA wastes DRAM bursts
+  int C = 8;
+  while (C > 1 && C * L2 > kColElems) C >>= 1;
+  if (C < 8) c *= 1.0 + 0.12 * (C == 4 ? 1 : C == 2 ? 2 : 3);
   return c;
 }
 
@@ -416,7 +434,7 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
     a.Y = f.Bhat.p;
     k_colfwd<IN_PLAIN><<<dim3((unsigned)ceil_div(f.L1, f.C), 1), 256, smc, s>>>(a);
     SF_LAUNCH_CHECK();
-    k_rowmul<<<dim3((unsigned)f.L2, 1), 512, smr, s>>>(a, 1);
+    k_rowmul<<<dim3((unsigned)f.L2, 1), 256, smr, s>>>(a, 1);
     SF_LAUNCH_CHECK();
   }
   SF_CUDA(cudaStreamSynchronize(s));  // b is released at scope exit
@@ -439,7 +457,7 @@ void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* w
   const dim3 gc((unsigned)ceil_div(f.L1, f.C), batch);
   k_colfwd<IN_GP><<<gc, 256, smc, s>>>(a);
   SF_LAUNCH_CHECK();
-  k_rowmul<<<dim3((unsigned)f.L2, batch), 512, smr, s>>>(a, 0);
+  k_rowmul<<<dim3((unsigned)f.L2, batch), 256, smr, s>>>(a, 0);
   SF_LAUNCH_CHECK();
   k_colinv<<<gc, 256, smc, s>>>(a);
   SF_LAUNCH_CHECK();

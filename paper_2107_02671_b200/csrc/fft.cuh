@@ -8,7 +8,7 @@
 // the gather reads only the Kout ~ N2/sigma1 outputs around s = 0, so the
 // DFT is realised as a PRUNED Bluestein chirp-z transform over a 7-smooth
 // length L >= K + Kout - 1 ~ N2 (fft.cu), whose two FFTs of length L are
-// built from the in-place mixed-radix (2,3,4,5,7,8) routines below.
+// built from the in-place mixed-radix (2,3,4,5,7,8,16) routines below.
 //
 // Layout conventions
 //   * a transform of length n in shared memory occupies elements e in
@@ -85,6 +85,40 @@ struct Dft<8> {
   }
 };
 
+// 16 = 4 x 4: X[k1 + 4 k2] = DFT4_{n2}( W16^{n2 k1} DFT4_{n1}(x[4 n1 + n2]) )
+template <>
+struct Dft<16> {
+  static __device__ __forceinline__ void run(double2* x) {
+    const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;  // cos, sin(pi/8)
+    const double h = 0.70710678118654752440;
+    double2 y[4][4];
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+      double2 t[4] = {x[n2], x[4 + n2], x[8 + n2], x[12 + n2]};
+      Dft<4>::run(t);
+#pragma unroll
+      for (int k1 = 0; k1 < 4; ++k1) y[n2][k1] = t[k1];
+    }
+    // W16^e = exp(-2 pi i e / 16) for e = n2*k1 in {1,2,3,4,6,9}
+    y[1][1] = cmul(y[1][1], make_double2(c1, -s1));
+    y[1][2] = cmul(y[1][2], make_double2(h, -h));
+    y[1][3] = cmul(y[1][3], make_double2(s1, -c1));
+    y[2][1] = cmul(y[2][1], make_double2(h, -h));
+    y[2][2] = cmul_mi(y[2][2]);
+    y[2][3] = cmul(y[2][3], make_double2(-h, -h));
+    y[3][1] = cmul(y[3][1], make_double2(s1, -c1));
+    y[3][2] = cmul(y[3][2], make_double2(-h, -h));
+    y[3][3] = cmul(y[3][3], make_double2(-c1, s1));
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      double2 t[4] = {y[0][k1], y[1][k1], y[2][k1], y[3][k1]};
+      Dft<4>::run(t);
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) x[k1 + 4 * k2] = t[k2];
+    }
+  }
+};
+
 // generic odd radix via the symmetric real-pair formulation
 template <int R>
 struct DftOdd {
@@ -132,32 +166,56 @@ struct Dft<7> : DftOdd<7> {};
 // DIF stage (natural -> reversed): twiddle after the butterfly.
 // DIT stage (reversed -> natural): twiddle before the butterfly.
 // Butterfly q = g*S + j touches elements g*R*S + j + r*S, r < R; its twiddle
-// for leg r is W_n^{r*j*G} with G = n/(R*S).
+// for leg r is W_n^{r*j*G} with G = n/(R*S).  One table load per butterfly
+// (w = W_n^{j*G}); leg r uses w^r by running multiplication (<= 15 roundings,
+// ~2e-15 relative -- far inside the 1e-12 parity budget).
 template <int R, bool DIT>
 __device__ __forceinline__ void fft_stage(double2* s, int nb_log2, int S, int G,
                                           const double2* __restrict__ tw, int tid, int nthr) {
   const int nb = 1 << nb_log2;
   const int nbf = (G * S) << nb_log2;
-  for (int idx = tid; idx < nbf; idx += nthr) {
-    const int b = idx & (nb - 1);
-    const int q = idx >> nb_log2;
-    const int g = q / S;
-    const int j = q - g * S;
+  if (tid >= nbf) return;
+  // nthr is a multiple of nb, so the batch lane b is fixed per thread and the
+  // butterfly index q advances by dq = nthr/nb: update (g, j) incrementally
+  const int b = tid & (nb - 1);
+  int q = tid >> nb_log2;
+  const int dq = nthr >> nb_log2;
+  int g = q / S;
+  int j = q - g * S;
+  const int dg = dq / S, dj = dq - dg * S;
+  for (; q < (nbf >> nb_log2); q += dq) {
     const int base = g * R * S + j;
     double2 x[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = s[spad(((base + r * S) << nb_log2) + b)];
-    if (DIT && j != 0) {
+    const bool twid = j != 0;
+    double2 w1 = make_double2(1.0, 0.0);
+    if (twid) w1 = __ldg(tw + j * G);
+    if (DIT && twid) {
+      double2 wr = w1;
 #pragma unroll
-      for (int r = 1; r < R; ++r) x[r] = cmul(x[r], __ldg(tw + r * j * G));
+      for (int r = 1; r < R; ++r) {
+        x[r] = cmul(x[r], wr);
+        if (r + 1 < R) wr = cmul(wr, w1);
+      }
     }
     Dft<R>::run(x);
-    if (!DIT && j != 0) {
+    if (!DIT && twid) {
+      double2 wr = w1;
 #pragma unroll
-      for (int r = 1; r < R; ++r) x[r] = cmul(x[r], __ldg(tw + r * j * G));
+      for (int r = 1; r < R; ++r) {
+        x[r] = cmul(x[r], wr);
+        if (r + 1 < R) wr = cmul(wr, w1);
+      }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) s[spad(((base + r * S) << nb_log2) + b)] = x[r];
+    j += dj;
+    g += dg;
+    if (j >= S) {
+      j -= S;
+      ++g;
+    }
   }
 }
 
@@ -172,6 +230,7 @@ __device__ __forceinline__ void fft_stage_dispatch(int R, double2* s, int nb_log
     case 5: fft_stage<5, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
     case 7: fft_stage<7, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
     case 8: fft_stage<8, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
+    case 16: fft_stage<16, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
     default: break;
   }
 }

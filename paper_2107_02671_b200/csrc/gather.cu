@@ -23,28 +23,59 @@ struct GatherArgs {
   int batch;
 };
 
+constexpr int kGatherThreads = 256;
+constexpr int kGatherSpan = 2048;  // h values staged per CTA (32 KiB)
+
 template <int M>
-__global__ void __launch_bounds__(256) k_gather(GatherArgs a, WinCoef C) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= a.M2) return;
-  const int col = blockIdx.y;
-  const double pos = a.pos[j];
-  const double c = floor(pos);
-  const double d = pos - c;
-  double w[2 * M];
-  window_taps<M>(C, d, w);
-  const double2* h = a.h + (int64_t)col * a.Kout;
-  int64_t k0 = (int64_t)c + (1 - M) - a.s_lo;
+__device__ __forceinline__ double2 gather_dot(const double2* hp, const double* w) {
   double2 s = make_double2(0.0, 0.0);
-  if (k0 >= 0 && k0 + 2 * M <= a.Kout) {
-    const double2* hp = h + k0;
 #pragma unroll
-    for (int i = 0; i < 2 * M; ++i) {
-      const double2 v = __ldg(hp + i);
-      s.x = fma(v.x, w[i], s.x);
-      s.y = fma(v.y, w[i], s.y);
-    }
+  for (int i = 0; i < 2 * M; ++i) {
+    const double2 v = hp[i];
+    s.x = fma(v.x, w[i], s.x);
+    s.y = fma(v.y, w[i], s.y);
+  }
+  return s;
+}
+
+// One CTA = 256 consecutive sorted targets.  Their 2m-tap windows cover one
+// short contiguous range of h (targets are sorted); the CTA stages that range
+// in shared memory with coalesced loads, so each tap is an LDS (broadcast for
+// coincident targets) instead of a dependent global load.  CTAs whose range
+// exceeds kGatherSpan (sparse regions) or wraps around N2 read h directly.
+template <int M>
+__global__ void __launch_bounds__(kGatherThreads) k_gather(GatherArgs a, WinCoef C) {
+  __shared__ double2 hs[kGatherSpan];
+  const int64_t j0 = (int64_t)blockIdx.x * kGatherThreads;
+  const int64_t j = j0 + threadIdx.x;
+  const int64_t jl = min(j0 + kGatherThreads, a.M2) - 1;
+  const int col = blockIdx.y;
+  const bool act = j < a.M2;
+  double pos = 0.0, sc = 0.0;
+  if (act) {
+    pos = __ldg(a.pos + j);
+    sc = __ldg(a.scale + j);
+  }
+  const double2* h = a.h + (int64_t)col * a.Kout;
+  const int64_t klo = (int64_t)floor(__ldg(a.pos + j0)) + (1 - M) - a.s_lo;
+  const int64_t khi = (int64_t)floor(__ldg(a.pos + jl)) + M - a.s_lo;
+  const bool staged = klo >= 0 && khi < a.Kout && khi - klo + 1 <= kGatherSpan;
+  if (staged) {
+    for (int64_t i = threadIdx.x; i <= khi - klo; i += kGatherThreads) hs[i] = __ldg(h + klo + i);
+    __syncthreads();
+  }
+  if (!act) return;
+  const double c = floor(pos);
+  double w[2 * M];
+  window_taps<M>(C, pos - c, w);
+  const int64_t k0 = (int64_t)c + (1 - M) - a.s_lo;
+  double2 s;
+  if (staged) {
+    s = gather_dot<M>(hs + (k0 - klo), w);
+  } else if (k0 >= 0 && k0 + 2 * M <= a.Kout) {
+    s = gather_dot<M>(h + k0, w);
   } else {  // periodic wrap (only when Kout == N2 covers every residue)
+    s = make_double2(0.0, 0.0);
 #pragma unroll
     for (int i = 0; i < 2 * M; ++i) {
       int64_t k = (k0 + i) % a.N2;
@@ -54,26 +85,42 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a, WinCoef C) {
       s.y = fma(v.y, w[i], s.y);
     }
   }
-  const double sc = a.scale[j];
-  a.out[(int64_t)a.perm[j] * a.batch + col] = make_double2(s.x * sc, s.y * sc);
+  a.out[j * a.batch + col] = make_double2(s.x * sc, s.y * sc);  // sorted order, coalesced
+}
+
+// out[i] = sorted[inv[i]]: coalesced stores, random 16-byte loads (a scatter
+// of the sorted results would instead force partial-sector read-modify-write
+// traffic in L2/DRAM for every 16-byte store)
+__global__ void __launch_bounds__(256) k_unpermute(const double2* __restrict__ sorted,
+                                                   const int* __restrict__ inv, double2* out,
+                                                   int64_t n, int batch) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t src = (int64_t)__ldg(inv + i) * batch;
+  for (int b = 0; b < batch; ++b) out[i * batch + b] = __ldg(sorted + src + b);
 }
 
 void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batch,
                 cudaStream_t s) {
-  GatherArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, h,          out,
+  Scratch sorted(sizeof(double2) * (size_t)p.g.M2 * batch, s);
+  GatherArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, h,          sorted.as<double2>(),
                p.g.M2,     p.fft.Kout,  p.g.N2,        p.fft.s_lo, batch};
-  const dim3 grid((unsigned)ceil_div(p.g.M2, 256), batch);
+  const dim3 grid((unsigned)ceil_div(p.g.M2, kGatherThreads), batch);
   switch (p.g.m2) {
 #define SF_CASE(MM)                                          \
   case MM:                                                   \
-    k_gather<MM><<<grid, 256, 0, s>>>(a, p.c2);              \
-    SF_LAUNCH_CHECK();                                       \
-    return;
+    k_gather<MM><<<grid, kGatherThreads, 0, s>>>(a, p.c2);  \
+    break;
     SF_CASE(2) SF_CASE(3) SF_CASE(4) SF_CASE(5) SF_CASE(6) SF_CASE(7) SF_CASE(8) SF_CASE(9)
     SF_CASE(10) SF_CASE(11) SF_CASE(12) SF_CASE(13) SF_CASE(14) SF_CASE(15) SF_CASE(16)
 #undef SF_CASE
+    default:
+      fail(5, "unsupported m2");
   }
-  fail(5, "unsupported m2");
+  SF_LAUNCH_CHECK();
+  k_unpermute<<<(unsigned)ceil_div(p.g.M2, 256), 256, 0, s>>>(sorted.as<double2>(), p.gp.inv.p,
+                                                              out, p.g.M2, batch);
+  SF_LAUNCH_CHECK();
 }
 
 }  // namespace sfb

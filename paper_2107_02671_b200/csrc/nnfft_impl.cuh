@@ -50,6 +50,7 @@ struct SpreadPlan {
 struct GatherPlan {
   DevArray<double> pos;
   DevArray<int> perm;
+  DevArray<int> inv;      // inv[perm[j]] = j
   DevArray<double> scale;
 };
 
@@ -98,6 +99,8 @@ void run_spread(const NnfftPlanImpl& p, const double2* f, double2* grid, int bat
                 cudaStream_t stream);
 // real-valued coefficients (fast sinc input), batch 1
 void run_spread_real(const NnfftPlanImpl& p, const double* f, double2* grid, cudaStream_t stream);
+// out: (M2, batch) row-major, original target order.  Two kernels: windowed
+// interpolation in sorted order into a scratch, then the permutation back.
 void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batch,
                 cudaStream_t stream);
 

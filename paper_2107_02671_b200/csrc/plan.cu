@@ -201,6 +201,11 @@ __global__ void k_hat2(double* hat2, int64_t K, double beta2, int m2, int64_t N2
   if (!(h > 0.0)) atomicAdd(bad, 1ull);
 }
 
+__global__ void k_invert(const int* perm, int64_t n, int* inv) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) inv[perm[j]] = (int)j;
+}
+
 __global__ void k_mul_scale(double* scale, const int* perm, const double* w, int64_t n) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j < n) scale[j] *= w[perm[j]];
@@ -372,6 +377,9 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
     }
     p.gp.pos.alloc(M2);
     p.gp.scale.alloc(M2);
+    p.gp.inv.alloc(M2);
+    k_invert<<<blocks(M2), 256, 0, s>>>(p.gp.perm.p, M2, p.gp.inv.p);
+    SF_LAUNCH_CHECK();
     Scratch bad(sizeof(unsigned long long), s);
     SF_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
     k_tgt_tables<<<blocks(M2), 256, 0, s>>>(p.x_clip.p, p.gp.perm.p, M2, ratio, (double)g.N2,

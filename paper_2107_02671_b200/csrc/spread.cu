@@ -33,7 +33,7 @@ struct SpreadArgs {
 };
 
 template <int M, bool REAL>
-__global__ void __launch_bounds__(kSpreadThreads) k_spread(SpreadArgs a, WinCoef C) {
+__global__ void __launch_bounds__(kSpreadThreads, 2) k_spread(SpreadArgs a, WinCoef C) {
   constexpr int SPAN = kTile + 2 * M - 1;
   extern __shared__ double2 acc[];
   const int lane = threadIdx.x & 31;
@@ -49,32 +49,35 @@ __global__ void __launch_bounds__(kSpreadThreads) k_spread(SpreadArgs a, WinCoef
     const bool valid = ci < u.z;
     int start = 0, cnt = 0, lcell = 0;
     if (valid) {
-      const int2 d = a.chunks[ci];
+      const int2 d = __ldg(a.chunks + ci);
       start = d.x;
       cnt = d.y & 255;
       lcell = d.y >> 8;
     }
+    // issue every load of the chunk before any math: the f gather is a
+    // random DRAM access per source and must not serialise with the windows
+    double pos[kChunk];
+    double2 fv[kChunk];
+#pragma unroll
+    for (int s = 0; s < kChunk; ++s) {
+      pos[s] = 0.0;
+      fv[s] = make_double2(0.0, 0.0);
+      if (s < cnt) {
+        pos[s] = __ldg(a.pos + start + s);
+        const int src = __ldg(a.perm + start + s);
+        if (REAL) {
+          fv[s].x = __ldg(static_cast<const double*>(a.f) + src);
+        } else {
+          fv[s] = __ldg(static_cast<const double2*>(a.f) + (int64_t)src * a.batch + col);
+        }
+      }
+    }
     double2 r[2 * M];
 #pragma unroll
     for (int i = 0; i < 2 * M; ++i) r[i] = make_double2(0.0, 0.0);
-    for (int s = 0; s < cnt; ++s) {
-      const int j = start + s;
-      const double pos = a.pos[j];
-      const int src = a.perm[j];
-      double2 fv;
-      if (REAL) {
-        fv = make_double2(static_cast<const double*>(a.f)[src], 0.0);
-      } else {
-        fv = static_cast<const double2*>(a.f)[(int64_t)src * a.batch + col];
-      }
-      const double d = pos - floor(pos);
-      double w[2 * M];
-      window_taps<M>(C, d, w);
 #pragma unroll
-      for (int i = 0; i < 2 * M; ++i) {
-        r[i].x = fma(fv.x, w[i], r[i].x);
-        if (!REAL) r[i].y = fma(fv.y, w[i], r[i].y);
-      }
+    for (int s = 0; s < kChunk; ++s) {
+      if (s < cnt) window_accumulate<M, REAL>(C, pos[s] - floor(pos[s]), fv[s], r);
     }
     // add into the warp-private tile accumulator; equal cells in one warp
     // would race, so leaders of each cell group go first, round by round

@@ -76,6 +76,42 @@ __host__ __device__ __forceinline__ void window_taps(const WinCoef& C, double d,
   }
 }
 
+// Accumulate f * g_t(d) into r[t + M - 1] for all 2M taps, consuming each tap
+// pair as soon as it is formed (keeps the live register set small).
+template <int M, bool REAL>
+__device__ __forceinline__ void window_accumulate(const WinCoef& C, double d, double2 fv,
+                                                  double2* r) {
+  constexpr int P = window_degree(M);
+  constexpr int NE = P / 2 + 1;
+  constexpr int NO = (P + 1) / 2;
+  const double u = 2.0 * d - 1.0;
+  const double u2 = u * u;
+  const double sq_hi = sqrt(d), sq_lo = sqrt(1.0 - d);
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    double E = C.e[q][NE - 1];
+#pragma unroll
+    for (int k = NE - 2; k >= 0; --k) E = fma(E, u2, C.e[q][k]);
+    double O = C.o[q][NO - 1];
+#pragma unroll
+    for (int k = NO - 2; k >= 0; --k) O = fma(O, u2, C.o[q][k]);
+    double hi = fma(u, O, E);
+    double lo = fma(-u, O, E);
+    const int ih = (q < M - 1) ? M + q : 2 * M - 1;
+    const int il = (q < M - 1) ? M - 1 - q : 0;
+    if (q == M - 1) {
+      hi *= sq_hi;
+      lo *= sq_lo;
+    }
+    r[ih].x = fma(fv.x, hi, r[ih].x);
+    r[il].x = fma(fv.x, lo, r[il].x);
+    if (!REAL) {
+      r[ih].y = fma(fv.y, hi, r[ih].y);
+      r[il].y = fma(fv.y, lo, r[il].y);
+    }
+  }
+}
+
 // Fourier transform of the sinh shape function, omega_hat(v)
 // (windows.py:143-160), all three branches; on the NNFFT path only the
 // w > 1e-3 branch is reachable.
