@@ -4,11 +4,14 @@
 // Reference (pkg/src/sincfft/nnfft.py:198-205, 241-243):
 //     out_j = sum_{t=1-m2}^{m2} h[(c_j + t) mod N2] phi_2(xs_j - (c_j+t)/N2)
 //             / phi_hat_1(N x_j),   xs_j = x_j N/N1, c_j = floor(N2 xs_j).
-// Targets are sorted by position at plan time, so a warp reads one short,
-// contiguous window of h (L1-resident); the 2m2 window values come from the
-// per-tap polynomials (window.cuh); the scale 1/phi_hat_1 (times the
-// Clenshaw-Curtis weight for fast-sinc stage 1) is one sorted fp64 stream;
-// the result is stored to the target's original index.
+// Targets are sorted at plan time by (slice of the original index, position):
+// within a slice a CTA's targets read one short contiguous window of h (staged
+// in shared memory), and its outputs -- stored to the targets' original
+// indices -- all fall in the slice's window of `out`, small enough to stay
+// L2-resident so the scattered 16-byte stores merge into full sectors.  The
+// 2m2 window values come from the per-tap polynomials (window.cuh); the scale
+// 1/phi_hat_1 (times the Clenshaw-Curtis weight for fast-sinc stage 1) is one
+// sorted fp64 stream.
 #include "nnfft_impl.cuh"
 
 namespace sfb {
@@ -38,8 +41,8 @@ __device__ __forceinline__ double2 gather_dot(const double2* hp, const double* w
   return s;
 }
 
-// One CTA = 256 consecutive sorted targets.  Their 2m-tap windows cover one
-// short contiguous range of h (targets are sorted); the CTA stages that range
+// One CTA = 256 consecutive sorted targets of one slice.  Their 2m-tap windows
+// cover one short contiguous range of h; the CTA stages that range
 // in shared memory with coalesced loads, so each tap is an LDS (broadcast for
 // coincident targets) instead of a dependent global load.  CTAs whose range
 // exceeds kGatherSpan (sparse regions) or wraps around N2 read h directly.
@@ -52,9 +55,11 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherArgs a, WinCoef
   const int col = blockIdx.y;
   const bool act = j < a.M2;
   double pos = 0.0, sc = 0.0;
+  int dst = 0;
   if (act) {
     pos = __ldg(a.pos + j);
     sc = __ldg(a.scale + j);
+    dst = __ldg(a.perm + j);
   }
   const double2* h = a.h + (int64_t)col * a.Kout;
   const int64_t klo = (int64_t)floor(__ldg(a.pos + j0)) + (1 - M) - a.s_lo;
@@ -85,25 +90,15 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherArgs a, WinCoef
       s.y = fma(v.y, w[i], s.y);
     }
   }
-  a.out[j * a.batch + col] = make_double2(s.x * sc, s.y * sc);  // sorted order, coalesced
-}
-
-// out[i] = sorted[inv[i]]: coalesced stores, random 16-byte loads (a scatter
-// of the sorted results would instead force partial-sector read-modify-write
-// traffic in L2/DRAM for every 16-byte store)
-__global__ void __launch_bounds__(256) k_unpermute(const double2* __restrict__ sorted,
-                                                   const int* __restrict__ inv, double2* out,
-                                                   int64_t n, int batch) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t src = (int64_t)__ldg(inv + i) * batch;
-  for (int b = 0; b < batch; ++b) out[i * batch + b] = __ldg(sorted + src + b);
+  // scattered store, but inside this slice's window of `out` (the plan sorts
+  // targets by (original-index slice, position)), which stays L2-resident, so
+  // both 16-byte halves of each 32-byte sector merge in L2 before eviction
+  a.out[(int64_t)dst * a.batch + col] = make_double2(s.x * sc, s.y * sc);
 }
 
 void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batch,
                 cudaStream_t s) {
-  Scratch sorted(sizeof(double2) * (size_t)p.g.M2 * batch, s);
-  GatherArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, h,          sorted.as<double2>(),
+  GatherArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, h,          out,
                p.g.M2,     p.fft.Kout,  p.g.N2,        p.fft.s_lo, batch};
   const dim3 grid((unsigned)ceil_div(p.g.M2, kGatherThreads), batch);
   switch (p.g.m2) {
@@ -117,9 +112,6 @@ void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batc
     default:
       fail(5, "unsupported m2");
   }
-  SF_LAUNCH_CHECK();
-  k_unpermute<<<(unsigned)ceil_div(p.g.M2, 256), 256, 0, s>>>(sorted.as<double2>(), p.gp.inv.p,
-                                                              out, p.g.M2, batch);
   SF_LAUNCH_CHECK();
 }
 

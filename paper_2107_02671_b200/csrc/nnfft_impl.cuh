@@ -47,10 +47,16 @@ struct SpreadPlan {
 // Targets sorted by fl(N2 * xs); scale = 1/phi_hat_1(N x_j) in sorted order
 // (optionally times an external per-target weight, used by the fast sinc
 // transform to fuse alpha = w * g into stage 1).
+// Targets are sorted by (j / kGatherSlice, fine-grid cell): slices of
+// kGatherSlice original indices keep each CTA's scattered output stores inside
+// a 16 MiB window of `out` (L2-resident; 2^20 measured best of 2^18..2^23).  kGatherSlice is a multiple of the
+// gather CTA size, so no CTA straddles two slices.
+constexpr int64_t kGatherSliceDefault = (int64_t)1 << 20;
+int64_t gather_slice();  // kGatherSliceDefault unless SFB_GATHER_SLICE_LOG2 is set (tuning)
+
 struct GatherPlan {
   DevArray<double> pos;
   DevArray<int> perm;
-  DevArray<int> inv;      // inv[perm[j]] = j
   DevArray<double> scale;
 };
 
@@ -99,8 +105,7 @@ void run_spread(const NnfftPlanImpl& p, const double2* f, double2* grid, int bat
                 cudaStream_t stream);
 // real-valued coefficients (fast sinc input), batch 1
 void run_spread_real(const NnfftPlanImpl& p, const double* f, double2* grid, cudaStream_t stream);
-// out: (M2, batch) row-major, original target order.  Two kernels: windowed
-// interpolation in sorted order into a scratch, then the permutation back.
+// out: (M2, batch) row-major, original target order.
 void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batch,
                 cudaStream_t stream);
 

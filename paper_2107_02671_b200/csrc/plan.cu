@@ -6,6 +6,8 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstring>
+#include <cstdlib>
 #include <string>
 
 #include "nnfft_impl.cuh"
@@ -169,13 +171,21 @@ __global__ void k_unit_emit(const int* tstart, const int* nu, const int* off, in
   }
 }
 
-// target keys: floor(N2 * xs) + N2 with xs = x * (N/N1)  (nnfft.py:200-201)
+// target keys: (original-index slice, floor(N2 * xs) + N2), xs = x * (N/N1)
+// (nnfft.py:200-201)
+int64_t gather_slice() {
+  const char* e = getenv("SFB_GATHER_SLICE_LOG2");
+  if (e && atoi(e) >= 8 && atoi(e) <= 30) return (int64_t)1 << atoi(e);
+  return kGatherSliceDefault;
+}
+
 __global__ void k_tgt_keys(const double* x, int64_t n, double ratio, double N2d, int64_t N2,
-                           unsigned* key, int* idx) {
+                           int cell_bits, int64_t slice, unsigned long long* key, int* idx) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double xs = x[i] * ratio;
-  key[i] = (unsigned)((int64_t)floor(N2d * xs) + N2);
+  const unsigned long long cell = (unsigned long long)((int64_t)floor(N2d * xs) + N2);
+  key[i] = ((unsigned long long)(i / slice) << cell_bits) | cell;
   idx[i] = (int)i;
 }
 
@@ -201,11 +211,6 @@ __global__ void k_hat2(double* hat2, int64_t K, double beta2, int m2, int64_t N2
   if (!(h > 0.0)) atomicAdd(bad, 1ull);
 }
 
-__global__ void k_invert(const int* perm, int64_t n, int* inv) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j < n) inv[perm[j]] = (int)j;
-}
-
 __global__ void k_mul_scale(double* scale, const int* perm, const double* w, int64_t n) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j < n) scale[j] *= w[perm[j]];
@@ -227,6 +232,51 @@ double device_absmax(const double* a, int64_t n, cudaStream_t s) {
   double m;
   std::memcpy(&m, &bits, sizeof(m));
   return m;
+}
+
+// min / max of a device array (order-preserving integer keys for doubles)
+__device__ __forceinline__ unsigned long long order_key(double d) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void k_minmax(const double* a, int64_t n, unsigned long long* mn,
+                         unsigned long long* mx) {
+  double lo = INFINITY, hi = -INFINITY;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    lo = fmin(lo, a[i]);
+    hi = fmax(hi, a[i]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mn, order_key(lo));
+    atomicMax(mx, order_key(hi));
+  }
+}
+
+double from_order_key(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  double d;
+  std::memcpy(&d, &b, sizeof d);
+  return d;
+}
+
+void device_minmax(const double* a, int64_t n, cudaStream_t s, double* lo, double* hi) {
+  Scratch r(2 * sizeof(unsigned long long), s);
+  const unsigned long long init[2] = {~0ull, 0ull};
+  SF_CUDA(cudaMemcpyAsync(r.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  k_minmax<<<std::min<unsigned>(blocks(n), 1024), 256, 0, s>>>(
+      a, n, r.as<unsigned long long>(), r.as<unsigned long long>() + 1);
+  SF_LAUNCH_CHECK();
+  unsigned long long out[2];
+  SF_CUDA(cudaMemcpyAsync(out, r.p, sizeof(out), cudaMemcpyDeviceToHost, s));
+  SF_CUDA(cudaStreamSynchronize(s));
+  *lo = from_order_key(out[0]);
+  *hi = from_order_key(out[1]);
 }
 
 int key_bits(uint64_t maxkey) {
@@ -356,30 +406,32 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
     SF_CUDA(cudaStreamSynchronize(s));
   }
 
-  // --- targets: sort by fine-grid cell, 1/phi_hat_1, output window [s_lo, s_hi]
+  // --- targets: sort by (original-index slice, fine-grid cell), 1/phi_hat_1,
+  //     and the output window [s_lo, s_hi] the gather reads
   {
     const int64_t M2 = g.M2;
     const double ratio = (double)g.N / (double)g.N1;  // x/sigma1 (nnfft.py:200)
-    Scratch kin(sizeof(unsigned) * M2, s), kout(sizeof(unsigned) * M2, s);
+    Scratch kin(sizeof(unsigned long long) * M2, s), kout(sizeof(unsigned long long) * M2, s);
     Scratch iin(sizeof(int) * M2, s);
     p.gp.perm.alloc(M2);
-    k_tgt_keys<<<blocks(M2), 256, 0, s>>>(p.x_clip.p, M2, ratio, (double)g.N2, g.N2,
-                                          kin.as<unsigned>(), iin.as<int>());
+    const int cbits = key_bits((uint64_t)(2 * g.N2 + 2));
+    const int64_t slice = gather_slice();
+    k_tgt_keys<<<blocks(M2), 256, 0, s>>>(p.x_clip.p, M2, ratio, (double)g.N2, g.N2, cbits, slice,
+                                          kin.as<unsigned long long>(), iin.as<int>());
     SF_LAUNCH_CHECK();
     size_t tb = 0;
-    const int bits = key_bits((uint64_t)(2 * g.N2 + 2));
-    SF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.as<unsigned>(), kout.as<unsigned>(),
-                                            iin.as<int>(), p.gp.perm.p, (int)M2, 0, bits, s));
+    const int bits = cbits + key_bits((uint64_t)((M2 - 1) / slice));
+    SF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.as<unsigned long long>(),
+                                            kout.as<unsigned long long>(), iin.as<int>(),
+                                            p.gp.perm.p, (int)M2, 0, bits, s));
     {
       Scratch t(tb, s);
-      SF_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kin.as<unsigned>(), kout.as<unsigned>(),
-                                              iin.as<int>(), p.gp.perm.p, (int)M2, 0, bits, s));
+      SF_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tb, kin.as<unsigned long long>(),
+                                              kout.as<unsigned long long>(), iin.as<int>(),
+                                              p.gp.perm.p, (int)M2, 0, bits, s));
     }
     p.gp.pos.alloc(M2);
     p.gp.scale.alloc(M2);
-    p.gp.inv.alloc(M2);
-    k_invert<<<blocks(M2), 256, 0, s>>>(p.gp.perm.p, M2, p.gp.inv.p);
-    SF_LAUNCH_CHECK();
     Scratch bad(sizeof(unsigned long long), s);
     SF_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
     k_tgt_tables<<<blocks(M2), 256, 0, s>>>(p.x_clip.p, p.gp.perm.p, M2, ratio, (double)g.N2,
@@ -388,8 +440,8 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
     SF_LAUNCH_CHECK();
     if (read1(bad.as<unsigned long long>(), s))
       fail(2, "nnfft_plan: phi_hat_1(N x_j) must be strictly positive at every node");
-    const double plo = read1(p.gp.pos.p, s);
-    const double phi = read1(p.gp.pos.p + (M2 - 1), s);
+    double plo, phi;
+    device_minmax(p.gp.pos.p, M2, s, &plo, &phi);
     const int64_t s_lo = (int64_t)std::floor(plo) + 1 - g.m2;
     const int64_t s_hi = (int64_t)std::floor(phi) + g.m2;
     p.fft.s_lo = s_lo;
