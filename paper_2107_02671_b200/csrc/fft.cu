@@ -117,36 +117,66 @@ struct FftArgs {
   FftStages st1, st2;
 };
 
+// Global <-> shared copies are issued kU elements per thread at a time so
+// that kU independent loads are in flight before the first dependent store
+// (a plain strided loop serialises one DRAM latency per element).
+constexpr int kU = 8;
+
 template <int MODE>
 __global__ void __launch_bounds__(512) k_single(FftArgs a, int spectrum) {
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int L = (int)a.L;
+  const int T = blockDim.x;
   const double2* g = a.g + (int64_t)col * (MODE == IN_GP ? a.K : 0);
-  for (int i = threadIdx.x; i < L; i += blockDim.x) {
-    double2 v = make_double2(0.0, 0.0);
-    if (MODE == IN_GP) {
-      if (i < a.K) v = cmul(g[i], a.P[i]);
-    } else {
-      v = g[i];
+  for (int i0 = threadIdx.x; i0 < L; i0 += kU * T) {
+    double2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * T;
+      v[u] = make_double2(0.0, 0.0);
+      if (MODE == IN_GP) {
+        if (i < a.K) v[u] = cmul(__ldg(g + i), __ldg(a.P + i));
+      } else if (i < L) {
+        v[u] = __ldg(g + i);
+      }
     }
-    sm[spad(i)] = v;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * T < L) sm[spad(i0 + u * T)] = v[u];
   }
   __syncthreads();
   fft_dif(sm, 0, a.st1, a.tw1);
   if (spectrum) {
     const double inv = 1.0 / (double)L;
-    for (int i = threadIdx.x; i < L; i += blockDim.x)
-      a.Y[i] = cscale(sm[spad(i)], inv);
+    for (int i = threadIdx.x; i < L; i += T) a.Y[i] = cscale(sm[spad(i)], inv);
     return;
   }
-  for (int i = threadIdx.x; i < L; i += blockDim.x)
-    sm[spad(i)] = cconj(cmul(sm[spad(i)], __ldg(a.Bhat + i)));
+  for (int i0 = threadIdx.x; i0 < L; i0 += kU * T) {
+    double2 bv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * T < L) bv[u] = __ldg(a.Bhat + i0 + u * T);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * T;
+      if (i < L) sm[spad(i)] = cconj(cmul(sm[spad(i)], bv[u]));
+    }
+  }
   __syncthreads();
   fft_dit(sm, 0, a.st1, a.tw1);
   double2* h = a.h + (int64_t)col * a.Kout;
-  for (int k = threadIdx.x; k < a.Kout; k += blockDim.x)
-    h[k] = cmul(cconj(sm[spad(k)]), __ldg(a.Q + k));
+  for (int k0 = threadIdx.x; k0 < a.Kout; k0 += kU * T) {
+    double2 qv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (k0 + u * T < a.Kout) qv[u] = __ldg(a.Q + k0 + u * T);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int k = k0 + u * T;
+      if (k < a.Kout) h[k] = cmul(cconj(sm[spad(k)]), qv[u]);
+    }
+  }
 }
 
 template <int MODE>
@@ -157,32 +187,45 @@ __global__ void __launch_bounds__(256) k_colfwd(FftArgs a) {
   const int64_t c0 = (int64_t)blockIdx.x * C;
   const int L2 = (int)a.L2;
   const int n_el = L2 << a.C_log2;
+  const int T = blockDim.x;
   const double2* g = a.g + (int64_t)col * (MODE == IN_GP ? a.K : 0);
-  for (int e = threadIdx.x; e < n_el; e += blockDim.x) {
-    const int b = e & (C - 1);
-    const int n2 = e >> a.C_log2;
-    const int64_t n1 = c0 + b;
-    double2 v = make_double2(0.0, 0.0);
-    if (n1 < a.L1) {
-      const int64_t n = n1 + a.L1 * n2;
-      if (MODE == IN_GP) {
-        if (n < a.K) v = cmul(g[n], a.P[n]);
-      } else {
-        v = g[n];
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int64_t n1 = c0 + (e & (C - 1));
+      const int64_t n = n1 + a.L1 * (e >> a.C_log2);
+      v[u] = make_double2(0.0, 0.0);
+      if (e < n_el && n1 < a.L1) {
+        if (MODE == IN_GP) {
+          if (n < a.K) v[u] = cmul(__ldg(g + n), __ldg(a.P + n));
+        } else {
+          v[u] = __ldg(g + n);
+        }
       }
     }
-    sm[spad(e)] = v;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = v[u];
   }
   __syncthreads();
   fft_dif(sm, a.C_log2, a.st2, a.tw2);
   double2* Y = a.Y + (int64_t)col * a.L;
-  for (int e = threadIdx.x; e < n_el; e += blockDim.x) {
-    const int b = e & (C - 1);
-    const int p = e >> a.C_log2;
-    const int64_t n1 = c0 + b;
-    if (n1 < a.L1) {
-      const int64_t k2 = a.rev2[p];
-      Y[n1 + a.L1 * p] = cmul(sm[spad(e)], wbig(a.tw_lo, a.tw_hi, n1 * k2));
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 w[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int64_t n1 = c0 + (e & (C - 1));
+      w[u] = make_double2(1.0, 0.0);
+      if (e < n_el && n1 < a.L1) w[u] = wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)__ldg(a.rev2 + (e >> a.C_log2)));
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int64_t n1 = c0 + (e & (C - 1));
+      if (e < n_el && n1 < a.L1) Y[n1 + a.L1 * (e >> a.C_log2)] = cmul(sm[spad(e)], w[u]);
     }
   }
 }
@@ -192,21 +235,39 @@ __global__ void __launch_bounds__(256) k_rowmul(FftArgs a, int spectrum) {
   const int col = blockIdx.y;
   const int64_t p = blockIdx.x;
   const int L1 = (int)a.L1;
+  const int T = blockDim.x;
   double2* row = a.Y + (int64_t)col * a.L + p * a.L1;
-  for (int i = threadIdx.x; i < L1; i += blockDim.x) sm[spad(i)] = row[i];
+  for (int i0 = threadIdx.x; i0 < L1; i0 += kU * T) {
+    double2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * T < L1) v[u] = row[i0 + u * T];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * T < L1) sm[spad(i0 + u * T)] = v[u];
+  }
   __syncthreads();
   fft_dif(sm, 0, a.st1, a.tw1);
   const double2* B = a.Bhat + p * a.L1;
   if (spectrum) {
     const double inv = 1.0 / (double)a.L;
-    for (int i = threadIdx.x; i < L1; i += blockDim.x) row[i] = cscale(sm[spad(i)], inv);
+    for (int i = threadIdx.x; i < L1; i += T) row[i] = cscale(sm[spad(i)], inv);
     return;
   }
-  for (int i = threadIdx.x; i < L1; i += blockDim.x)
-    sm[spad(i)] = cconj(cmul(sm[spad(i)], __ldg(B + i)));
+  for (int i0 = threadIdx.x; i0 < L1; i0 += kU * T) {
+    double2 bv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * T < L1) bv[u] = __ldg(B + i0 + u * T);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * T;
+      if (i < L1) sm[spad(i)] = cconj(cmul(sm[spad(i)], bv[u]));
+    }
+  }
   __syncthreads();
   fft_dit(sm, 0, a.st1, a.tw1);
-  for (int i = threadIdx.x; i < L1; i += blockDim.x) row[i] = cconj(sm[spad(i)]);
+  for (int i = threadIdx.x; i < L1; i += T) row[i] = cconj(sm[spad(i)]);
 }
 
 __global__ void __launch_bounds__(256) k_colinv(FftArgs a) {
@@ -216,27 +277,45 @@ __global__ void __launch_bounds__(256) k_colinv(FftArgs a) {
   const int64_t c0 = (int64_t)blockIdx.x * C;
   const int L2 = (int)a.L2;
   const int n_el = L2 << a.C_log2;
+  const int T = blockDim.x;
   const double2* Y = a.Y + (int64_t)col * a.L;
-  for (int e = threadIdx.x; e < n_el; e += blockDim.x) {
-    const int b = e & (C - 1);
-    const int p = e >> a.C_log2;
-    const int64_t n1 = c0 + b;
-    double2 v = make_double2(0.0, 0.0);
-    if (n1 < a.L1) {
-      const int64_t k2 = a.rev2[p];
-      v = cmul(cconj(Y[n1 + a.L1 * p]), wbig(a.tw_lo, a.tw_hi, n1 * k2));
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 v[kU], w[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int64_t n1 = c0 + (e & (C - 1));
+      const int p = e >> a.C_log2;
+      v[u] = make_double2(0.0, 0.0);
+      w[u] = make_double2(1.0, 0.0);
+      if (e < n_el && n1 < a.L1) {
+        v[u] = Y[n1 + a.L1 * p];
+        w[u] = wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)__ldg(a.rev2 + p));
+      }
     }
-    sm[spad(e)] = v;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = cmul(cconj(v[u]), w[u]);
   }
   __syncthreads();
   fft_dit(sm, a.C_log2, a.st2, a.tw2);
   double2* h = a.h + (int64_t)col * a.Kout;
-  for (int e = threadIdx.x; e < n_el; e += blockDim.x) {
-    const int b = e & (C - 1);
-    const int n2 = e >> a.C_log2;
-    const int64_t n1 = c0 + b;
-    const int64_t k = n1 + a.L1 * n2;
-    if (n1 < a.L1 && k < a.Kout) h[k] = cmul(cconj(sm[spad(e)]), __ldg(a.Q + k));
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 qv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int64_t k = c0 + (e & (C - 1)) + a.L1 * (e >> a.C_log2);
+      qv[u] = make_double2(0.0, 0.0);
+      if (e < n_el && c0 + (e & (C - 1)) < a.L1 && k < a.Kout) qv[u] = __ldg(a.Q + k);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int64_t n1 = c0 + (e & (C - 1));
+      const int64_t k = n1 + a.L1 * (e >> a.C_log2);
+      if (e < n_el && n1 < a.L1 && k < a.Kout) h[k] = cmul(cconj(sm[spad(e)]), qv[u]);
+    }
   }
 }
 
@@ -268,7 +347,13 @@ FftStages make_stages(int64_t n) {
   if (r != 1) fail(3, "internal: non-smooth FFT length");
   if ((int)rad.size() > kMaxStages) fail(3, "internal: too many FFT stages");
   st.nst = (int)rad.size();
-  for (int i = 0; i < st.nst; ++i) st.rad[i] = rad[i];
+  int off = 0, S = (int)n;
+  for (int i = 0; i < st.nst; ++i) {
+    st.rad[i] = rad[i];
+    S /= rad[i];
+    st.toff[i] = off;
+    off += S;
+  }
   if (st.nst == 0) {  // n == 1: no stages
     st.nst = 0;
   }
@@ -321,6 +406,20 @@ double cost(int64_t L1, int64_t L2) {
   while (C > 1 && C * L2 > kColElems) C >>= 1;
   if (C < 8) c *= 1.0 + 0.12 * (C == 4 ? 1 : C == 2 ? 2 : 3);
   return c;
+}
+
+// compact per-stage twiddles of an n-point FFT: stage q holds W_n^{j*G_q}, j < S_q
+void launch_stage_twiddles(DevArray<double2>& t, const FftStages& st, cudaStream_t s) {
+  int64_t total = 0, S = st.n, G = 1;
+  for (int q = 0; q < st.nst; ++q) S /= st.rad[q], total += S;
+  t.alloc(std::max<int64_t>(total, 1));
+  S = st.n;
+  for (int q = 0; q < st.nst; ++q) {
+    S /= st.rad[q];
+    k_twiddle<<<(unsigned)ceil_div(S, 256), 256, 0, s>>>(t.p + st.toff[q], st.n, S, G);
+    SF_LAUNCH_CHECK();
+    G *= st.rad[q];
+  }
 }
 
 void launch_twiddle(DevArray<double2>& t, int64_t n, int64_t count, int64_t step,
@@ -398,9 +497,9 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   }
   f.st1 = make_stages(f.L1);
   f.st2 = make_stages(f.L2);
-  launch_twiddle(f.tw1, f.L1, f.L1, 1, s);
+  launch_stage_twiddles(f.tw1, f.st1, s);
   if (!f.single) {
-    launch_twiddle(f.tw2, f.L2, f.L2, 1, s);
+    launch_stage_twiddles(f.tw2, f.st2, s);
     launch_twiddle(f.tw_lo, f.L, kTwSplit, 1, s);
     launch_twiddle(f.tw_hi, f.L, ceil_div(f.L, kTwSplit) + 1, kTwSplit, s);
     std::vector<int> rev = digit_reverse(f.st2);

@@ -31,7 +31,8 @@ constexpr int kMaxStages = 24;
 struct FftStages {
   int n;
   int nst;
-  int rad[kMaxStages];  // DIF order; product == n
+  int rad[kMaxStages];   // DIF order; product == n
+  int toff[kMaxStages];  // offset of stage q's twiddles W_n^{j*G_q}, j < S_q, in the table
 };
 
 __device__ __forceinline__ int spad(int e) { return e + (e >> 3); }
@@ -166,9 +167,11 @@ struct Dft<7> : DftOdd<7> {};
 // DIF stage (natural -> reversed): twiddle after the butterfly.
 // DIT stage (reversed -> natural): twiddle before the butterfly.
 // Butterfly q = g*S + j touches elements g*R*S + j + r*S, r < R; its twiddle
-// for leg r is W_n^{r*j*G} with G = n/(R*S).  One table load per butterfly
-// (w = W_n^{j*G}); leg r uses w^r by running multiplication (<= 15 roundings,
-// ~2e-15 relative -- far inside the 1e-12 parity budget).
+// for leg r is W_n^{r*j*G} with G = n/(R*S).  One load per butterfly from a
+// compact per-stage table (w = W_n^{j*G} at tw[j]; all stages of an n-point
+// FFT need only ~n/15 distinct values, so the table stays L1-resident); leg r
+// uses w^r by running multiplication (<= 15 roundings, ~2e-15 relative -- far
+// inside the 1e-12 parity budget).
 template <int R, bool DIT>
 __device__ __forceinline__ void fft_stage(double2* s, int nb_log2, int S, int G,
                                           const double2* __restrict__ tw, int tid, int nthr) {
@@ -190,7 +193,7 @@ __device__ __forceinline__ void fft_stage(double2* s, int nb_log2, int S, int G,
     for (int r = 0; r < R; ++r) x[r] = s[spad(((base + r * S) << nb_log2) + b)];
     const bool twid = j != 0;
     double2 w1 = make_double2(1.0, 0.0);
-    if (twid) w1 = __ldg(tw + j * G);
+    if (twid) w1 = __ldg(tw + j);
     if (DIT && twid) {
       double2 wr = w1;
 #pragma unroll
@@ -243,7 +246,7 @@ __device__ __forceinline__ void fft_dif(double2* s, int nb_log2, const FftStages
   for (int q = 0; q < st.nst; ++q) {
     const int R = st.rad[q];
     S /= R;
-    fft_stage_dispatch<false>(R, s, nb_log2, S, G, tw, threadIdx.x, blockDim.x);
+    fft_stage_dispatch<false>(R, s, nb_log2, S, G, tw + st.toff[q], threadIdx.x, blockDim.x);
     __syncthreads();
     G *= R;
   }
@@ -255,7 +258,7 @@ __device__ __forceinline__ void fft_dit(double2* s, int nb_log2, const FftStages
   for (int q = st.nst - 1; q >= 0; --q) {
     const int R = st.rad[q];
     G /= R;
-    fft_stage_dispatch<true>(R, s, nb_log2, S, G, tw, threadIdx.x, blockDim.x);
+    fft_stage_dispatch<true>(R, s, nb_log2, S, G, tw + st.toff[q], threadIdx.x, blockDim.x);
     __syncthreads();
     S *= R;
   }
