@@ -89,6 +89,14 @@ struct DevArray {
   DevArray(const DevArray&) = delete;
   DevArray& operator=(const DevArray&) = delete;
   DevArray(DevArray&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DevArray& operator=(DevArray&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p, n = o.n;
+      o.p = nullptr, o.n = 0;
+    }
+    return *this;
+  }
 };
 
 }  // namespace sfb

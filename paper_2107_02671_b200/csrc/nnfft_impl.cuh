@@ -30,16 +30,20 @@ struct Geometry {
 // at most kChunk sources of one cell.  Chunks of a tile of kTile cells are
 // ordered rank-major (chunk rank within its cell, then cell), so a warp's 32
 // consecutive chunks almost always have pairwise distinct cells.  Work units
-// (one CTA each) are ranges of at most kUnitChunks chunks of one tile.
+// (one CTA each) are ranges of at most kUnitChunks chunks of one tile.  The
+// sources are stored in chunk-slot order (chunk c owns slots [4c, 4c+4)), so
+// a lane's positions and permutation load as two vectors without first
+// reading a descriptor.
 constexpr int kTile = 256;
 constexpr int kChunk = 4;
 constexpr int kUnitChunks = 1024;
 constexpr int kSpreadThreads = 256;
 
 struct SpreadPlan {
-  DevArray<double> pos;   // fl(N1 * v), sorted by cell     [M1]
-  DevArray<int> perm;     // original source index          [M1]
-  DevArray<int2> chunks;  // {first sorted index, (local cell << 8) | count}
+  DevArray<double> pos;   // fl(N1 * v) in chunk-slot order    [n_chunks * kChunk]
+  DevArray<int> perm;     // original source index, slot order [n_chunks * kChunk]
+  DevArray<int> info;     // (local cell << 8) | count          [n_chunks]
+  DevArray<int2> chunks;  // plan-time only: {first sorted index, info}
   DevArray<int4> units;   // {tile, chunk begin, chunk end, 0}
   int64_t n_chunks = 0, n_units = 0;
 };

@@ -141,6 +141,19 @@ __global__ void k_chunk_emit(const int* start, const int* nch, const int* off, i
   }
 }
 
+__global__ void k_chunk_slots(const int2* chunks, int64_t n, const double* pos, const int* perm,
+                              double* spos, int* sperm, int* info) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int2 d = chunks[c];
+  const int cnt = d.y & 255;
+  info[c] = d.y;
+  for (int s = 0; s < kChunk; ++s) {
+    spos[c * kChunk + s] = s < cnt ? pos[d.x + s] : 0.5;
+    sperm[c * kChunk + s] = s < cnt ? perm[d.x + s] : 0;
+  }
+}
+
 __global__ void k_tile_bounds(const unsigned long long* key, int64_t n, int64_t ntile,
                               int* tstart) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -403,7 +416,17 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
     k_unit_emit<<<blocks(ntile), 256, 0, s>>>(tstart.as<int>(), nu.as<int>(), uoff.as<int>(), ntile,
                                               p.sp.units.p);
     SF_LAUNCH_CHECK();
+    // re-lay the sorted sources out in chunk-slot order (kChunk slots per chunk)
+    DevArray<double> spos(nchunks * kChunk);
+    DevArray<int> sperm(nchunks * kChunk);
+    p.sp.info.alloc(nchunks);
+    k_chunk_slots<<<blocks(nchunks), 256, 0, s>>>(p.sp.chunks.p, nchunks, p.sp.pos.p, p.sp.perm.p,
+                                                  spos.p, sperm.p, p.sp.info.p);
+    SF_LAUNCH_CHECK();
     SF_CUDA(cudaStreamSynchronize(s));
+    p.sp.pos = std::move(spos);
+    p.sp.perm = std::move(sperm);
+    p.sp.chunks.release();
   }
 
   // --- targets: sort by (original-index slice, fine-grid cell), 1/phi_hat_1,

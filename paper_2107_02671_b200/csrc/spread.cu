@@ -22,15 +22,38 @@
 namespace sfb {
 
 struct SpreadArgs {
-  const double* pos;
-  const int* perm;
-  const int2* chunks;
+  const double* pos;    // slot order
+  const int* perm;      // slot order
+  const int* info;      // per chunk
   const int4* units;
   const void* f;        // complex (M1, batch) row-major, or real (M1)
   double2* grid;        // [batch][K]
   int64_t K;
   int batch;
 };
+
+static_assert(kChunk == 4, "slot loads assume 4 sources per chunk");
+
+struct ChunkLoad {
+  int info;
+  double2 p01, p23;  // positions of slots 0..3
+  int4 perm;
+};
+
+__device__ __forceinline__ ChunkLoad load_chunk(const SpreadArgs& a, int ci, bool valid) {
+  ChunkLoad c;
+  c.info = 0;
+  c.p01 = c.p23 = make_double2(0.5, 0.5);
+  c.perm = make_int4(0, 0, 0, 0);
+  if (valid) {
+    c.info = __ldg(a.info + ci);
+    const double2* pp = reinterpret_cast<const double2*>(a.pos) + 2 * (int64_t)ci;
+    c.p01 = __ldg(pp);
+    c.p23 = __ldg(pp + 1);
+    c.perm = __ldg(reinterpret_cast<const int4*>(a.perm) + ci);
+  }
+  return c;
+}
 
 template <int M, bool REAL>
 __global__ void __launch_bounds__(kSpreadThreads, 2) k_spread(SpreadArgs a, WinCoef C) {
@@ -44,34 +67,31 @@ __global__ void __launch_bounds__(kSpreadThreads, 2) k_spread(SpreadArgs a, WinC
   __syncthreads();
   double2* my = acc + warp * SPAN;
   const int4 u = a.units[blockIdx.x];
-  for (int cb = u.y + warp * 32; cb < u.z; cb += nwarp * 32) {
-    const int ci = cb + lane;
-    const bool valid = ci < u.z;
-    int start = 0, cnt = 0, lcell = 0;
-    if (valid) {
-      const int2 d = __ldg(a.chunks + ci);
-      start = d.x;
-      cnt = d.y & 255;
-      lcell = d.y >> 8;
-    }
-    // issue every load of the chunk before any math: the f gather is a
-    // random DRAM access per source and must not serialise with the windows
-    double pos[kChunk];
+  const int stride = nwarp * 32;
+  int cb = u.y + warp * 32;
+  ChunkLoad nxt = load_chunk(a, cb + lane, cb + lane < u.z);
+  for (; cb < u.z; cb += stride) {
+    const ChunkLoad cur = nxt;
+    const bool valid = cb + lane < u.z;
+    const int cnt = cur.info & 255;
+    const int lcell = cur.info >> 8;
+    // the random f gather of this block (all four issued back to back) ...
     double2 fv[kChunk];
+    const int src[kChunk] = {cur.perm.x, cur.perm.y, cur.perm.z, cur.perm.w};
 #pragma unroll
     for (int s = 0; s < kChunk; ++s) {
-      pos[s] = 0.0;
       fv[s] = make_double2(0.0, 0.0);
       if (s < cnt) {
-        pos[s] = __ldg(a.pos + start + s);
-        const int src = __ldg(a.perm + start + s);
         if (REAL) {
-          fv[s].x = __ldg(static_cast<const double*>(a.f) + src);
+          fv[s].x = __ldg(static_cast<const double*>(a.f) + src[s]);
         } else {
-          fv[s] = __ldg(static_cast<const double2*>(a.f) + (int64_t)src * a.batch + col);
+          fv[s] = __ldg(static_cast<const double2*>(a.f) + (int64_t)src[s] * a.batch + col);
         }
       }
     }
+    // ... and the next block's descriptors, in flight during this block's math
+    nxt = load_chunk(a, cb + stride + lane, cb + stride + lane < u.z);
+    const double pos[kChunk] = {cur.p01.x, cur.p01.y, cur.p23.x, cur.p23.y};
     double2 r[2 * M];
 #pragma unroll
     for (int i = 0; i < 2 * M; ++i) r[i] = make_double2(0.0, 0.0);
@@ -122,7 +142,7 @@ template <int M, bool REAL>
 static void launch_spread_m(const NnfftPlanImpl& p, const void* f, double2* grid, int batch,
                             cudaStream_t s) {
   const size_t smem = sizeof(double2) * (kTile + 2 * M - 1) * (kSpreadThreads / 32);
-  SpreadArgs a{p.sp.pos.p, p.sp.perm.p, p.sp.chunks.p, p.sp.units.p, f, grid, p.g.K, batch};
+  SpreadArgs a{p.sp.pos.p, p.sp.perm.p, p.sp.info.p, p.sp.units.p, f, grid, p.g.K, batch};
   if (p.sp.n_units == 0) return;
   k_spread<M, REAL><<<dim3((unsigned)p.sp.n_units, batch), kSpreadThreads, smem, s>>>(a, p.c1);
   SF_LAUNCH_CHECK();
