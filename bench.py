@@ -52,6 +52,9 @@ CONFIGS = {
                    "0.5cos(pi u), complex128"),
     "4": dict(N=65536, M1=1 << 20, M2=1 << 20, m=6, clustered=False, batch=256,
               desc="config4: batched NNFFT N=65536, M1=M2=2^20, 256 columns, m1=m2=6"),
+    "5": dict(N=4096, M1=1 << 22, M2=1 << 22, m=8, clustered=False, batch=0, sinc=True,
+              desc="config5: fast sinc transform N=4096, L1=L2=2^22 uniform nodes, c real, "
+                   "n=4N Clenshaw-Curtis, m1=m2=8, sigma=2"),
 }
 
 
@@ -177,6 +180,87 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_sinc_b200(args, cfg):
+    """Config 5: one fast_sinc_transform per step (two NNFFTs), device pointers."""
+    import torch
+    import paper_2107_02671_b200 as sf
+    from paper_2107_02671_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    sh = C.c_void_p(stream.cuda_stream)
+    rng = np.random.default_rng(0)
+    a = rng.uniform(-0.5, 0.5, cfg["M1"])
+    b = rng.uniform(-0.5, 0.5, cfg["M2"])
+    c = rng.standard_normal(cfg["M1"])
+    # independent replicas per rank (the sinc path's large stages shard the
+    # same way as the NNFFT; here each rank runs the whole transform)
+    tp = time.perf_counter()
+    plan = sf.sinc_plan(cfg["N"], a, b, m1=cfg["m"], m2=cfg["m"], device=local)
+    torch.cuda.synchronize()
+    plan_ms = (time.perf_counter() - tp) * 1e3
+    d_c = torch.from_numpy(c).to(dev)
+    d_out = torch.empty(cfg["M2"], dtype=torch.complex128, device=dev)
+    L = _lib.lib
+
+    def step():
+        _lib.check(L.sincfft_sinc_execute(plan.handle, d_c.data_ptr(), 1, d_out.data_ptr(),
+                                          _lib.PTR_DEVICE, sh))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        ev1.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    units = cfg["M1"] + cfg["M2"]
+    h_c = torch.from_numpy(c).pin_memory()
+    h_out = torch.empty(cfg["M2"], dtype=torch.complex128).pin_memory()
+
+    def e2e_step():
+        _lib.check(L.sincfft_sinc_execute(plan.handle, h_c.data_ptr(), 1, h_out.data_ptr(),
+                                          _lib.PTR_HOST, sh))
+
+    e2e_step()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    ev1.record(stream)
+    ev1.synchronize()
+    e2e_ms = ev0.elapsed_time(ev1) / args.steps
+    g1, g3 = plan.stage_geometry()
+    # algorithmic bytes (SURVEY.md 8d, config 5): 16 L1 + 24 L2 + 64 (K + N2) + 56 (n+1)
+    alg = 16 * cfg["M1"] + 24 * cfg["M2"] + 64 * (g1["K"] + g1["N2"]) + 56 * (plan.n + 1)
+    peak, peak_kind = peaks()
+    achieved = alg / (ms * 1e-3) / 1e9
+    line = {"metric": "fast sinc transform (L1+L2) nodes/sec fp64", "value": units / (ms * 1e-3),
+            "unit": "nodes/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "n_star": plan.n_star, "K": g1["K"],
+                       "N2": g1["N2"], "fft_length_L": g1["L"]},
+            "roofline": {"bound": "hbm", "kernel": "whole transform", "achieved": achieved,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "alg_bytes_per_launch": alg},
+            "plan_ms": plan_ms,
+            "e2e": {"value": units / (e2e_ms * 1e-3), "unit": "nodes/s",
+                    "h2d_bytes_per_step": 8 * cfg["M1"], "d2h_bytes_per_step": 16 * cfg["M2"],
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": 2 * 5 * args.steps, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_b200(args, cfg):
     import torch
     import paper_2107_02671_b200 as sf
@@ -272,6 +356,12 @@ def run_b200(args, cfg):
     t_dom = stage[names.index(dom)] * 1e-3
     peak, peak_kind = peaks()
     achieved = alg[dom] / t_dom / 1e9
+    # FP64 side of the same kernel: the window polynomials + tap MACs are the
+    # floor for spread/gather; DFMA per node from the kernel's
+    # structure (window.cuh): m pairs x (P + 1) + 2 sqrt (~8 each) + 4m MACs
+    P = 16 if m <= 2 else 15 if m <= 3 else 14 if m <= 6 else 13 if m <= 9 else 12
+    dfma_node = m * (P + 1) + 16 + 4 * m * B
+    flops = {"spread": 2 * dfma_node * Ms, "gather": 2 * dfma_node * Mt, "fft": None}
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
@@ -313,6 +403,7 @@ def run_b200(args, cfg):
         "e2e and device outputs differ"
 
     launches = L.sincfft_nnfft_launches_per_execute(ph) * args.steps
+    fp64_peak = 148 * 64 * 2 * (clk.max_mhz or 1965) * 1e6 / 1e12
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample_rate(cfg)
@@ -334,7 +425,13 @@ def run_b200(args, cfg):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "alg_bytes_per_launch": alg[dom],
-                         "launch_ms": t_dom * 1e3},
+                         "launch_ms": t_dom * 1e3,
+                         "fp64": None if flops[dom] is None else {
+                             "achieved_tflops": flops[dom] / t_dom / 1e12,
+                             "peak_tflops": fp64_peak,
+                             "frac": flops[dom] / t_dom / 1e12 / fp64_peak,
+                             "dfma_per_node": dfma_node,
+                             "peak_note": "148 SMs x 64 DFMA/clk x 2 flops x max SM clock"}},
             "stage_ms": {n: float(stage[i]) for i, n in enumerate(names)},
             "plan_ms": plan_ms,
             "e2e": {"value": e2e_val, "unit": "nodes/s", "h2d_bytes_per_step": h2d,
@@ -362,6 +459,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif cfg.get("sinc"):
+        run_sinc_b200(args, cfg)
     else:
         run_b200(args, cfg)
 
