@@ -1,0 +1,185 @@
+"""Wider GPU parity coverage against the CPU oracle (pinned to the reference by
+tests/test_oracle_golden.py): every window cut-off the kernels instantiate,
+oversampling combinations, m1 != m2, degenerate node sets, heavy cells,
+batches, streams, and size-independent properties at the BASELINE sizes."""
+
+import numpy as np
+import pytest
+
+import paper_2107_02671_b200 as sf
+from oracle import sincfft_oracle as O
+from tests.inputs import nodes_and_coeffs
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def relerr(a, b, f):
+    return float(np.max(np.abs(np.asarray(a) - np.asarray(b))) / np.sum(np.abs(f)))
+
+
+def both(N, v, x, f, sigma1=2.0, sigma2=2.0, m1=4, m2=4):
+    plan = sf.nnfft_plan(N, v, x, sigma1=sigma1, sigma2=sigma2, m1=m1, m2=m2)
+    got = sf.nnfft_trafo(plan, f)
+    ref = O.trafo(O.plan(N, v, x, sigma1, sigma2, m1, m2), f)
+    return got, ref
+
+
+@pytest.mark.parametrize("m", [2, 3, 5, 7, 9, 11, 12, 14, 16])
+def test_every_cutoff(m):
+    v, x, f = nodes_and_coeffs(100 + m, 3000, 2000)
+    N, vs = sf.rescale_frequencies(256, v, 2.0, m)
+    got, ref = both(N, vs, x, f, m1=m, m2=m)
+    assert relerr(got, ref, f) <= TOL
+
+
+@pytest.mark.parametrize("sigma1,sigma2", [(1.25, 1.25), (1.5, 2.0), (2.0, 1.5), (1.25, 2.0)])
+def test_oversampling_pairs(sigma1, sigma2):
+    m = 5
+    v, x, f = nodes_and_coeffs(7, 2500, 1700)
+    N, vs = sf.rescale_frequencies(400, v, sigma1, m)
+    if (sigma1 * N) % 2:
+        N += 1  # keep sigma1*N an even integer; the band still holds
+    got, ref = both(N, vs, x, f, sigma1, sigma2, m, m)
+    assert relerr(got, ref, f) <= TOL
+
+
+@pytest.mark.parametrize("m1,m2", [(4, 8), (8, 4), (2, 10)])
+def test_unequal_cutoffs(m1, m2):
+    v, x, f = nodes_and_coeffs(3, 4000, 3000)
+    N, vs = sf.rescale_frequencies(512, v, 2.0, m1)
+    got, ref = both(N, vs, x, f, m1=m1, m2=m2)
+    assert relerr(got, ref, f) <= TOL
+
+
+def test_single_node_and_band_edges():
+    geo = sf.NnfftGeometry.from_parameters(64, 1, 1, 2.0, 2.0, 4, 4)
+    lim = 0.5 / geo.a
+    for v0 in (-lim, lim, 0.0, 7.0 / geo.N1):
+        for x0 in (-0.5, 0.5, 0.0):
+            got, ref = both(64, np.array([v0]), np.array([x0]), np.array([1.0 - 2.0j]))
+            assert relerr(got, ref, np.array([1.0])) <= TOL, (v0, x0)
+
+
+def test_heavy_cell_splits_units():
+    # 200k sources in ONE cell: ~50k chunks -> many work units on one tile,
+    # exercising the multi-unit atomic flush and the equal-cell rounds
+    rng = np.random.default_rng(5)
+    M1 = 200_000
+    v = np.full(M1, 0.123456)
+    v[::7] = 0.123456 + 1e-7  # a second, neighbouring cell
+    x = rng.uniform(-0.5, 0.5, 5000)
+    f = rng.standard_normal(M1) + 1j * rng.standard_normal(M1)
+    got, ref = both(1024, v, x, f, m1=6, m2=6)
+    assert relerr(got, ref, f) <= TOL
+
+
+def test_duplicate_and_sorted_targets():
+    rng = np.random.default_rng(9)
+    v = rng.uniform(-0.45, 0.45, 3000)
+    x = np.concatenate([np.full(700, -0.25), np.sort(rng.uniform(-0.5, 0.5, 2000)),
+                        np.full(300, 0.5)])
+    f = rng.standard_normal(3000) + 1j * rng.standard_normal(3000)
+    got, ref = both(300, v, x, f, m1=6, m2=6)
+    assert relerr(got, ref, f) <= TOL
+
+
+def test_batched_matches_oracle_columns():
+    v, x, f = nodes_and_coeffs(12, 6000, 5000, batch=16)
+    N, vs = sf.rescale_frequencies(1024, v, 2.0, 6)
+    plan = sf.nnfft_plan(N, vs, x, m1=6, m2=6)
+    out = sf.nnfft_trafo(plan, f)
+    tab = O.plan(N, vs, x, m1=6, m2=6)
+    for b in range(16):
+        assert relerr(out[:, b], O.trafo(tab, f[:, b]), f[:, b]) <= TOL
+
+
+def test_concurrent_streams_one_plan():
+    torch = pytest.importorskip("torch")
+    v, x, f = nodes_and_coeffs(13, 20000, 15000)
+    N, vs = sf.rescale_frequencies(2048, v, 2.0, 8)
+    plan = sf.nnfft_plan(N, vs, x, m1=8, m2=8)
+    ref = sf.nnfft_trafo(plan, f)
+    df = torch.from_numpy(f).cuda()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for st in (s1, s2, s1, s2):
+        with torch.cuda.stream(st):
+            outs.append(sf.nnfft_trafo(plan, df))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert relerr(o.cpu().numpy(), ref, f) <= 1e-15
+
+
+def test_shape_and_domain_errors():
+    plan = sf.nnfft_plan(64, np.zeros(5), np.zeros(3))
+    with pytest.raises(sf.ParameterError):
+        sf.nnfft_trafo(plan, np.ones(4, complex))
+    with pytest.raises(sf.ParameterError):
+        sf.nnfft_plan(64, np.zeros(0), np.zeros(3))
+    with pytest.raises(sf.ParameterError):
+        sf.nnfft_plan(64, np.zeros(5), np.zeros(3), m1=17, m2=17)  # beyond the kernels
+    with pytest.raises(sf.ParameterError):
+        sf.nnfft_plan(64, np.zeros(5), np.zeros(3), window1="bspline")
+
+
+def test_sinc_default_and_epsilon_plans():
+    rng = np.random.default_rng(21)
+    a = rng.uniform(-0.5, 0.5, 300)
+    b = rng.uniform(-0.5, 0.5, 200)
+    c = rng.standard_normal(300) + 1j * rng.standard_normal(300)
+    for kw in ({}, {"epsilon": 1e-10}, {"n": 777, "m1": 7, "m2": 9}):
+        plan = sf.sinc_plan(96, a, b, **kw)
+        out = sf.fast_sinc_transform(plan, c)
+        st = O.sinc_plan(96, a, b, n=plan.n, m1=plan.m1, m2=plan.m2)
+        assert relerr(out, O.sinc_transform(st, c), c) <= TOL, kw
+        err = np.max(np.abs(out[:50] - O.sinc_direct(c, a, b[:50], 96))) / np.sum(np.abs(c))
+        assert err <= plan.error_bound()["full"], kw
+
+
+def test_sinc_mode_detection_and_general_route():
+    N = 32
+    grid_a = (np.arange(16) - 8) / 16
+    grid_b = (np.arange(N) - N // 2) / N
+    rng = np.random.default_rng(0)
+    ra, rb = rng.uniform(-0.5, 0.5, 16), rng.uniform(-0.5, 0.5, 24)
+    assert sf.sinc_plan(N, ra, rb).mode is sf.SincMode.GENERAL
+    assert sf.sinc_plan(N, grid_a, rb).mode is sf.SincMode.EQUISPACED_SOURCES
+    assert sf.sinc_plan(N, ra, grid_b).mode is sf.SincMode.EQUISPACED_TARGETS
+    assert sf.sinc_plan(N, grid_a, grid_b).mode is sf.SincMode.EQUISPACED_BOTH
+    with pytest.raises(sf.ParameterError):
+        sf.sinc_plan(N, ra, rb, mode="equispaced-sources")
+    with pytest.raises(sf.ParameterError):
+        sf.sinc_plan(16, rng.uniform(-0.5, 0.5, 7), rb)
+
+
+@pytest.mark.slow
+def test_config3_full_size_properties():
+    """BASELINE config 3 at full size: linearity, and the paper's bound against
+    the direct NDFT on 48 targets (the O(M1 M2) oracle is infeasible in full)."""
+    v, x, f = nodes_and_coeffs(0, 1 << 24, 1 << 24, clustered=True)
+    N, vs = sf.rescale_frequencies(1 << 20, v, 2.0, 8)
+    plan = sf.nnfft_plan(N, vs, x, m1=8, m2=8)
+    out = sf.nnfft_trafo(plan, f)
+    g = np.random.default_rng(1).standard_normal(f.size) * (1 - 1j)
+    lin = sf.nnfft_trafo(plan, f - 2.0 * g)
+    l1 = np.sum(np.abs(f)) + 2 * np.sum(np.abs(g))
+    assert np.max(np.abs(lin - (out - 2.0 * sf.nnfft_trafo(plan, g)))) <= 1e-13 * l1
+    idx = np.r_[0:16, np.argsort(np.abs(x))[:16], np.argsort(-np.abs(x))[:16]]
+    direct = O.nndft_direct(f, v, x[idx], 1 << 20, chunk=4)
+    err = np.max(np.abs(out[idx] - direct)) / np.sum(np.abs(f))
+    assert err <= O.bound_nnfft_sinh(N, 2.0, 2.0, 8, 8)
+    assert err <= 1e-12  # the reference measured ~3.5e-15 at m = 8
+
+
+@pytest.mark.slow
+def test_config5_full_size_vs_oracle():
+    """BASELINE config 5 (fast sinc, L1 = L2 = 2^22) against the CPU oracle."""
+    rng = np.random.default_rng(0)
+    a = rng.uniform(-0.5, 0.5, 1 << 22)
+    b = rng.uniform(-0.5, 0.5, 1 << 22)
+    c = rng.standard_normal(1 << 22)
+    plan = sf.sinc_plan(4096, a, b, m1=8, m2=8)
+    out = sf.fast_sinc_transform(plan, c)
+    ref = O.sinc_transform(O.sinc_plan(4096, a, b, m1=8, m2=8), c)
+    assert relerr(out, ref, c) <= TOL
