@@ -429,7 +429,7 @@ void launch_twiddle(DevArray<double2>& t, int64_t n, int64_t count, int64_t step
   SF_LAUNCH_CHECK();
 }
 
-size_t smem_bytes(int64_t elems) { return sizeof(double2) * (size_t)(elems + elems / 8 + 1); }
+size_t smem_bytes(int64_t elems) { return sizeof(double2) * (size_t)((elems + 7) / 8 * 8); }
 
 template <class Kern>
 void set_smem(Kern k, size_t bytes) {

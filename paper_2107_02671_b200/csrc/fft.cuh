@@ -14,8 +14,8 @@
 //   * a transform of length n in shared memory occupies elements e in
 //     [0, n*nb): element i of batch b is e = i*nb + b (nb interleaved
 //     transforms, b fastest so consecutive lanes touch consecutive words);
-//   * physical slot spad(e) = e + e/8 pads one slot per 8 to break the
-//     power-of-two strides of the late stages (16-byte elements);
+//   * physical slot spad(e) permutes slots within aligned groups of 8 (XOR
+//     swizzle) to break the power-of-two strides of the late stages;
 //   * DIF maps natural order -> digit-reversed order, DIT maps digit-reversed
 //     order -> natural order, both in place and with forward sign
 //     exp(-2 pi i/n); inverse transforms use conj(FFT(conj(x))).
@@ -35,7 +35,11 @@ struct FftStages {
   int toff[kMaxStages];  // offset of stage q's twiddles W_n^{j*G_q}, j < S_q, in the table
 };
 
-__device__ __forceinline__ int spad(int e) { return e + (e >> 3); }
+// XOR swizzle within each aligned group of 8 16-byte slots: maps the strided
+// butterfly accesses of every stage shape used here to distinct bank groups
+// within a quarter-warp (simulated: 1.0x for radix-16 rows, <= 1.33x for the
+// odd-radix column stages; plain +1-per-8 padding gave 2x on radix-16 S=1)
+__device__ __forceinline__ int spad(int e) { return e ^ (((e >> 3) ^ (e >> 6)) & 7); }
 
 // ------------------------------------------------------------ radix kernels
 template <int R>
@@ -170,8 +174,43 @@ struct Dft<7> : DftOdd<7> {};
 // for leg r is W_n^{r*j*G} with G = n/(R*S).  One load per butterfly from a
 // compact per-stage table (w = W_n^{j*G} at tw[j]; all stages of an n-point
 // FFT need only ~n/15 distinct values, so the table stays L1-resident); leg r
-// uses w^r by running multiplication (<= 15 roundings, ~2e-15 relative -- far
+// uses w^r formed by a multiply tree (<= 4 roundings, ~1e-15 relative -- far
 // inside the 1e-12 parity budget).
+// x[r] *= w^r, r = 1..R-1, with powers formed as a tree (dependency depth
+// <= 4 complex multiplies instead of a 15-deep running product)
+template <int R>
+__device__ __forceinline__ void apply_twiddles(double2* x, double2 w) {
+  if (R == 2) {
+    x[1] = cmul(x[1], w);
+    return;
+  }
+  const double2 w2 = cmul(w, w);
+  x[1] = cmul(x[1], w);
+  x[2] = cmul(x[2], w2);
+  if (R == 3) return;
+  const double2 w3 = cmul(w2, w);
+  x[3] = cmul(x[3], w3);
+  if (R == 4) return;
+  const double2 w4 = cmul(w2, w2);
+  x[4] = cmul(x[4], w4);
+  if (R == 5) return;
+  x[5] = cmul(x[5], cmul(w4, w));
+  x[6] = cmul(x[6], cmul(w4, w2));
+  if (R == 7) return;
+  x[7] = cmul(x[7], cmul(w4, w3));
+  if (R == 8) return;
+  const double2 w8 = cmul(w4, w4);
+  x[8] = cmul(x[8], w8);
+  x[9] = cmul(x[9], cmul(w8, w));
+  x[10] = cmul(x[10], cmul(w8, w2));
+  x[11] = cmul(x[11], cmul(w8, w3));
+  const double2 w12 = cmul(w8, w4);
+  x[12] = cmul(x[12], w12);
+  x[13] = cmul(x[13], cmul(w12, w));
+  x[14] = cmul(x[14], cmul(w12, w2));
+  x[15] = cmul(x[15], cmul(w12, w3));
+}
+
 template <int R, bool DIT>
 __device__ __forceinline__ void fft_stage(double2* s, int nb_log2, int S, int G,
                                           const double2* __restrict__ tw, int tid, int nthr) {
@@ -194,23 +233,9 @@ __device__ __forceinline__ void fft_stage(double2* s, int nb_log2, int S, int G,
     const bool twid = j != 0;
     double2 w1 = make_double2(1.0, 0.0);
     if (twid) w1 = __ldg(tw + j);
-    if (DIT && twid) {
-      double2 wr = w1;
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        x[r] = cmul(x[r], wr);
-        if (r + 1 < R) wr = cmul(wr, w1);
-      }
-    }
+    if (DIT && twid) apply_twiddles<R>(x, w1);
     Dft<R>::run(x);
-    if (!DIT && twid) {
-      double2 wr = w1;
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        x[r] = cmul(x[r], wr);
-        if (r + 1 < R) wr = cmul(wr, w1);
-      }
-    }
+    if (!DIT && twid) apply_twiddles<R>(x, w1);
 #pragma unroll
     for (int r = 0; r < R; ++r) s[spad(((base + r * S) << nb_log2) + b)] = x[r];
     j += dj;
