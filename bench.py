@@ -402,7 +402,7 @@ def run_b200(args, cfg):
     assert np.max(np.abs(h_out.numpy() - dev_out)) <= 1e-13 * np.abs(fshard).sum(), \
         "e2e and device outputs differ"
 
-    launches = L.sincfft_nnfft_launches_per_execute(ph) * args.steps
+    launches = L.sincfft_nnfft_launches_per_execute(ph, B) * args.steps
     fp64_peak = 148 * 64 * 2 * (clk.max_mhz or 1965) * 1e6 / 1e12
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -418,7 +418,7 @@ def run_b200(args, cfg):
             "config": {"workload": cfg["desc"], "N": cfg["N"], "M1": cfg["M1"], "M2": cfg["M2"],
                        "m1": m, "m2": m, "sigma1": 2.0, "sigma2": 2.0, "batch": B,
                        "N_star": n_star, "N1": geo["N1"], "K": K, "N2": N2,
-                       "fft_length_L": geo["L"], "l2": "inputs larger than L2 "
+                       "fft_length_L": geo["L"], "fft_L1xL2": [geo["L1"], geo["L2"]], "l2": "inputs larger than L2 "
                        "(f and out 256 MiB each per column vs 126 MB L2)",
                        "parallelism": f"sources+targets sharded x{world}" +
                        (", NCCL all-reduce of the K-grid" if world > 1 else "")},

@@ -111,8 +111,8 @@ SINCFFT_API int sincfft_nnfft_execute_profiled(sincfft_nnfft_plan plan, const do
                                                double *out, int64_t batch, void *stream,
                                                double *stage_ms);
 
-/* Number of kernel launches one execute issues (for launch accounting). */
-SINCFFT_API int sincfft_nnfft_launches_per_execute(sincfft_nnfft_plan plan);
+/* Number of kernel launches one execute of `batch` columns issues. */
+SINCFFT_API int sincfft_nnfft_launches_per_execute(sincfft_nnfft_plan plan, int64_t batch);
 
 /* Materialise the reference's step-0 tables (NnfftPlan.spread_idx/_val,
  * gather_idx/_val, hat1, hat2; nnfft.py:92-107,175-205) into HOST buffers,

@@ -60,7 +60,7 @@ SIGNATURES = {
     "sincfft_nnfft_finish": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, _vp]),
     "sincfft_nnfft_export_tables": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sincfft_nnfft_execute_profiled": (C.c_int, [_vp, _vp, _vp, C.c_int64, _vp, _vp]),
-    "sincfft_nnfft_launches_per_execute": (C.c_int, [_vp]),
+    "sincfft_nnfft_launches_per_execute": (C.c_int, [_vp, C.c_int64]),
     "sincfft_sinc_plan_create": (C.c_int, [C.POINTER(_vp), C.c_int64, C.c_int64, C.c_int64,
                                            C.c_int64, C.c_int64, _vp, _vp, _vp, _vp,
                                            C.c_double, C.c_double, C.c_int32, C.c_int32,

@@ -1,0 +1,302 @@
+// batched.cu -- B >= kBatchedMin coefficient columns sharing one plan
+// (BASELINE config 4: 256 columns).  The reference applies nnfft_trafo column
+// by column; here the columns are the vector dimension:
+//
+//   * a lane owns one column, a warp 32 consecutive columns, so every load of
+//     F[src, :] and store of out[dst, :] (row-major (M, B) user layouts) is a
+//     512-byte coalesced row segment;
+//   * window values are evaluated ONCE per node per warp (lane l evaluates
+//     node l of a 32-node block, the block's windows are broadcast from shared
+//     memory) and reused by all 32 columns;
+//   * spread: nodes sorted by cell; each lane keeps a ROLLING register window
+//     of the 2m grid points the current cell touches; when the cell advances
+//     the lowest point is final and is stored (tile interior: plain store,
+//     exclusive; tile halo: fp64 atomic into zeroed rows) -- no shared-memory
+//     accumulator and no per-tap atomics;
+//   * gather: targets sorted by position; each lane keeps a rolling window of
+//     the 2m h rows the current target reads, loading only rows that enter the
+//     window (consecutive targets share almost all of them).
+// Grid and h use point-major layouts [K][B], [Kout][B]; the length-L FFT
+// stage still runs per column, with tiled transposes around it.
+#include "nnfft_impl.cuh"
+
+namespace sfb {
+
+constexpr int kTileB = 128;   // cells per spread CTA
+constexpr int kSub = 8;       // F rows prefetched per sub-block
+
+// ------------------------------------------------------------------ spread
+struct SpreadBArgs {
+  const double* pos;   // cell-sorted fl(N1 v)
+  const int* perm;
+  const int* tile;     // first sorted source of each kTileB-cell tile [ntile+1]
+  const double2* f;    // (M1, B) row-major
+  double2* grid;       // [K][B]
+  int64_t K;
+  int B;
+};
+
+template <int M>
+__device__ __forceinline__ void spread_flush(const SpreadBArgs& a, double2* r, int64_t& ccur,
+                                             int64_t cell0, int64_t cend, int col, bool colok) {
+  const int64_t p = ccur + 1 - M;
+  if (colok && p >= 0 && p < a.K) {
+    double2* dst = a.grid + p * a.B + col;
+    if (p >= cell0 + M && p <= cend - M) {
+      *dst = r[0];  // interior: only this tile touches it
+    } else if (r[0].x != 0.0 || r[0].y != 0.0) {
+      atomicAdd(&dst->x, r[0].x);
+      atomicAdd(&dst->y, r[0].y);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2 * M - 1; ++i) r[i] = r[i + 1];
+  r[2 * M - 1] = make_double2(0.0, 0.0);
+  ++ccur;
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) k_spread_b(SpreadBArgs a, WinCoef C) {
+  extern __shared__ double wsm[];
+  constexpr int WS = 2 * M + 1;  // padded row
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double* wl = wsm + warp * 32 * WS;
+  const int col = blockIdx.y * blockDim.x + threadIdx.x;
+  const bool colok = col < a.B;
+  const int64_t cell0 = (int64_t)blockIdx.x * kTileB;
+  const int64_t cend = min(cell0 + kTileB, a.K);
+  const int s0 = a.tile[blockIdx.x], s1 = a.tile[blockIdx.x + 1];
+  const int64_t halfK = a.K / 2;
+  double2 r[2 * M];
+#pragma unroll
+  for (int i = 0; i < 2 * M; ++i) r[i] = make_double2(0.0, 0.0);
+  int64_t ccur = cell0 - 1;
+  for (int sb = s0; sb < s1; sb += 32) {
+    const int j = sb + lane;
+    int cl = 0, src = 0;
+    if (j < s1) {
+      const double pos = __ldg(a.pos + j);
+      const double fl = floor(pos);
+      cl = (int)((int64_t)fl + halfK);
+      src = __ldg(a.perm + j);
+      double w[2 * M];
+      window_taps<M>(C, pos - fl, w);
+#pragma unroll
+      for (int i = 0; i < 2 * M; ++i) wl[lane * WS + i] = w[i];
+    }
+    __syncwarp();
+    const int n = min(32, s1 - sb);
+    for (int s0b = 0; s0b < n; s0b += kSub) {
+      double2 fv[kSub];
+#pragma unroll
+      for (int k = 0; k < kSub; ++k) {
+        const int sr = __shfl_sync(0xffffffffu, src, (s0b + k) & 31);
+        fv[k] = make_double2(0.0, 0.0);
+        if (colok && s0b + k < n) fv[k] = __ldg(a.f + (int64_t)sr * a.B + col);
+      }
+#pragma unroll
+      for (int k = 0; k < kSub; ++k) {
+        if (s0b + k < n) {  // warp-uniform
+          const int64_t c = __shfl_sync(0xffffffffu, cl, s0b + k);
+          while (ccur < c) spread_flush<M>(a, r, ccur, cell0, cend, col, colok);
+          const double* wr = wl + (s0b + k) * WS;
+#pragma unroll
+          for (int i = 0; i < 2 * M; ++i) {
+            const double wi = wr[i];
+            r[i].x = fma(fv[k].x, wi, r[i].x);
+            r[i].y = fma(fv[k].y, wi, r[i].y);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  while (ccur < cend - 1) spread_flush<M>(a, r, ccur, cell0, cend, col, colok);
+#pragma unroll
+  for (int i = 0; i < 2 * M; ++i) spread_flush<M>(a, r, ccur, cell0, cend, col, colok);
+}
+
+// zero the grid rows shared by two tiles (touched with atomics)
+__global__ void k_zero_halo(double2* grid, int64_t K, int B, int m, int64_t ntile) {
+  const int64_t t = blockIdx.x;
+  const int64_t b = min(t * kTileB, K);  // the grid end is a tile boundary too
+  for (int64_t p = b - m + 1 + threadIdx.y; p <= b + m - 1; p += blockDim.y) {
+    if (p < 0 || p >= K) continue;
+    for (int c = threadIdx.x; c < B; c += blockDim.x) grid[p * B + c] = make_double2(0.0, 0.0);
+  }
+}
+
+// ------------------------------------------------------------------ gather
+struct GatherBArgs {
+  const double* pos;   // sorted target positions fl(N2 xs)
+  const int* perm;
+  const double* scale;
+  const double2* h;    // [Kout][B]
+  double2* out;        // (M2, B) row-major
+  int64_t M2, Kout, N2, s_lo;
+  int B;
+  int per_cta;         // targets per CTA
+};
+
+template <int M>
+__global__ void __launch_bounds__(256) k_gather_b(GatherBArgs a, WinCoef C) {
+  extern __shared__ double wsm[];
+  constexpr int WS = 2 * M + 1;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  double* wl = wsm + warp * 32 * WS;
+  const int col = blockIdx.y * blockDim.x + threadIdx.x;
+  const bool colok = col < a.B;
+  const int64_t j0 = (int64_t)blockIdx.x * a.per_cta;
+  const int64_t j1 = min(j0 + a.per_cta, a.M2);
+  double2 hr[2 * M];
+  int64_t kbase = INT64_MIN / 2;  // h rows [kbase, kbase + 2M) are in hr
+  auto row = [&](int64_t k) -> double2 {
+    if (!colok) return make_double2(0.0, 0.0);
+    int64_t kk = k;
+    if (kk < 0 || kk >= a.Kout) {  // periodic wrap (only when Kout == N2)
+      kk %= a.N2;
+      if (kk < 0) kk += a.N2;
+    }
+    return __ldg(a.h + kk * a.B + col);
+  };
+  for (int64_t jb = j0; jb < j1; jb += 32) {
+    const int64_t j = jb + lane;
+    int64_t kl = 0;
+    int dst = 0;
+    double sc = 0.0;
+    if (j < j1) {
+      const double pos = __ldg(a.pos + j);
+      const double c = floor(pos);
+      kl = (int64_t)c + (1 - M) - a.s_lo;
+      dst = __ldg(a.perm + j);
+      sc = __ldg(a.scale + j);
+      double w[2 * M];
+      window_taps<M>(C, pos - c, w);
+#pragma unroll
+      for (int i = 0; i < 2 * M; ++i) wl[lane * WS + i] = w[i];
+    }
+    __syncwarp();
+    const int n = (int)min((int64_t)32, j1 - jb);
+    for (int s = 0; s < n; ++s) {
+      const int64_t k0 = __shfl_sync(0xffffffffu, kl, s);
+      const int d = __shfl_sync(0xffffffffu, dst, s);
+      const double scs = __shfl_sync(0xffffffffu, sc, s);
+      if (k0 < kbase || k0 >= kbase + 2 * M) {  // (re)load the whole window
+#pragma unroll
+        for (int i = 0; i < 2 * M; ++i) hr[i] = row(k0 + i);
+        kbase = k0;
+      } else {
+        while (kbase < k0) {  // warp-uniform, < 2M steps
+#pragma unroll
+          for (int i = 0; i < 2 * M - 1; ++i) hr[i] = hr[i + 1];
+          hr[2 * M - 1] = row(kbase + 2 * M);
+          ++kbase;
+        }
+      }
+      const double* wr = wl + s * WS;
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < 2 * M; ++i) {
+        const double wi = wr[i];
+        acc.x = fma(hr[i].x, wi, acc.x);
+        acc.y = fma(hr[i].y, wi, acc.y);
+      }
+      if (colok) a.out[(int64_t)d * a.B + col] = make_double2(acc.x * scs, acc.y * scs);
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------- transposes
+// out[c][r] = in[r][c] for an R x Cc complex matrix (32 x 32 tiles)
+__global__ void __launch_bounds__(256) k_transpose(const double2* __restrict__ in,
+                                                   double2* __restrict__ out, int64_t R,
+                                                   int64_t Cc) {
+  __shared__ double2 t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < R && c < Cc) t[i][threadIdx.x] = __ldg(in + r * Cc + c);
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < R && c < Cc) out[c * R + r] = t[threadIdx.x][i];
+  }
+}
+
+static void transpose(const double2* in, double2* out, int64_t R, int64_t Cc, cudaStream_t s) {
+  const dim3 grid((unsigned)ceil_div(Cc, 32), (unsigned)ceil_div(R, 32));
+  k_transpose<<<grid, dim3(32, 8), 0, s>>>(in, out, R, Cc);
+  SF_LAUNCH_CHECK();
+}
+
+// --------------------------------------------------------------- drivers
+template <int M>
+static void spread_b_m(const NnfftPlanImpl& p, const double2* f, double2* grid, int B,
+                       cudaStream_t s) {
+  const int64_t ntile = ceil_div(p.g.K, kTileB);
+  k_zero_halo<<<(unsigned)(ntile + 1), dim3(32, 8), 0, s>>>(grid, p.g.K, B, M, ntile);
+  SF_LAUNCH_CHECK();
+  SpreadBArgs a{p.sp.bpos.p, p.sp.bperm.p, p.sp.btile.p, f, grid, p.g.K, B};
+  const int threads = (int)std::min<int64_t>(256, ceil_div(B, 32) * 32);
+  const size_t smem = sizeof(double) * (2 * M + 1) * 32 * (threads / 32);
+  k_spread_b<M><<<dim3((unsigned)ntile, (unsigned)ceil_div(B, 256)), threads, smem, s>>>(a, p.c1);
+  SF_LAUNCH_CHECK();
+}
+
+template <int M>
+static void gather_b_m(const NnfftPlanImpl& p, const double2* h, double2* out, int B,
+                       cudaStream_t s) {
+  const int per_cta = 64;
+  GatherBArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, h, out, p.g.M2, p.fft.Kout, p.g.N2,
+                p.fft.s_lo, B, per_cta};
+  const int threads = (int)std::min<int64_t>(256, ceil_div(B, 32) * 32);
+  const size_t smem = sizeof(double) * (2 * M + 1) * 32 * (threads / 32);
+  k_gather_b<M><<<dim3((unsigned)ceil_div(p.g.M2, per_cta), (unsigned)ceil_div(B, 256)), threads,
+                  smem, s>>>(a, p.c2);
+  SF_LAUNCH_CHECK();
+}
+
+#define SF_DISPATCH(m, FN, ...)                                                         \
+  switch (m) {                                                                          \
+    case 2: FN<2>(__VA_ARGS__); break;                                                  \
+    case 3: FN<3>(__VA_ARGS__); break;                                                  \
+    case 4: FN<4>(__VA_ARGS__); break;                                                  \
+    case 5: FN<5>(__VA_ARGS__); break;                                                  \
+    case 6: FN<6>(__VA_ARGS__); break;                                                  \
+    case 7: FN<7>(__VA_ARGS__); break;                                                  \
+    case 8: FN<8>(__VA_ARGS__); break;                                                  \
+    case 9: FN<9>(__VA_ARGS__); break;                                                  \
+    case 10: FN<10>(__VA_ARGS__); break;                                                \
+    case 11: FN<11>(__VA_ARGS__); break;                                                \
+    case 12: FN<12>(__VA_ARGS__); break;                                                \
+    case 13: FN<13>(__VA_ARGS__); break;                                                \
+    case 14: FN<14>(__VA_ARGS__); break;                                                \
+    case 15: FN<15>(__VA_ARGS__); break;                                                \
+    case 16: FN<16>(__VA_ARGS__); break;                                                \
+    default: fail(5, "unsupported window cut-off");                                     \
+  }
+
+void run_execute_batched(const NnfftPlanImpl& p, const double2* f, double2* out, int B,
+                         cudaStream_t s, cudaEvent_t* ev) {
+  const int64_t K = p.g.K, Ko = p.fft.Kout;
+  Scratch gp(sizeof(double2) * (size_t)K * B, s);   // [K][B]
+  Scratch gc(sizeof(double2) * (size_t)K * B, s);   // [B][K]
+  Scratch work(sizeof(double2) * (size_t)p.fft.work_elems() * B, s);
+  Scratch hc(sizeof(double2) * (size_t)Ko * B, s);  // [B][Kout]
+  Scratch hp(sizeof(double2) * (size_t)Ko * B, s);  // [Kout][B]
+  if (ev) SF_CUDA(cudaEventRecord(ev[0], s));
+  SF_DISPATCH(p.g.m1, spread_b_m, p, f, gp.as<double2>(), B, s);
+  if (ev) SF_CUDA(cudaEventRecord(ev[1], s));
+  transpose(gp.as<double2>(), gc.as<double2>(), K, B, s);
+  run_fft(p, gc.as<double2>(), hc.as<double2>(), work.as<double2>(), B, s);
+  transpose(hc.as<double2>(), hp.as<double2>(), B, Ko, s);
+  if (ev) SF_CUDA(cudaEventRecord(ev[2], s));
+  SF_DISPATCH(p.g.m2, gather_b_m, p, hp.as<double2>(), out, B, s);
+  if (ev) SF_CUDA(cudaEventRecord(ev[3], s));
+}
+
+}  // namespace sfb

@@ -199,8 +199,9 @@ namespace sfb {
 
 void run_execute(const NnfftPlanImpl& p, const double2* f, double2* out, int batch,
                  cudaStream_t s) {
+  if (batch >= kBatchedMin) return run_execute_batched(p, f, out, batch, s);
   Scratch grid(sizeof(double2) * (size_t)p.g.K * batch, s);
-  Scratch work(p.fft.single ? 0 : sizeof(double2) * (size_t)p.fft.L * batch, s);
+  Scratch work(sizeof(double2) * (size_t)p.fft.work_elems() * batch, s);
   Scratch h(sizeof(double2) * (size_t)p.fft.Kout * batch, s);
   run_spread(p, f, grid.as<double2>(), batch, s);
   run_fft(p, grid.as<double2>(), h.as<double2>(), work.as<double2>(), batch, s);
@@ -313,7 +314,7 @@ int sincfft_nnfft_finish(sincfft_nnfft_plan plan, const double* grid_dev, double
     const sfb::NnfftPlanImpl& p = plan->impl;
     set_device(p.device);
     cudaStream_t s = as_stream(stream);
-    sfb::Scratch work(p.fft.single ? 0 : sizeof(double2) * (size_t)p.fft.L * batch, s);
+    sfb::Scratch work(sizeof(double2) * (size_t)p.fft.work_elems() * batch, s);
     sfb::Scratch h(sizeof(double2) * (size_t)p.fft.Kout * batch, s);
     sfb::run_fft(p, (const double2*)grid_dev, h.as<double2>(), work.as<double2>(), (int)batch, s);
     const size_t ob = sizeof(double2) * (size_t)p.g.M2 * batch;
@@ -336,18 +337,23 @@ int sincfft_nnfft_execute_profiled(sincfft_nnfft_plan plan, const double* f, dou
     const sfb::NnfftPlanImpl& p = plan->impl;
     set_device(p.device);
     cudaStream_t s = as_stream(stream);
-    sfb::Scratch grid(sizeof(double2) * (size_t)p.g.K * batch, s);
-    sfb::Scratch work(p.fft.single ? 0 : sizeof(double2) * (size_t)p.fft.L * batch, s);
-    sfb::Scratch h(sizeof(double2) * (size_t)p.fft.Kout * batch, s);
+    const bool batched = batch >= sfb::kBatchedMin;
+    sfb::Scratch grid(batched ? 0 : sizeof(double2) * (size_t)p.g.K * batch, s);
+    sfb::Scratch work(batched ? 0 : sizeof(double2) * (size_t)p.fft.work_elems() * batch, s);
+    sfb::Scratch h(batched ? 0 : sizeof(double2) * (size_t)p.fft.Kout * batch, s);
     cudaEvent_t ev[4];
     for (auto& e : ev) SF_CUDA(cudaEventCreate(&e));
-    SF_CUDA(cudaEventRecord(ev[0], s));
-    sfb::run_spread(p, (const double2*)f, grid.as<double2>(), (int)batch, s);
-    SF_CUDA(cudaEventRecord(ev[1], s));
-    sfb::run_fft(p, grid.as<double2>(), h.as<double2>(), work.as<double2>(), (int)batch, s);
-    SF_CUDA(cudaEventRecord(ev[2], s));
-    sfb::run_gather(p, h.as<double2>(), (double2*)out, (int)batch, s);
-    SF_CUDA(cudaEventRecord(ev[3], s));
+    if (batch >= sfb::kBatchedMin) {
+      sfb::run_execute_batched(p, (const double2*)f, (double2*)out, (int)batch, s, ev);
+    } else {
+      SF_CUDA(cudaEventRecord(ev[0], s));
+      sfb::run_spread(p, (const double2*)f, grid.as<double2>(), (int)batch, s);
+      SF_CUDA(cudaEventRecord(ev[1], s));
+      sfb::run_fft(p, grid.as<double2>(), h.as<double2>(), work.as<double2>(), (int)batch, s);
+      SF_CUDA(cudaEventRecord(ev[2], s));
+      sfb::run_gather(p, h.as<double2>(), (double2*)out, (int)batch, s);
+      SF_CUDA(cudaEventRecord(ev[3], s));
+    }
     SF_CUDA(cudaEventSynchronize(ev[3]));
     float t;
     for (int i = 0; i < 3; ++i) {
@@ -360,10 +366,13 @@ int sincfft_nnfft_execute_profiled(sincfft_nnfft_plan plan, const double* f, dou
   });
 }
 
-int sincfft_nnfft_launches_per_execute(sincfft_nnfft_plan plan) {
+int sincfft_nnfft_launches_per_execute(sincfft_nnfft_plan plan, int64_t batch) {
   if (!plan) return -1;
-  // memset node (counted as a launch) + spread + FFT (1 or 3) + gather + unpermute
-  return 1 + 1 + (plan->impl.fft.single ? 1 : 3) + 2;
+  const int fft = plan->impl.fft.single ? 1 : plan->impl.fft.direct ? 2 : 3;
+  // column-vectorised batch: halo zeroing + spread + 2 transposes + FFT + gather
+  if (batch >= sfb::kBatchedMin) return 1 + 1 + 2 + fft + 1;
+  // grid memset (a launch on the stream) + spread + FFT + gather
+  return 1 + 1 + fft + 1;
 }
 
 int sincfft_nnfft_export_tables(sincfft_nnfft_plan plan, int64_t* spread_idx, double* spread_val,
@@ -480,7 +489,7 @@ int sincfft_sinc_execute(sincfft_sinc_plan plan, const double* c, int32_t c_is_r
     const size_t cb = (c_is_real ? sizeof(double) : sizeof(double2)) * (size_t)plan->L1;
     InBuf cin(c, cb, ptr_kind, s);
     sfb::Scratch g1(sizeof(double2) * (size_t)p1.g.K, s);
-    sfb::Scratch w1(p1.fft.single ? 0 : sizeof(double2) * (size_t)p1.fft.L, s);
+    sfb::Scratch w1(sizeof(double2) * (size_t)p1.fft.work_elems(), s);
     sfb::Scratch h1(sizeof(double2) * (size_t)p1.fft.Kout, s);
     sfb::Scratch alpha(sizeof(double2) * (size_t)p1.g.M2, s);
     if (c_is_real) sfb::run_spread_real(p1, (const double*)cin.ptr, g1.as<double2>(), s);

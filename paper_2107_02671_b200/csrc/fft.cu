@@ -26,6 +26,7 @@
 // Bhat is produced at plan time by k_colfwd + k_rowmul(spectrum mode) (or
 // k_single) on b, so it is in exactly the layout the forward pass produces.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "nnfft_impl.cuh"
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(512) k_single(FftArgs a, int spectrum) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256) k_colfwd(FftArgs a) {
+__global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd(FftArgs a) {
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int C = 1 << a.C_log2;
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(256) k_colfwd(FftArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_rowmul(FftArgs a, int spectrum) {
+__global__ void __launch_bounds__(256, SFB_FFT_MINB) k_rowmul(FftArgs a, int spectrum) {
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int64_t p = blockIdx.x;
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(256) k_rowmul(FftArgs a, int spectrum) {
   for (int i = threadIdx.x; i < L1; i += T) row[i] = cconj(sm[spad(i)]);
 }
 
-__global__ void __launch_bounds__(256) k_colinv(FftArgs a) {
+__global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv(FftArgs a) {
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int C = 1 << a.C_log2;
@@ -319,6 +320,166 @@ __global__ void __launch_bounds__(256) k_colinv(FftArgs a) {
   }
 }
 
+// ------------------------------------------------------ direct four-step
+// n = P n1 + n2 (n1 < A, n2 < P),  k = k1 + A k2:
+//   X[k1 + A k2] = sum_n2 W_P^{n2 k2} [ W_N2^{n2 k1} sum_n1 x[P n1 + n2] W_A^{n1 k1} ]
+// x[n] = g[l] D[l] for n = (l - K/2) mod N2, l in [0, K) (the embedded,
+// deconvolved grid of nnfft.py:236-238 with the 1/N1, 1/N2 factors in D).
+struct DirectArgs {
+  const double2* g;   // [batch][K]
+  const double* D;
+  double2* Y;         // [batch][A][P]
+  double2* h;         // [batch][Kout]
+  const double2* twA;
+  const double2* twP;
+  const double2* w_lo;  // W_N2 two-level table
+  const double2* w_hi;
+  const double2* cp;    // omega_P^{n^2/2}, n < P
+  const double2* bhat;  // FFT_LP(b)/LP, reversed layout
+  const int* revA;
+  const int* revP;
+  int64_t K, N2, A, P, LP, Kout, s_lo;
+  int C_log2, R_log2;
+  int p_smooth;
+  FftStages stA, stP;
+};
+
+__global__ void __launch_bounds__(256, SFB_FFT_MINB) k_dstep1(DirectArgs a) {
+  extern __shared__ double2 sm[];
+  const int col = blockIdx.y;
+  const int C = 1 << a.C_log2;
+  const int64_t c0 = (int64_t)blockIdx.x * C;
+  const int A = (int)a.A;
+  const int n_el = A << a.C_log2;
+  const int T = blockDim.x;
+  const double2* g = a.g + (int64_t)col * a.K;
+  const int64_t halfK = a.K / 2;
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int64_t n2 = c0 + (e & (C - 1));
+      const int64_t n = a.P * (int64_t)(e >> a.C_log2) + n2;
+      v[u] = make_double2(0.0, 0.0);
+      if (e < n_el && n2 < a.P) {
+        int64_t l = -1;
+        if (n < a.K - halfK) l = n + halfK;                     // n in [0, K/2)
+        else if (n >= a.N2 - halfK) l = n - a.N2 + halfK;       // n in [N2 - K/2, N2)
+        if (l >= 0) v[u] = cscale(__ldg(g + l), __ldg(a.D + l));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = v[u];
+  }
+  __syncthreads();
+  fft_dif(sm, a.C_log2, a.stA, a.twA);
+  double2* Y = a.Y + (int64_t)col * a.A * a.P;
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 w[kU];
+    int64_t k1v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int64_t n2 = c0 + (e & (C - 1));
+      w[u] = make_double2(1.0, 0.0);
+      k1v[u] = 0;
+      if (e < n_el && n2 < a.P) {
+        k1v[u] = __ldg(a.revA + (e >> a.C_log2));
+        w[u] = wbig(a.w_lo, a.w_hi, n2 * k1v[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int64_t n2 = c0 + (e & (C - 1));
+      if (e < n_el && n2 < a.P) Y[k1v[u] * a.P + n2] = cmul(sm[spad(e)], w[u]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, SFB_FFT_MINB) k_dstep2(DirectArgs a) {
+  extern __shared__ double2 sm[];
+  const int col = blockIdx.y;
+  const int R = 1 << a.R_log2;
+  const int64_t r0 = (int64_t)blockIdx.x * R;
+  const int n = a.p_smooth ? (int)a.P : (int)a.LP;
+  const int n_el = n << a.R_log2;
+  const int T = blockDim.x;
+  const double2* Y = a.Y + (int64_t)col * a.A * a.P;
+  // load rows r0.. (element (n2, row b) at e = n2 * R + b), Bluestein pre-chirp
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int64_t k1 = r0 + (e & (R - 1));
+      const int n2 = e >> a.R_log2;
+      v[u] = make_double2(0.0, 0.0);
+      if (e < n_el && k1 < a.A && n2 < a.P) {
+        v[u] = Y[k1 * a.P + n2];
+        if (!a.p_smooth) v[u] = cmul(v[u], __ldg(a.cp + n2));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = v[u];
+  }
+  __syncthreads();
+  fft_dif(sm, a.R_log2, a.stP, a.twP);
+  if (!a.p_smooth) {
+    for (int e = threadIdx.x; e < n_el; e += T)
+      sm[spad(e)] = cconj(cmul(sm[spad(e)], __ldg(a.bhat + (e >> a.R_log2))));
+    __syncthreads();
+    fft_dit(sm, a.R_log2, a.stP, a.twP);
+  }
+  double2* h = a.h + (int64_t)col * a.Kout;
+  const int nout = (int)a.P << a.R_log2;  // positions 0..P-1 of each row
+  for (int e = threadIdx.x; e < nout; e += T) {
+    const int64_t k1 = r0 + (e & (R - 1));
+    if (k1 >= a.A) continue;
+    const int q = e >> a.R_log2;
+    int64_t k2;
+    double2 X;
+    if (a.p_smooth) {
+      k2 = __ldg(a.revP + q);
+      X = sm[spad(e)];
+    } else {
+      k2 = q;
+      X = cmul(cconj(sm[spad(e)]), __ldg(a.cp + q));
+    }
+    int64_t kk = (k1 + a.A * k2 - a.s_lo) % a.N2;
+    if (kk < 0) kk += a.N2;
+    if (kk < a.Kout) h[kk] = X;
+  }
+}
+
+// b_j = conj(cp_|j|) on the cyclic length LP: j in [0, P) and LP - j, j in [1, P)
+__global__ void k_bluestein_b(double2* b, const double2* cp, int64_t P, int64_t LP) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= LP) return;
+  int64_t j = -1;
+  if (i < P) j = i;
+  else if (i > LP - P) j = LP - i;
+  b[i] = j >= 0 ? cconj(cp[j]) : make_double2(0.0, 0.0);
+}
+
+__global__ void k_chirp_p(double2* cp, int64_t P) {
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (n >= P) return;
+  // omega_P^{n^2/2} = exp(-pi i (n^2 mod 2P) / P)
+  const int64_t r = (n * n) % (2 * P);
+  double sn, cs;
+  sincospi(-(double)r / (double)P, &sn, &cs);
+  cp[n] = make_double2(cs, sn);
+}
+
+__global__ void k_deconv(double* D, const double* hat2, int64_t K, double inv_n1n2) {
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (l < K) D[l] = inv_n1n2 / hat2[l];
+}
+
 // ------------------------------------------------------------ host planning
 namespace {
 
@@ -338,8 +499,10 @@ FftStages make_stages(int64_t n) {
   st.n = (int)n;
   int64_t r = n;
   std::vector<int> rad;
+#if SFB_FFT_MAXR >= 16
   while (r % 16 == 0) rad.push_back(16), r /= 16;
-  if (r % 8 == 0) rad.push_back(8), r /= 8;
+#endif
+  while (r % 8 == 0) rad.push_back(8), r /= 8;
   if (r % 4 == 0) rad.push_back(4), r /= 4;
   if (r % 2 == 0) rad.push_back(2), r /= 2;
   for (int p : {7, 5, 3})
@@ -460,7 +623,121 @@ FftArgs make_args(const NnfftPlanImpl& p) {
 
 }  // namespace
 
+namespace {
+
+constexpr int kDirectSmem = 4096;   // elements per CTA in step 1 (and step 2 target)
+constexpr int kDirectSmem2 = 8192;  // hard cap for one step-2 row (R = 1)
+
+// pick N2 = A * P for the direct path; false if no split fits.  best_out is
+// the model cost per point (stage costs + ~1 unit per byte of HBM traffic)
+bool choose_direct(int64_t N2, DirectFft& d, double* best_out = nullptr) {
+  double best = 1e300;
+  bool found = false;
+  for (int64_t A = 2; A <= 2048 && A <= N2; ++A) {
+    if (N2 % A || !smooth7(A)) continue;
+    const int64_t P = N2 / A;
+    const bool ps = smooth7(P);
+    const int64_t LP = ps ? P : next_smooth(2 * P - 1);
+    if (LP > kDirectSmem2) continue;
+    int C = 8;
+    while (C > 1 && C * A > kDirectSmem) C >>= 1;
+    if (C < 2) continue;
+    const double cst = (stage_cost(A) + (ps ? stage_cost(P)
+                                          : 2.0 * stage_cost(LP) * (double)LP / (double)P) +
+                        48.0) *
+                       (C < 4 ? 1.15 : 1.0);
+    if (cst < best) {
+      best = cst, found = true;
+      d.A = A, d.P = P, d.LP = LP, d.p_smooth = ps, d.C = C;
+    }
+  }
+  if (best_out) *best_out = best;
+  return found;
+}
+
+int log2i(int x) {
+  int l = 0;
+  while ((1 << l) < x) ++l;
+  return l;
+}
+
+void build_direct(NnfftPlanImpl& p, cudaStream_t s) {
+  DirectFft& d = p.fft.d;
+  const Geometry& g = p.g;
+  d.C_log2 = log2i(d.C);
+  const int n2len = (int)(d.p_smooth ? d.P : d.LP);
+  d.R = 1;
+  while (2 * d.R * n2len <= kDirectSmem && d.R < 64) d.R *= 2;
+  d.R_log2 = log2i(d.R);
+  d.stA = make_stages(d.A);
+  d.stP = make_stages(n2len);
+  launch_stage_twiddles(d.twA, d.stA, s);
+  launch_stage_twiddles(d.twP, d.stP, s);
+  launch_twiddle(d.w_lo, g.N2, kTwSplit, 1, s);
+  launch_twiddle(d.w_hi, g.N2, ceil_div(g.N2, kTwSplit) + 1, kTwSplit, s);
+  auto upload = [&](DevArray<int>& dst, const std::vector<int>& v) {
+    dst.alloc((int64_t)v.size());
+    SF_CUDA(cudaMemcpyAsync(dst.p, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice, s));
+    SF_CUDA(cudaStreamSynchronize(s));
+  };
+  upload(d.revA, digit_reverse(d.stA));
+  if (d.p_smooth) upload(d.revP, digit_reverse(d.stP));
+  d.D.alloc(g.K);
+  k_deconv<<<(unsigned)ceil_div(g.K, 256), 256, 0, s>>>(d.D.p, p.hat2.p, g.K,
+                                                       1.0 / ((double)g.N1 * (double)g.N2));
+  SF_LAUNCH_CHECK();
+  if (!d.p_smooth) {
+    d.cp.alloc(d.P);
+    k_chirp_p<<<(unsigned)ceil_div(d.P, 256), 256, 0, s>>>(d.cp.p, d.P);
+    SF_LAUNCH_CHECK();
+    DevArray<double2> b(d.LP);
+    k_bluestein_b<<<(unsigned)ceil_div(d.LP, 256), 256, 0, s>>>(b.p, d.cp.p, d.P, d.LP);
+    SF_LAUNCH_CHECK();
+    d.bhat.alloc(d.LP);
+    FftArgs fa{};
+    fa.g = b.p;
+    fa.Y = d.bhat.p;
+    fa.L = d.LP;
+    fa.st1 = d.stP;
+    fa.tw1 = d.twP.p;
+    k_single<IN_PLAIN><<<dim3(1, 1), 512, smem_bytes(d.LP), s>>>(fa, 1);
+    SF_LAUNCH_CHECK();
+    SF_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
+DirectArgs make_direct_args(const NnfftPlanImpl& p) {
+  const DirectFft& d = p.fft.d;
+  DirectArgs a{};
+  a.D = d.D.p;
+  a.twA = d.twA.p;
+  a.twP = d.twP.p;
+  a.w_lo = d.w_lo.p;
+  a.w_hi = d.w_hi.p;
+  a.cp = d.cp.p;
+  a.bhat = d.bhat.p;
+  a.revA = d.revA.p;
+  a.revP = d.revP.p;
+  a.K = p.g.K;
+  a.N2 = p.g.N2;
+  a.A = d.A;
+  a.P = d.P;
+  a.LP = d.LP;
+  a.Kout = p.fft.Kout;
+  a.s_lo = p.fft.s_lo;
+  a.C_log2 = d.C_log2;
+  a.R_log2 = d.R_log2;
+  a.p_smooth = d.p_smooth ? 1 : 0;
+  a.stA = d.stA;
+  a.stP = d.stP;
+  return a;
+}
+
+}  // namespace
+
 void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
+  set_smem(k_dstep1, smem_bytes(kDirectSmem));
+  set_smem(k_dstep2, smem_bytes(kDirectSmem2));
   // dynamic shared memory limits (per device; the plan's device is current)
   set_smem(k_single<IN_GP>, smem_bytes(kSingleMax));
   set_smem(k_single<IN_PLAIN>, smem_bytes(kSingleMax));
@@ -471,6 +748,34 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   FftPlan& f = p.fft;
   const Geometry& g = p.g;
   const int64_t Lmin = g.K + f.Kout - 1;
+  // direct four-step when it is cheaper than the Bluestein over L (model:
+  // stage costs per point + ~1 unit per byte moved; Bluestein moves ~144
+  // bytes per point of L, the direct path ~48 per point of N2), and always for
+  // launch-bound sizes (2 kernels instead of 3)
+  double dcost = 0.0;
+  const bool can_direct = Lmin > kSingleMax && !getenv("SFB_NO_DIRECT_FFT") &&
+                          choose_direct(g.N2, f.d, &dcost);
+  bool use_direct = false;
+  if (can_direct) {
+    double gbest = 1e300;
+    for (int64_t L2 = 2; L2 <= 2048; ++L2) {
+      if (!smooth7(L2)) continue;
+      const int64_t L1 = next_smooth(ceil_div(Lmin, L2));
+      if (L1 > kRowMax || L1 < 2) continue;
+      gbest = std::min(gbest, (double)(L1 * L2) / (double)g.N2 *
+                                  (2.0 * stage_cost(L1) + 2.0 * stage_cost(L2) + 144.0));
+    }
+    use_direct = g.N2 <= 65536 || dcost < gbest;
+  }
+  if (use_direct) {
+    f.direct = true;
+    f.single = false;
+    f.L = f.d.A * f.d.P;
+    f.L1 = f.d.A;
+    f.L2 = f.d.P;
+    build_direct(p, s);
+    return;
+  }
   if (Lmin <= kSingleMax) {
     f.single = true;
     f.L = next_smooth(Lmin);
@@ -542,6 +847,19 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
 void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work, int batch,
              cudaStream_t s) {
   const FftPlan& f = p.fft;
+  if (f.direct) {
+    DirectArgs a = make_direct_args(p);
+    a.g = grid;
+    a.Y = work;
+    a.h = h;
+    const DirectFft& d = f.d;
+    k_dstep1<<<dim3((unsigned)ceil_div(d.P, d.C), batch), 256, smem_bytes(d.A * d.C), s>>>(a);
+    SF_LAUNCH_CHECK();
+    const int64_t n2len = d.p_smooth ? d.P : d.LP;
+    k_dstep2<<<dim3((unsigned)ceil_div(d.A, d.R), batch), 256, smem_bytes(n2len * d.R), s>>>(a);
+    SF_LAUNCH_CHECK();
+    return;
+  }
   FftArgs a = make_args(p);
   a.g = grid;
   a.h = h;

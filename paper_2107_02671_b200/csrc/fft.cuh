@@ -26,6 +26,18 @@
 
 namespace sfb {
 
+// largest butterfly radix (16: fewer shared-memory passes; 8: fewer registers,
+// measured faster: 3 resident CTAs/SM beat one fewer smem pass --
+// more resident CTAs) and the matching minimum CTAs/SM for __launch_bounds__
+#ifndef SFB_FFT_MAXR
+#define SFB_FFT_MAXR 8
+#endif
+#if SFB_FFT_MAXR >= 16
+#define SFB_FFT_MINB 2
+#else
+#define SFB_FFT_MINB 3
+#endif
+
 constexpr int kMaxStages = 24;
 
 struct FftStages {
@@ -258,7 +270,9 @@ __device__ __forceinline__ void fft_stage_dispatch(int R, double2* s, int nb_log
     case 5: fft_stage<5, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
     case 7: fft_stage<7, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
     case 8: fft_stage<8, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
+#if SFB_FFT_MAXR >= 16
     case 16: fft_stage<16, DIT>(s, nb_log2, S, G, tw, tid, nthr); break;
+#endif
     default: break;
   }
 }

@@ -46,7 +46,13 @@ struct SpreadPlan {
   DevArray<int2> chunks;  // plan-time only: {first sorted index, info}
   DevArray<int4> units;   // {tile, chunk begin, chunk end, 0}
   int64_t n_chunks = 0, n_units = 0;
+  // batched path (batched.cu): cell-sorted sources and per-128-cell tile starts
+  DevArray<double> bpos;
+  DevArray<int> bperm;
+  DevArray<int> btile;
 };
+
+constexpr int kBatchedMin = 16;  // columns from which the column-vectorised path is used
 
 // Targets sorted by fl(N2 * xs); scale = 1/phi_hat_1(N x_j) in sorted order
 // (optionally times an external per-target weight, used by the fast sinc
@@ -68,14 +74,35 @@ struct GatherPlan {
 // k' in [0, Kout), l in [0, K), realised as a cyclic convolution of length
 // L = L1 * L2 (7-smooth) via FFT.  Bhat = FFT_L(b)/L stored in the four-step
 // "digit-reversed" layout the forward kernels produce.
+// Direct four-step DFT of length N2 = A * P (used when it fits): step 1 does
+// the A-point DFTs of the P columns x[P n1 + n2] in shared memory (A 7-smooth)
+// reading only the K nonzero inputs; step 2 does the P-point DFTs of the A rows
+// in shared memory -- directly when P is 7-smooth, else by an in-smem
+// Bluestein of smooth length LP >= 2P-1 -- writing only the Kout outputs the
+// gather reads.  Traffic ~16(K + 2 N2 + Kout) bytes instead of ~3 passes over L.
+struct DirectFft {
+  int64_t A = 0, P = 0, LP = 0;
+  int C = 1, C_log2 = 0;  // step-1 columns per CTA
+  int R = 1, R_log2 = 0;  // step-2 rows per CTA
+  bool p_smooth = false;
+  FftStages stA{}, stP{};  // stP: P (smooth) or LP (Bluestein)
+  DevArray<double2> twA, twP, w_lo, w_hi, cp, bhat;
+  DevArray<int> revA, revP;
+  DevArray<double> D;      // 1 / (N1 N2 phi_hat_2(l - K/2)), l in [0, K)
+};
+
 struct FftPlan {
   int64_t L = 0, L1 = 0, L2 = 0, Kout = 0, s_lo = 0;
   int C = 1, C_log2 = 0;  // columns per CTA in the column kernels
   bool single = true;     // L fits one CTA
+  bool direct = false;    // DirectFft path instead of the Bluestein over L
   FftStages st1{}, st2{}; // L1 (rows / single) and L2 (columns)
   DevArray<double2> tw1, tw2, tw_lo, tw_hi;
   DevArray<int> rev2;
   DevArray<double2> P, Q, Bhat;
+  DirectFft d;
+  // scratch elements per column for run_fft's `work`
+  int64_t work_elems() const { return single ? 0 : direct ? d.A * d.P : L; }
 };
 
 struct NnfftPlanImpl {
@@ -116,5 +143,9 @@ void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batc
 // whole transform with device pointers (scratch allocated stream-ordered)
 void run_execute(const NnfftPlanImpl& p, const double2* f, double2* out, int batch,
                  cudaStream_t stream);
+// ----- batched.cu: batch >= kBatchedMin columns, columns across lanes
+// ev (optional): 4 events recorded around spread | transpose+FFT+transpose | gather
+void run_execute_batched(const NnfftPlanImpl& p, const double2* f, double2* out, int batch,
+                         cudaStream_t stream, cudaEvent_t* ev = nullptr);
 
 }  // namespace sfb

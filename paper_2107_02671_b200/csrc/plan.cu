@@ -154,6 +154,11 @@ __global__ void k_chunk_slots(const int2* chunks, int64_t n, const double* pos, 
   }
 }
 
+__global__ void k_tile_starts(const int* cstart, int64_t K, int T, int64_t ntile, int* out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t <= ntile) out[t] = cstart[min(t * T, K)];
+}
+
 __global__ void k_tile_bounds(const unsigned long long* key, int64_t n, int64_t ntile,
                               int* tstart) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -416,6 +421,13 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
     k_unit_emit<<<blocks(ntile), 256, 0, s>>>(tstart.as<int>(), nu.as<int>(), uoff.as<int>(), ntile,
                                               p.sp.units.p);
     SF_LAUNCH_CHECK();
+    // batched path: keep the cell-sorted arrays and the 128-cell tile starts
+    {
+      const int64_t ntb = ceil_div(K, 128);
+      p.sp.btile.alloc(ntb + 1);
+      k_tile_starts<<<blocks(ntb + 1), 256, 0, s>>>(cstart.as<int>(), K, 128, ntb, p.sp.btile.p);
+      SF_LAUNCH_CHECK();
+    }
     // re-lay the sorted sources out in chunk-slot order (kChunk slots per chunk)
     DevArray<double> spos(nchunks * kChunk);
     DevArray<int> sperm(nchunks * kChunk);
@@ -424,6 +436,8 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
                                                   spos.p, sperm.p, p.sp.info.p);
     SF_LAUNCH_CHECK();
     SF_CUDA(cudaStreamSynchronize(s));
+    p.sp.bpos = std::move(p.sp.pos);
+    p.sp.bperm = std::move(p.sp.perm);
     p.sp.pos = std::move(spos);
     p.sp.perm = std::move(sperm);
     p.sp.chunks.release();

@@ -183,3 +183,19 @@ def test_config5_full_size_vs_oracle():
     out = sf.fast_sinc_transform(plan, c)
     ref = O.sinc_transform(O.sinc_plan(4096, a, b, m1=8, m2=8), c)
     assert relerr(out, ref, c) <= TOL
+
+
+@pytest.mark.parametrize("B,m,clustered", [(16, 6, False), (40, 3, True), (64, 8, True),
+                                           (300, 5, False)])
+def test_column_vectorised_batch_path(B, m, clustered):
+    """B >= 16 columns run the column-vectorised kernels (csrc/batched.cu);
+    every column must match the oracle applied to that column."""
+    v, x, f = nodes_and_coeffs(40 + B, 5000, 3500, clustered=clustered, batch=B)
+    N, vs = sf.rescale_frequencies(700, v, 2.0, m)
+    plan = sf.nnfft_plan(N, vs, x, m1=m, m2=m)
+    out = sf.nnfft_trafo(plan, f)
+    tab = O.plan(N, vs, x, m1=m, m2=m)
+    for b in sorted({0, 1, B // 2, B - 1}):
+        assert relerr(out[:, b], O.trafo(tab, f[:, b]), f[:, b]) <= TOL, b
+    one = sf.nnfft_trafo(plan, np.ascontiguousarray(f[:, 5]))
+    assert relerr(out[:, 5], one, f[:, 5]) <= 1e-14
