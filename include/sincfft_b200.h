@@ -13,7 +13,8 @@
  *   - a batch of B coefficient vectors is an (M1, B) row-major array
  *     (column b of F is F[:, b]); outputs are (M2, B) row-major;
  *   - `ptr_kind` says whether user pointers are host (SINCFFT_PTR_HOST,
- *     copied inside the call) or device (SINCFFT_PTR_DEVICE) memory;
+ *     copied inside the call; SINCFFT_PTR_HOST_ASYNC: same, without the final
+ *     synchronisation) or device (SINCFFT_PTR_DEVICE) memory;
  *   - `stream` is a cudaStream_t (NULL = legacy default stream); all work of
  *     one call is ordered on it, and host-pointer calls synchronize it before
  *     returning;
@@ -47,8 +48,13 @@ extern "C" {
 #define SINCFFT_ENOMEM 4       /* device allocation failed (MemoryError)  */
 #define SINCFFT_EUNSUPPORTED 5 /* outside the implemented envelope        */
 
-#define SINCFFT_PTR_HOST 0
-#define SINCFFT_PTR_DEVICE 1
+#define SINCFFT_PTR_HOST 0       /* host memory; the call returns when done   */
+#define SINCFFT_PTR_DEVICE 1     /* device memory, stream-ordered             */
+#define SINCFFT_PTR_HOST_ASYNC 2 /* host memory (page-locked for overlap): the
+                                  * copies and kernels are enqueued on `stream`
+                                  * and the call returns at once; the caller
+                                  * synchronizes `stream` before reading `out`
+                                  * or reusing `f` (pipelined batches)        */
 
 typedef struct sincfft_nnfft_plan_s *sincfft_nnfft_plan;
 typedef struct sincfft_sinc_plan_s *sincfft_sinc_plan;

@@ -12,14 +12,14 @@ from . import bounds
 from .errors import ParameterError, PositivityError
 from .fast_sinc import SincMode, SincPlan, fast_sinc_transform, sinc_plan
 from .nnfft import (NnfftGeometry, NnfftPlan, WindowSpec, nnfft_plan, nnfft_trafo,
-                    rescale_frequencies)
+                    nnfft_trafo_into, rescale_frequencies)
 from .quadrature import CcQuadrature, cc_quadrature, cc_weights_direct, cc_weights_fast
 
 __version__ = "0.1.0"
 
 __all__ = [
     "ParameterError", "PositivityError",
-    "WindowSpec", "NnfftGeometry", "NnfftPlan", "nnfft_plan", "nnfft_trafo",
+    "WindowSpec", "NnfftGeometry", "NnfftPlan", "nnfft_plan", "nnfft_trafo", "nnfft_trafo_into",
     "rescale_frequencies",
     "CcQuadrature", "cc_quadrature", "cc_weights_direct", "cc_weights_fast",
     "SincMode", "SincPlan", "sinc_plan", "fast_sinc_transform",

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("SINCFFT_B200_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "lib", "libsincfft_b200.so")
 
 OK, EPARAM, EPOSITIVITY, ECUDA, ENOMEM, EUNSUPPORTED = range(6)
-PTR_HOST, PTR_DEVICE = 0, 1
+PTR_HOST, PTR_DEVICE, PTR_HOST_ASYNC = 0, 1, 2
 
 
 class Geometry(C.Structure):

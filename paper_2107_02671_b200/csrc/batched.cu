@@ -23,7 +23,8 @@
 namespace sfb {
 
 constexpr int kTileB = 128;   // cells per spread CTA
-constexpr int kSub = 8;       // F rows prefetched per sub-block
+constexpr int kSub = 4;       // F rows per pipelined sub-block
+constexpr int kThreadsB = 128;  // 4 warps = 128 columns per CTA
 
 // ------------------------------------------------------------------ spread
 struct SpreadBArgs {
@@ -56,7 +57,7 @@ __device__ __forceinline__ void spread_flush(const SpreadBArgs& a, double2* r, i
 }
 
 template <int M>
-__global__ void __launch_bounds__(256) k_spread_b(SpreadBArgs a, WinCoef C) {
+__global__ void __launch_bounds__(kThreadsB, 4) k_spread_b(SpreadBArgs a, WinCoef C) {
   extern __shared__ double wsm[];
   constexpr int WS = 2 * M + 1;  // padded row
   const int lane = threadIdx.x & 31;
@@ -64,6 +65,7 @@ __global__ void __launch_bounds__(256) k_spread_b(SpreadBArgs a, WinCoef C) {
   double* wl = wsm + warp * 32 * WS;
   const int col = blockIdx.y * blockDim.x + threadIdx.x;
   const bool colok = col < a.B;
+  const double2* fcol = a.f + col;
   const int64_t cell0 = (int64_t)blockIdx.x * kTileB;
   const int64_t cend = min(cell0 + kTileB, a.K);
   const int s0 = a.tile[blockIdx.x], s1 = a.tile[blockIdx.x + 1];
@@ -87,13 +89,25 @@ __global__ void __launch_bounds__(256) k_spread_b(SpreadBArgs a, WinCoef C) {
     }
     __syncwarp();
     const int n = min(32, s1 - sb);
+    // software pipeline: the F rows of sub-block k+1 are in flight while the
+    // taps of sub-block k are accumulated
+    double2 fn[kSub];
+#pragma unroll
+    for (int k = 0; k < kSub; ++k) {
+      const int sr = __shfl_sync(0xffffffffu, src, k);
+      fn[k] = make_double2(0.0, 0.0);
+      if (colok && k < n) fn[k] = __ldg(fcol + (int64_t)sr * a.B);
+    }
     for (int s0b = 0; s0b < n; s0b += kSub) {
       double2 fv[kSub];
 #pragma unroll
+      for (int k = 0; k < kSub; ++k) fv[k] = fn[k];
+#pragma unroll
       for (int k = 0; k < kSub; ++k) {
-        const int sr = __shfl_sync(0xffffffffu, src, (s0b + k) & 31);
-        fv[k] = make_double2(0.0, 0.0);
-        if (colok && s0b + k < n) fv[k] = __ldg(a.f + (int64_t)sr * a.B + col);
+        const int sn = s0b + kSub + k;
+        const int sr = __shfl_sync(0xffffffffu, src, sn & 31);
+        fn[k] = make_double2(0.0, 0.0);
+        if (colok && sn < n) fn[k] = __ldg(fcol + (int64_t)sr * a.B);
       }
 #pragma unroll
       for (int k = 0; k < kSub; ++k) {
@@ -140,7 +154,7 @@ struct GatherBArgs {
 };
 
 template <int M>
-__global__ void __launch_bounds__(256) k_gather_b(GatherBArgs a, WinCoef C) {
+__global__ void __launch_bounds__(kThreadsB, 4) k_gather_b(GatherBArgs a, WinCoef C) {
   extern __shared__ double wsm[];
   constexpr int WS = 2 * M + 1;
   const int lane = threadIdx.x & 31;
@@ -148,28 +162,29 @@ __global__ void __launch_bounds__(256) k_gather_b(GatherBArgs a, WinCoef C) {
   double* wl = wsm + warp * 32 * WS;
   const int col = blockIdx.y * blockDim.x + threadIdx.x;
   const bool colok = col < a.B;
+  const double2* hcol = a.h + (colok ? col : 0);
+  double2* ocol = a.out + col;
   const int64_t j0 = (int64_t)blockIdx.x * a.per_cta;
   const int64_t j1 = min(j0 + a.per_cta, a.M2);
+  const int Kout = (int)a.Kout;
   double2 hr[2 * M];
-  int64_t kbase = INT64_MIN / 2;  // h rows [kbase, kbase + 2M) are in hr
-  auto row = [&](int64_t k) -> double2 {
-    if (!colok) return make_double2(0.0, 0.0);
-    int64_t kk = k;
-    if (kk < 0 || kk >= a.Kout) {  // periodic wrap (only when Kout == N2)
-      kk %= a.N2;
-      if (kk < 0) kk += a.N2;
+  int kbase = -(1 << 30);  // h rows [kbase, kbase + 2M) are in hr
+  auto row = [&](int k) -> double2 {
+    int kk = k;
+    if (kk < 0 || kk >= Kout) {  // periodic wrap (only when Kout == N2)
+      kk %= (int)a.N2;
+      if (kk < 0) kk += (int)a.N2;
     }
-    return __ldg(a.h + kk * a.B + col);
+    return __ldg(hcol + (int64_t)kk * a.B);
   };
   for (int64_t jb = j0; jb < j1; jb += 32) {
     const int64_t j = jb + lane;
-    int64_t kl = 0;
-    int dst = 0;
+    int kl = 0, dst = 0;
     double sc = 0.0;
     if (j < j1) {
       const double pos = __ldg(a.pos + j);
       const double c = floor(pos);
-      kl = (int64_t)c + (1 - M) - a.s_lo;
+      kl = (int)((int64_t)c + (1 - M) - a.s_lo);
       dst = __ldg(a.perm + j);
       sc = __ldg(a.scale + j);
       double w[2 * M];
@@ -180,19 +195,21 @@ __global__ void __launch_bounds__(256) k_gather_b(GatherBArgs a, WinCoef C) {
     __syncwarp();
     const int n = (int)min((int64_t)32, j1 - jb);
     for (int s = 0; s < n; ++s) {
-      const int64_t k0 = __shfl_sync(0xffffffffu, kl, s);
+      const int k0 = __shfl_sync(0xffffffffu, kl, s);
       const int d = __shfl_sync(0xffffffffu, dst, s);
       const double scs = __shfl_sync(0xffffffffu, sc, s);
-      if (k0 < kbase || k0 >= kbase + 2 * M) {  // (re)load the whole window
+      if (k0 != kbase) {
+        if (k0 < kbase || k0 >= kbase + 2 * M) {  // (re)load the whole window
 #pragma unroll
-        for (int i = 0; i < 2 * M; ++i) hr[i] = row(k0 + i);
-        kbase = k0;
-      } else {
-        while (kbase < k0) {  // warp-uniform, < 2M steps
+          for (int i = 0; i < 2 * M; ++i) hr[i] = row(k0 + i);
+          kbase = k0;
+        } else {
+          do {  // warp-uniform, < 2M steps
 #pragma unroll
-          for (int i = 0; i < 2 * M - 1; ++i) hr[i] = hr[i + 1];
-          hr[2 * M - 1] = row(kbase + 2 * M);
-          ++kbase;
+            for (int i = 0; i < 2 * M - 1; ++i) hr[i] = hr[i + 1];
+            hr[2 * M - 1] = row(kbase + 2 * M);
+            ++kbase;
+          } while (kbase < k0);
         }
       }
       const double* wr = wl + s * WS;
@@ -203,7 +220,7 @@ __global__ void __launch_bounds__(256) k_gather_b(GatherBArgs a, WinCoef C) {
         acc.x = fma(hr[i].x, wi, acc.x);
         acc.y = fma(hr[i].y, wi, acc.y);
       }
-      if (colok) a.out[(int64_t)d * a.B + col] = make_double2(acc.x * scs, acc.y * scs);
+      if (colok) ocol[(int64_t)d * a.B] = make_double2(acc.x * scs, acc.y * scs);
     }
     __syncwarp();
   }
@@ -241,9 +258,10 @@ static void spread_b_m(const NnfftPlanImpl& p, const double2* f, double2* grid, 
   k_zero_halo<<<(unsigned)(ntile + 1), dim3(32, 8), 0, s>>>(grid, p.g.K, B, M, ntile);
   SF_LAUNCH_CHECK();
   SpreadBArgs a{p.sp.bpos.p, p.sp.bperm.p, p.sp.btile.p, f, grid, p.g.K, B};
-  const int threads = (int)std::min<int64_t>(256, ceil_div(B, 32) * 32);
+  const int threads = (int)std::min<int64_t>(kThreadsB, ceil_div(B, 32) * 32);
   const size_t smem = sizeof(double) * (2 * M + 1) * 32 * (threads / 32);
-  k_spread_b<M><<<dim3((unsigned)ntile, (unsigned)ceil_div(B, 256)), threads, smem, s>>>(a, p.c1);
+  k_spread_b<M><<<dim3((unsigned)ntile, (unsigned)ceil_div(B, threads)), threads, smem, s>>>(a,
+                                                                                             p.c1);
   SF_LAUNCH_CHECK();
 }
 
@@ -253,10 +271,10 @@ static void gather_b_m(const NnfftPlanImpl& p, const double2* h, double2* out, i
   const int per_cta = 64;
   GatherBArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, h, out, p.g.M2, p.fft.Kout, p.g.N2,
                 p.fft.s_lo, B, per_cta};
-  const int threads = (int)std::min<int64_t>(256, ceil_div(B, 32) * 32);
+  const int threads = (int)std::min<int64_t>(kThreadsB, ceil_div(B, 32) * 32);
   const size_t smem = sizeof(double) * (2 * M + 1) * 32 * (threads / 32);
-  k_gather_b<M><<<dim3((unsigned)ceil_div(p.g.M2, per_cta), (unsigned)ceil_div(B, 256)), threads,
-                  smem, s>>>(a, p.c2);
+  k_gather_b<M><<<dim3((unsigned)ceil_div(p.g.M2, per_cta), (unsigned)ceil_div(B, threads)),
+                  threads, smem, s>>>(a, p.c2);
   SF_LAUNCH_CHECK();
 }
 

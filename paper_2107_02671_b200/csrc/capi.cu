@@ -47,7 +47,8 @@ int guarded(F&& f) {
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 void check_ptr_kind(int32_t k) {
-  if (k != SINCFFT_PTR_HOST && k != SINCFFT_PTR_DEVICE) sfb::fail(1, "ptr_kind must be 0 (host) or 1 (device)");
+  if (k != SINCFFT_PTR_HOST && k != SINCFFT_PTR_DEVICE && k != SINCFFT_PTR_HOST_ASYNC)
+    sfb::fail(1, "ptr_kind must be 0 (host), 1 (device) or 2 (host, asynchronous)");
 }
 
 // device copy of caller data (host -> device, or device alias)
@@ -285,7 +286,7 @@ int sincfft_nnfft_execute(sincfft_nnfft_plan plan, const double* f, double* out,
       sfb::Scratch o(ob, s);
       sfb::run_execute(p, (const double2*)fin.ptr, o.as<double2>(), (int)batch, s);
       SF_CUDA(cudaMemcpyAsync(out, o.p, ob, cudaMemcpyDeviceToHost, s));
-      SF_CUDA(cudaStreamSynchronize(s));
+      if (ptr_kind == SINCFFT_PTR_HOST) SF_CUDA(cudaStreamSynchronize(s));
     }
   });
 }
@@ -324,7 +325,7 @@ int sincfft_nnfft_finish(sincfft_nnfft_plan plan, const double* grid_dev, double
       sfb::Scratch o(ob, s);
       sfb::run_gather(p, h.as<double2>(), o.as<double2>(), (int)batch, s);
       SF_CUDA(cudaMemcpyAsync(out, o.p, ob, cudaMemcpyDeviceToHost, s));
-      SF_CUDA(cudaStreamSynchronize(s));
+      if (ptr_kind == SINCFFT_PTR_HOST) SF_CUDA(cudaStreamSynchronize(s));
     }
   });
 }
@@ -503,7 +504,7 @@ int sincfft_sinc_execute(sincfft_sinc_plan plan, const double* c, int32_t c_is_r
       sfb::Scratch o(ob, s);
       sfb::run_execute(p3, alpha.as<double2>(), o.as<double2>(), 1, s);
       SF_CUDA(cudaMemcpyAsync(out, o.p, ob, cudaMemcpyDeviceToHost, s));
-      SF_CUDA(cudaStreamSynchronize(s));
+      if (ptr_kind == SINCFFT_PTR_HOST) SF_CUDA(cudaStreamSynchronize(s));
     }
   });
 }

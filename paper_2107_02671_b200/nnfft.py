@@ -314,3 +314,34 @@ def _trafo_torch(plan, f):
                                               C.c_void_p(out.data_ptr()), batch,
                                               _lib.PTR_DEVICE, _stream_handle(f)))
     return out
+
+
+def nnfft_trafo_into(plan, f, out, stream=None, blocking=True):
+    """Extension for pipelined host-side use: write the transform of ``f`` into
+    ``out`` (CPU torch tensors, ideally page-locked, or numpy arrays).  With
+    ``blocking=False`` the H2D copy, the kernels and the D2H copy are only
+    enqueued on ``stream`` (a ``torch.cuda.Stream``; default: current) via
+    ``SINCFFT_PTR_HOST_ASYNC`` and the caller synchronizes the stream before
+    reading ``out`` or reusing ``f`` -- alternating two streams overlaps the
+    copies of consecutive transforms."""
+    import torch
+    geo = plan.geometry
+    if isinstance(f, np.ndarray):
+        f = torch.from_numpy(np.ascontiguousarray(f, dtype=complex))
+    if isinstance(out, np.ndarray):
+        out = torch.from_numpy(out)
+    if f.dtype != torch.complex128 or out.dtype != torch.complex128:
+        raise ParameterError("nnfft_trafo_into: f and out must be complex128")
+    if f.device.type != "cpu" or out.device.type != "cpu":
+        raise ParameterError("nnfft_trafo_into: f and out must be host tensors")
+    if not (f.is_contiguous() and out.is_contiguous()):
+        raise ParameterError("nnfft_trafo_into: f and out must be contiguous")
+    batch = 1 if f.ndim == 1 else f.shape[1]
+    if f.shape[0] != geo.M1 or tuple(out.shape) != ((geo.M2,) if f.ndim == 1 else (geo.M2, batch)):
+        raise ParameterError("nnfft_trafo_into: shape mismatch with the plan")
+    st = stream if stream is not None else torch.cuda.current_stream(plan.device)
+    kind = _lib.PTR_HOST if blocking else _lib.PTR_HOST_ASYNC
+    _lib.check(_lib.lib.sincfft_nnfft_execute(plan.handle, C.c_void_p(f.data_ptr()),
+                                              C.c_void_p(out.data_ptr()), batch, kind,
+                                              C.c_void_p(st.cuda_stream)))
+    return out

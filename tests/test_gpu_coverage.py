@@ -199,3 +199,19 @@ def test_column_vectorised_batch_path(B, m, clustered):
         assert relerr(out[:, b], O.trafo(tab, f[:, b]), f[:, b]) <= TOL, b
     one = sf.nnfft_trafo(plan, np.ascontiguousarray(f[:, 5]))
     assert relerr(out[:, 5], one, f[:, 5]) <= 1e-14
+
+
+def test_pipelined_host_async_two_streams():
+    torch = pytest.importorskip("torch")
+    v, x, f = nodes_and_coeffs(17, 30000, 20000)
+    N, vs = sf.rescale_frequencies(1024, v, 2.0, 8)
+    plan = sf.nnfft_plan(N, vs, x, m1=8, m2=8)
+    ref = sf.nnfft_trafo(plan, f)
+    fs = [torch.from_numpy(f * (k + 1)).pin_memory() for k in range(2)]
+    outs = [torch.empty(20000, dtype=torch.complex128).pin_memory() for _ in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for k in range(4):
+        sf.nnfft_trafo_into(plan, fs[k % 2], outs[k % 2], stream=streams[k % 2], blocking=False)
+    torch.cuda.synchronize()
+    for k in range(2):
+        assert relerr(outs[k].numpy(), (k + 1) * ref, (k + 1) * f) <= 1e-14
