@@ -26,6 +26,7 @@
 // Bhat is produced at plan time by k_colfwd + k_rowmul(spectrum mode) (or
 // k_single) on b, so it is in exactly the layout the forward pass produces.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -790,6 +791,12 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
       if (L1 > kRowMax || L1 < 2) continue;
       const double c = cost(L1, L2);
       if (c < best) best = c, f.L1 = L1, f.L2 = L2;
+    }
+    if (const char* e = getenv("SFB_FFT_L1L2")) {  // tuning override "L1xL2"
+      long long a1 = 0, a2 = 0;
+      if (sscanf(e, "%lldx%lld", &a1, &a2) == 2 && a1 * a2 >= Lmin && smooth7(a1) &&
+          smooth7(a2) && a1 <= kRowMax && a2 <= 2048)
+        f.L1 = a1, f.L2 = a2, best = 0;
     }
     if (best >= 1e300)
       fail(5, "FFT length " + std::to_string(Lmin) + " exceeds the supported four-step range");
