@@ -193,7 +193,7 @@ __global__ void k_unit_emit(const int* tstart, const int* nu, const int* off, in
 // (nnfft.py:200-201)
 int64_t gather_slice() {
   const char* e = getenv("SFB_GATHER_SLICE_LOG2");
-  if (e && atoi(e) >= 8 && atoi(e) <= 30) return (int64_t)1 << atoi(e);
+  if (e && atoi(e) >= 9 && atoi(e) <= 30) return (int64_t)1 << atoi(e);
   return kGatherSliceDefault;
 }
 

@@ -96,8 +96,12 @@ __global__ void __launch_bounds__(kSpreadThreads, 2) k_spread(SpreadArgs a, WinC
 #pragma unroll
     for (int i = 0; i < 2 * M; ++i) r[i] = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int s = 0; s < kChunk; ++s) {
-      if (s < cnt) window_accumulate<M, REAL>(C, pos[s] - floor(pos[s]), fv[s], r);
+    for (int s = 0; s < kChunk; s += 2) {
+      // a padding slot has f = 0 and a harmless position, so pairs may run
+      // with a dead second node; skip only fully empty pairs
+      if (s < cnt)
+        window_accumulate2<M, REAL>(C, pos[s] - floor(pos[s]), fv[s], pos[s + 1] - floor(pos[s + 1]),
+                                    fv[s + 1], r);
     }
     // add into the warp-private tile accumulator; equal cells in one warp
     // would race, so leaders of each cell group go first, round by round

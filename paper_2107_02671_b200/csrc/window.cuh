@@ -112,6 +112,87 @@ __device__ __forceinline__ void window_accumulate(const WinCoef& C, double d, do
   }
 }
 
+// window_taps for two nodes at once (shared coefficient loads)
+template <int M>
+__device__ __forceinline__ void window_taps2(const WinCoef& C, double d0, double d1, double* w0,
+                                             double* w1) {
+  constexpr int P = window_degree(M);
+  constexpr int NE = P / 2 + 1;
+  constexpr int NO = (P + 1) / 2;
+  const double u0 = 2.0 * d0 - 1.0, u1 = 2.0 * d1 - 1.0;
+  const double v0 = u0 * u0, v1 = u1 * u1;
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    double E0 = C.e[q][NE - 1], E1 = E0;
+#pragma unroll
+    for (int k = NE - 2; k >= 0; --k) {
+      const double c = C.e[q][k];
+      E0 = fma(E0, v0, c);
+      E1 = fma(E1, v1, c);
+    }
+    double O0 = C.o[q][NO - 1], O1 = O0;
+#pragma unroll
+    for (int k = NO - 2; k >= 0; --k) {
+      const double c = C.o[q][k];
+      O0 = fma(O0, v0, c);
+      O1 = fma(O1, v1, c);
+    }
+    const double hi0 = fma(u0, O0, E0), lo0 = fma(-u0, O0, E0);
+    const double hi1 = fma(u1, O1, E1), lo1 = fma(-u1, O1, E1);
+    if (q < M - 1) {
+      w0[M + q] = hi0, w0[M - 1 - q] = lo0;
+      w1[M + q] = hi1, w1[M - 1 - q] = lo1;
+    } else {
+      w0[2 * M - 1] = sqrt(d0) * hi0, w0[0] = sqrt(1.0 - d0) * lo0;
+      w1[2 * M - 1] = sqrt(d1) * hi1, w1[0] = sqrt(1.0 - d1) * lo1;
+    }
+  }
+}
+
+// Two nodes (d0, f0) and (d1, f1) of ONE cell accumulated into the same taps:
+// every coefficient (a uniform constant-bank load) feeds two independent
+// Horner chains, halving the constant loads per node and doubling the ILP.
+template <int M, bool REAL>
+__device__ __forceinline__ void window_accumulate2(const WinCoef& C, double d0, double2 f0,
+                                                   double d1, double2 f1, double2* r) {
+  constexpr int P = window_degree(M);
+  constexpr int NE = P / 2 + 1;
+  constexpr int NO = (P + 1) / 2;
+  const double u0 = 2.0 * d0 - 1.0, u1 = 2.0 * d1 - 1.0;
+  const double v0 = u0 * u0, v1 = u1 * u1;
+  const double sh0 = sqrt(d0), sl0 = sqrt(1.0 - d0), sh1 = sqrt(d1), sl1 = sqrt(1.0 - d1);
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    double E0 = C.e[q][NE - 1], E1 = E0;
+#pragma unroll
+    for (int k = NE - 2; k >= 0; --k) {
+      const double c = C.e[q][k];
+      E0 = fma(E0, v0, c);
+      E1 = fma(E1, v1, c);
+    }
+    double O0 = C.o[q][NO - 1], O1 = O0;
+#pragma unroll
+    for (int k = NO - 2; k >= 0; --k) {
+      const double c = C.o[q][k];
+      O0 = fma(O0, v0, c);
+      O1 = fma(O1, v1, c);
+    }
+    double hi0 = fma(u0, O0, E0), lo0 = fma(-u0, O0, E0);
+    double hi1 = fma(u1, O1, E1), lo1 = fma(-u1, O1, E1);
+    const int ih = (q < M - 1) ? M + q : 2 * M - 1;
+    const int il = (q < M - 1) ? M - 1 - q : 0;
+    if (q == M - 1) {
+      hi0 *= sh0, lo0 *= sl0, hi1 *= sh1, lo1 *= sl1;
+    }
+    r[ih].x = fma(f1.x, hi1, fma(f0.x, hi0, r[ih].x));
+    r[il].x = fma(f1.x, lo1, fma(f0.x, lo0, r[il].x));
+    if (!REAL) {
+      r[ih].y = fma(f1.y, hi1, fma(f0.y, hi0, r[ih].y));
+      r[il].y = fma(f1.y, lo1, fma(f0.y, lo0, r[il].y));
+    }
+  }
+}
+
 // Fourier transform of the sinh shape function, omega_hat(v)
 // (windows.py:143-160), all three branches; on the NNFFT path only the
 // w > 1e-3 branch is reachable.
