@@ -20,14 +20,18 @@ struct GatherArgs {
   const double* pos;
   const int* perm;
   const double* scale;
+  const int2* span;  // per CTA block: {klo, khi} h range read (plan time)
   const double2* h;  // [batch][Kout], h[k'] = h_{s_lo + k'}
   double2* out;      // (M2, batch) row-major
   int64_t M2, Kout, N2, s_lo;
   int batch;
 };
 
-constexpr int kGatherThreads = 256;
-constexpr int kGatherSpan = 2048;  // h values staged per CTA (32 KiB)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
 
 template <int M>
 __device__ __forceinline__ double2 gather_dot(const double2* hp, const double* w) {
@@ -51,7 +55,6 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherArgs a, WinCoef
   __shared__ double2 hs[kGatherSpan];
   const int64_t j0 = (int64_t)blockIdx.x * kGatherThreads;
   const int64_t j = j0 + threadIdx.x;
-  const int64_t jl = min(j0 + kGatherThreads, a.M2) - 1;
   const int col = blockIdx.y;
   const bool act = j < a.M2;
   double pos = 0.0, sc = 0.0;
@@ -62,17 +65,24 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherArgs a, WinCoef
     dst = __ldg(a.perm + j);
   }
   const double2* h = a.h + (int64_t)col * a.Kout;
-  const int64_t klo = (int64_t)floor(__ldg(a.pos + j0)) + (1 - M) - a.s_lo;
-  const int64_t khi = (int64_t)floor(__ldg(a.pos + jl)) + M - a.s_lo;
+  // the block's h range is precomputed at plan time, so its asynchronous copy
+  // into shared memory starts at once and overlaps the window evaluation
+  const int2 sp = __ldg(a.span + blockIdx.x);
+  const int64_t klo = sp.x, khi = sp.y;
   const bool staged = klo >= 0 && khi < a.Kout && khi - klo + 1 <= kGatherSpan;
   if (staged) {
-    for (int64_t i = threadIdx.x; i <= khi - klo; i += kGatherThreads) hs[i] = __ldg(h + klo + i);
-    __syncthreads();
+    for (int64_t i = threadIdx.x; i <= khi - klo; i += kGatherThreads)
+      cp_async16(hs + i, h + klo + i);
+    asm volatile("cp.async.commit_group;\n" ::);
   }
-  if (!act) return;
   const double c = floor(pos);
   double w[2 * M];
   window_taps<M>(C, pos - c, w);
+  if (staged) {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+  }
+  if (!act) return;
   const int64_t k0 = (int64_t)c + (1 - M) - a.s_lo;
   double2 s;
   if (staged) {
@@ -98,8 +108,8 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherArgs a, WinCoef
 
 void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batch,
                 cudaStream_t s) {
-  GatherArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, h,          out,
-               p.g.M2,     p.fft.Kout,  p.g.N2,        p.fft.s_lo, batch};
+  GatherArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, p.gp.span.p, h, out,
+               p.g.M2,     p.fft.Kout,  p.g.N2,        p.fft.s_lo,  batch};
   const dim3 grid((unsigned)ceil_div(p.g.M2, kGatherThreads), batch);
   switch (p.g.m2) {
 #define SF_CASE(MM)                                          \

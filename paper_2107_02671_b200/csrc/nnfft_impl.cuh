@@ -64,10 +64,14 @@ constexpr int kBatchedMin = 16;  // columns from which the column-vectorised pat
 constexpr int64_t kGatherSliceDefault = (int64_t)1 << 20;
 int64_t gather_slice();  // kGatherSliceDefault unless SFB_GATHER_SLICE_LOG2 is set (tuning)
 
+constexpr int kGatherThreads = 256;  // targets per gather CTA
+constexpr int kGatherSpan = 2048;    // h values staged per CTA (32 KiB)
+
 struct GatherPlan {
   DevArray<double> pos;
   DevArray<int> perm;
   DevArray<double> scale;
+  DevArray<int2> span;  // per gather CTA: {klo, khi} h range (h index k' = s - s_lo)
 };
 
 // Pruned Bluestein: h_{s_lo + k'} = Q[k'] * sum_l (g_l P_l) b_{k'-l},

@@ -220,6 +220,19 @@ __global__ void k_tgt_tables(const double* x, const int* perm, int64_t n, double
   if (!(hat > 0.0)) atomicAdd(min_hat_bits, 1ull);
 }
 
+// h range [klo, khi] (k' = s - s_lo) read by each gather CTA of kGatherThreads
+// sorted targets; {-1, -1} (never staged) if it does not fit in int
+__global__ void k_gather_spans(const double* pos, int64_t n, int64_t nblk, int m2, int64_t s_lo,
+                               int2* span) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= nblk) return;
+  const int64_t j0 = b * kGatherThreads, jl = min(j0 + kGatherThreads, n) - 1;
+  const int64_t lo = (int64_t)floor(pos[j0]) + 1 - m2 - s_lo;
+  const int64_t hi = (int64_t)floor(pos[jl]) + m2 - s_lo;
+  span[b] = (lo >= 0 && hi < (1ll << 31) && lo <= hi) ? make_int2((int)lo, (int)hi)
+                                                       : make_int2(-1, -1);
+}
+
 __global__ void k_hat2(double* hat2, int64_t K, double beta2, int m2, int64_t N2,
                        unsigned long long* bad) {
   const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -483,6 +496,10 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
     const int64_t s_hi = (int64_t)std::floor(phi) + g.m2;
     p.fft.s_lo = s_lo;
     p.fft.Kout = std::min<int64_t>(s_hi - s_lo + 1, g.N2);
+    const int64_t nblk = ceil_div(M2, kGatherThreads);
+    p.gp.span.alloc(nblk);
+    k_gather_spans<<<blocks(nblk), 256, 0, s>>>(p.gp.pos.p, M2, nblk, g.m2, s_lo, p.gp.span.p);
+    SF_LAUNCH_CHECK();
   }
 
   build_fft(p, s);
