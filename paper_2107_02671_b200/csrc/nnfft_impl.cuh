@@ -34,9 +34,15 @@ struct Geometry {
 // sources are stored in chunk-slot order (chunk c owns slots [4c, 4c+4)), so
 // a lane's positions and permutation load as two vectors without first
 // reading a descriptor.
-constexpr int kTile = 256;
+#ifndef SFB_SPREAD_TILE
+#define SFB_SPREAD_TILE 256
+#endif
+constexpr int kTile = SFB_SPREAD_TILE;
 constexpr int kChunk = 4;
-constexpr int kUnitChunks = 1024;
+#ifndef SFB_UNIT_CHUNKS
+#define SFB_UNIT_CHUNKS 1024
+#endif
+constexpr int kUnitChunks = SFB_UNIT_CHUNKS;
 constexpr int kSpreadThreads = 256;
 
 struct SpreadPlan {

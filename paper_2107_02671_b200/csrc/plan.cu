@@ -125,6 +125,11 @@ __global__ void k_chunk_counts(const int* start, int64_t ncell, int* nch) {
   nch[c] = (start[c + 1] - start[c] + kChunk - 1) / kChunk;
 }
 
+// chunk sort key: (tile, rank within cell, local cell)
+constexpr int kLcBits = 12;                   // local cell < kTile <= 4096
+constexpr int kTileKeyShift = kLcBits + 30;  // rank < 2^30
+static_assert(kTile <= (1 << kLcBits), "local cell field too small");
+
 __global__ void k_chunk_emit(const int* start, const int* nch, const int* off, int64_t ncell,
                              unsigned long long* key, int2* desc) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -135,7 +140,7 @@ __global__ void k_chunk_emit(const int* start, const int* nch, const int* off, i
   const unsigned long long tile = (unsigned long long)(c / kTile);
   const int lc = (int)(c % kTile);
   for (int r = 0; r < k; ++r) {
-    key[o + r] = (tile << 40) | ((unsigned long long)r << 8) | (unsigned long long)lc;
+    key[o + r] = (tile << kTileKeyShift) | ((unsigned long long)r << kLcBits) | (unsigned long long)lc;
     const int cnt = min(kChunk, n - r * kChunk);
     desc[o + r] = make_int2(start[c] + r * kChunk, (lc << 8) | cnt);
   }
@@ -163,7 +168,7 @@ __global__ void k_tile_bounds(const unsigned long long* key, int64_t n, int64_t 
                               int* tstart) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t > ntile) return;
-  const unsigned long long target = (unsigned long long)t << 40;
+  const unsigned long long target = (unsigned long long)t << kTileKeyShift;
   int64_t lo = 0, hi = n;
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
@@ -412,7 +417,7 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
                                            ckey.as<unsigned long long>(), cdesc.as<int2>());
     SF_LAUNCH_CHECK();
     const int64_t ntile = ceil_div(K, kTile);
-    const int kb = 40 + key_bits((uint64_t)ntile);
+    const int kb = kTileKeyShift + key_bits((uint64_t)ntile);
     tb = 0;
     SF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ckey.as<unsigned long long>(),
                                             ckey2.as<unsigned long long>(), cdesc.as<int2>(),
