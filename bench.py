@@ -446,7 +446,14 @@ def run_b200(args, cfg):
               file=sys.stderr)
 
     launches = L.sincfft_nnfft_launches_per_execute(ph, B) * args.steps
-    fp64_peak = 148 * 64 * 2 * (clk.max_mhz or 1965) * 1e6 / 1e12
+    fp64_peak, fp64_note = 148 * 64 * 2 * (clk.max_mhz or 1965) * 1e6 / 1e12, \
+        "derived: 148 SMs x 64 DFMA/clk x 2 flops x max SM clock"
+    pf = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(pf):
+        with open(pf) as fh:
+            fp64_peak, fp64_note = float(json.load(fh)["fp64_dfma_tflops"]), \
+                "measured: tools/fp64_peak.cu (DFMA microbenchmark on this pool's B200)"
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample_rate(cfg)
@@ -474,7 +481,7 @@ def run_b200(args, cfg):
                              "peak_tflops": fp64_peak,
                              "frac": flops[dom] / t_dom / 1e12 / fp64_peak,
                              "dfma_per_node": dfma_node,
-                             "peak_note": "148 SMs x 64 DFMA/clk x 2 flops x max SM clock"}},
+                             "peak_note": fp64_note}},
             "stage_ms": {n: float(stage[i]) for i, n in enumerate(names)},
             "plan_ms": plan_ms,
             "e2e": {"value": e2e_val, "unit": "nodes/s", "h2d_bytes_per_step": h2d,
