@@ -19,6 +19,10 @@
 //     point (REDG.ADD.F64, native on sm_100a) into the zeroed K-grid.
 #include "nnfft_impl.cuh"
 
+#ifndef SFB_SPREAD_WARP_FLUSH
+#define SFB_SPREAD_WARP_FLUSH 1  // measured: 0.479 -> 0.472 ms at config 3
+#endif
+
 namespace sfb {
 
 struct SpreadArgs {
@@ -63,9 +67,16 @@ __global__ void __launch_bounds__(kSpreadThreads, 2) k_spread(SpreadArgs a, WinC
   const int warp = threadIdx.x >> 5;
   const int nwarp = blockDim.x >> 5;
   const int col = blockIdx.y;
+  double2* my = acc + warp * SPAN;
+#if SFB_SPREAD_WARP_FLUSH
+  // warps are independent: each zeroes and flushes its own accumulator, so a
+  // warp that runs out of blocks never waits for the slowest one of the CTA
+  for (int i = lane; i < SPAN; i += 32) my[i] = make_double2(0.0, 0.0);
+  __syncwarp();
+#else
   for (int i = threadIdx.x; i < SPAN * nwarp; i += blockDim.x) acc[i] = make_double2(0.0, 0.0);
   __syncthreads();
-  double2* my = acc + warp * SPAN;
+#endif
   const int4 u = a.units[blockIdx.x];
   const int stride = nwarp * 32;
   int cb = u.y + warp * 32;
@@ -123,10 +134,22 @@ __global__ void __launch_bounds__(kSpreadThreads, 2) k_spread(SpreadArgs a, WinC
       pending &= ~__ballot_sync(0xffffffffu, leader);
     }
   }
-  __syncthreads();
   // flush: grid index of accumulator slot p is tile*kTile - (M-1) + p
   double2* grid = a.grid + (int64_t)col * a.K;
   const int64_t base = (int64_t)u.x * kTile - (M - 1);
+#if SFB_SPREAD_WARP_FLUSH
+  __syncwarp();
+  for (int p = lane; p < SPAN; p += 32) {
+    const double2 t = my[p];
+    const int64_t gi = base + p;
+    if (gi >= 0 && gi < a.K && (t.x != 0.0 || t.y != 0.0)) {
+      atomicAdd(&grid[gi].x, t.x);
+      atomicAdd(&grid[gi].y, t.y);
+    }
+  }
+  return;
+#endif
+  __syncthreads();
   for (int p = threadIdx.x; p < SPAN; p += blockDim.x) {
     double2 s = make_double2(0.0, 0.0);
     for (int w = 0; w < nwarp; ++w) {

@@ -215,3 +215,18 @@ def test_pipelined_host_async_two_streams():
     torch.cuda.synchronize()
     for k in range(2):
         assert relerr(outs[k].numpy(), (k + 1) * ref, (k + 1) * f) <= 1e-14
+
+
+@pytest.mark.slow
+def test_config4_full_size_columns_vs_oracle():
+    """BASELINE config 4 geometry at full size (N = 65536, M1 = M2 = 2^20,
+    m = 6), 32 columns through the column-vectorised path; four of them are
+    checked against the oracle applied column by column (the reference's
+    own batching)."""
+    v, x, f = nodes_and_coeffs(4, 1 << 20, 1 << 20, batch=32)
+    N, vs = sf.rescale_frequencies(65536, v, 2.0, 6)
+    plan = sf.nnfft_plan(N, vs, x, m1=6, m2=6)
+    out = sf.nnfft_trafo(plan, f)
+    tab = O.plan(N, vs, x, m1=6, m2=6)
+    for b in (0, 7, 19, 31):
+        assert relerr(out[:, b], O.trafo(tab, f[:, b]), f[:, b]) <= TOL, b
