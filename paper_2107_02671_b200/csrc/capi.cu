@@ -4,16 +4,38 @@
 // (pkg/src/sincfft/nnfft.py, fast_sinc.py); the ctypes shim in
 // paper_2107_02671_b200/_lib.py binds them and maps status codes to the
 // reference's exception classes (errors.py:4-13).
+#include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <vector>
 #include <new>
 #include <string>
 
 #include "../../include/sincfft_b200.h"
 #include "nnfft_impl.cuh"
 
+// Small transforms are launch-bound (configs 1-2: microseconds of GPU work
+// behind ~10 runtime calls), so device-pointer executes of small plans are
+// captured once per (f, out, batch) into a CUDA graph and replayed.
+struct GraphCache {
+  struct Entry {
+    const void* f;
+    void* out;
+    int64_t batch;
+    cudaGraphExec_t exec;
+  };
+  std::mutex mu;
+  std::vector<Entry> entries;  // most recent last, at most kMax
+  static constexpr size_t kMax = 8;
+  ~GraphCache() {
+    for (auto& e : entries) cudaGraphExecDestroy(e.exec);
+  }
+};
+
 struct sincfft_nnfft_plan_s {
   sfb::NnfftPlanImpl impl;
+  GraphCache graphs;
 };
 
 struct sincfft_sinc_plan_s {
@@ -194,6 +216,50 @@ void build_nnfft(sfb::NnfftPlanImpl& p, int64_t N, int64_t M1, int64_t M2, doubl
   sfb::build_plan(p, v_dev, x_dev, s);
 }
 
+bool use_graph(const sfb::NnfftPlanImpl& p, int64_t batch) {
+  static const bool off = getenv("SINCFFT_NO_GRAPHS") != nullptr;
+  return !off && (p.g.M1 + p.g.M2) * batch <= ((int64_t)1 << 19);
+}
+
+void launch_graph(sincfft_nnfft_plan plan, const double2* f, double2* out, int64_t batch,
+                  cudaStream_t s) {
+  GraphCache& gc = plan->graphs;
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(gc.mu);
+    for (size_t i = 0; i < gc.entries.size(); ++i) {
+      if (gc.entries[i].f == f && gc.entries[i].out == out && gc.entries[i].batch == batch) {
+        exec = gc.entries[i].exec;
+        break;
+      }
+    }
+    if (!exec) {
+      cudaStream_t cs;
+      SF_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      cudaGraph_t graph = nullptr;
+      try {
+        SF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        sfb::run_execute(plan->impl, f, out, (int)batch, cs);
+        SF_CUDA(cudaStreamEndCapture(cs, &graph));
+        SF_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      } catch (...) {
+        cudaStreamEndCapture(cs, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        cudaStreamDestroy(cs);
+        throw;
+      }
+      cudaGraphDestroy(graph);
+      cudaStreamDestroy(cs);
+      if (gc.entries.size() == GraphCache::kMax) {
+        cudaGraphExecDestroy(gc.entries.front().exec);
+        gc.entries.erase(gc.entries.begin());
+      }
+      gc.entries.push_back({f, out, batch, exec});
+    }
+  }
+  SF_CUDA(cudaGraphLaunch(exec, s));
+}
+
 }  // namespace
 
 namespace sfb {
@@ -280,7 +346,9 @@ int sincfft_nnfft_execute(sincfft_nnfft_plan plan, const double* f, double* out,
     const size_t fb = sizeof(double2) * (size_t)p.g.M1 * batch;
     const size_t ob = sizeof(double2) * (size_t)p.g.M2 * batch;
     InBuf fin(f, fb, ptr_kind, s);
-    if (ptr_kind == SINCFFT_PTR_DEVICE) {
+    if (ptr_kind == SINCFFT_PTR_DEVICE && use_graph(p, batch)) {
+      launch_graph(plan, (const double2*)f, (double2*)out, batch, s);
+    } else if (ptr_kind == SINCFFT_PTR_DEVICE) {
       sfb::run_execute(p, (const double2*)fin.ptr, (double2*)out, (int)batch, s);
     } else {
       sfb::Scratch o(ob, s);
