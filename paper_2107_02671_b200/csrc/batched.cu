@@ -302,16 +302,21 @@ void run_execute_batched(const NnfftPlanImpl& p, const double2* f, double2* out,
                          cudaStream_t s, cudaEvent_t* ev) {
   const int64_t K = p.g.K, Ko = p.fft.Kout;
   Scratch gp(sizeof(double2) * (size_t)K * B, s);   // [K][B]
-  Scratch gc(sizeof(double2) * (size_t)K * B, s);   // [B][K]
+  const bool pm = fft_supports_point_major(p);
+  Scratch gc(pm ? 0 : sizeof(double2) * (size_t)K * B, s);   // [B][K]
   Scratch work(sizeof(double2) * (size_t)p.fft.work_elems() * B, s);
-  Scratch hc(sizeof(double2) * (size_t)Ko * B, s);  // [B][Kout]
+  Scratch hc(pm ? 0 : sizeof(double2) * (size_t)Ko * B, s);  // [B][Kout]
   Scratch hp(sizeof(double2) * (size_t)Ko * B, s);  // [Kout][B]
   if (ev) SF_CUDA(cudaEventRecord(ev[0], s));
   SF_DISPATCH(p.g.m1, spread_b_m, p, f, gp.as<double2>(), B, s);
   if (ev) SF_CUDA(cudaEventRecord(ev[1], s));
-  transpose(gp.as<double2>(), gc.as<double2>(), K, B, s);
-  run_fft(p, gc.as<double2>(), hc.as<double2>(), work.as<double2>(), B, s);
-  transpose(hc.as<double2>(), hp.as<double2>(), B, Ko, s);
+  if (fft_supports_point_major(p)) {
+    run_fft_point_major(p, gp.as<double2>(), hp.as<double2>(), work.as<double2>(), B, s);
+  } else {
+    transpose(gp.as<double2>(), gc.as<double2>(), K, B, s);
+    run_fft(p, gc.as<double2>(), hc.as<double2>(), work.as<double2>(), B, s);
+    transpose(hc.as<double2>(), hp.as<double2>(), B, Ko, s);
+  }
   if (ev) SF_CUDA(cudaEventRecord(ev[2], s));
   SF_DISPATCH(p.g.m2, gather_b_m, p, hp.as<double2>(), out, B, s);
   if (ev) SF_CUDA(cudaEventRecord(ev[3], s));

@@ -321,6 +321,145 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv(FftArgs a) {
   }
 }
 
+// ------------------------------------------- batch-minor (point-major) I/O
+// Same three Bluestein passes for B columns stored point-major: element
+// (n, b) at n*B + b (the layout of the column-vectorised spread/gather,
+// batched.cu).  A CTA interleaves CB consecutive COLUMNS in shared memory
+// (instead of CB consecutive n1), so every global row access is CB*16
+// contiguous bytes and no transposes are needed around the FFT.
+struct FftBArgs {
+  FftArgs a;
+  int B;
+  int cb_log2_col, cb_log2_row;
+};
+
+__global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd_b(FftBArgs x) {
+  extern __shared__ double2 sm[];
+  const FftArgs& a = x.a;
+  const int CB = 1 << x.cb_log2_col;
+  const int64_t n1 = blockIdx.x;
+  const int b0 = blockIdx.y * CB;
+  const int L2 = (int)a.L2;
+  const int n_el = L2 << x.cb_log2_col;
+  const int T = blockDim.x;
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int b = b0 + (e & (CB - 1));
+      const int64_t n = n1 + a.L1 * (int64_t)(e >> x.cb_log2_col);
+      v[u] = make_double2(0.0, 0.0);
+      if (e < n_el && b < x.B && n < a.K) v[u] = cmul(__ldg(a.g + n * x.B + b), __ldg(a.P + n));
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = v[u];
+  }
+  __syncthreads();
+  fft_dif(sm, x.cb_log2_col, a.st2, a.tw2);
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 w[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      w[u] = make_double2(1.0, 0.0);
+      if (e < n_el) w[u] = wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)__ldg(a.rev2 + (e >> x.cb_log2_col)));
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int b = b0 + (e & (CB - 1));
+      if (e < n_el && b < x.B)
+        a.Y[(n1 + a.L1 * (int64_t)(e >> x.cb_log2_col)) * x.B + b] = cmul(sm[spad(e)], w[u]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, SFB_FFT_MINB) k_rowmul_b(FftBArgs x) {
+  extern __shared__ double2 sm[];
+  const FftArgs& a = x.a;
+  const int CB = 1 << x.cb_log2_row;
+  const int64_t p = blockIdx.x;
+  const int b0 = blockIdx.y * CB;
+  const int L1 = (int)a.L1;
+  const int n_el = L1 << x.cb_log2_row;
+  const int T = blockDim.x;
+  double2* Y = a.Y + p * a.L1 * x.B;
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int b = b0 + (e & (CB - 1));
+      v[u] = make_double2(0.0, 0.0);
+      if (e < n_el && b < x.B) v[u] = Y[(int64_t)(e >> x.cb_log2_row) * x.B + b];
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = v[u];
+  }
+  __syncthreads();
+  fft_dif(sm, x.cb_log2_row, a.st1, a.tw1);
+  const double2* Bh = a.Bhat + p * a.L1;
+  for (int e = threadIdx.x; e < n_el; e += T)
+    sm[spad(e)] = cconj(cmul(sm[spad(e)], __ldg(Bh + (e >> x.cb_log2_row))));
+  __syncthreads();
+  fft_dit(sm, x.cb_log2_row, a.st1, a.tw1);
+  for (int e = threadIdx.x; e < n_el; e += T) {
+    const int b = b0 + (e & (CB - 1));
+    if (b < x.B) Y[(int64_t)(e >> x.cb_log2_row) * x.B + b] = cconj(sm[spad(e)]);
+  }
+}
+
+__global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv_b(FftBArgs x) {
+  extern __shared__ double2 sm[];
+  const FftArgs& a = x.a;
+  const int CB = 1 << x.cb_log2_col;
+  const int64_t n1 = blockIdx.x;
+  const int b0 = blockIdx.y * CB;
+  const int L2 = (int)a.L2;
+  const int n_el = L2 << x.cb_log2_col;
+  const int T = blockDim.x;
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 v[kU], w[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int b = b0 + (e & (CB - 1));
+      const int pp = e >> x.cb_log2_col;
+      v[u] = make_double2(0.0, 0.0);
+      w[u] = make_double2(1.0, 0.0);
+      if (e < n_el && b < x.B) {
+        v[u] = a.Y[(n1 + a.L1 * (int64_t)pp) * x.B + b];
+        w[u] = wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)__ldg(a.rev2 + pp));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = cmul(cconj(v[u]), w[u]);
+  }
+  __syncthreads();
+  fft_dit(sm, x.cb_log2_col, a.st2, a.tw2);
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
+    double2 qv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int64_t k = n1 + a.L1 * (int64_t)(e >> x.cb_log2_col);
+      qv[u] = make_double2(0.0, 0.0);
+      if (e < n_el && k < a.Kout) qv[u] = __ldg(a.Q + k);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * T;
+      const int b = b0 + (e & (CB - 1));
+      const int64_t k = n1 + a.L1 * (int64_t)(e >> x.cb_log2_col);
+      if (e < n_el && b < x.B && k < a.Kout) a.h[k * x.B + b] = cmul(cconj(sm[spad(e)]), qv[u]);
+    }
+  }
+}
+
 // ------------------------------------------------------ direct four-step
 // n = P n1 + n2 (n1 < A, n2 < P),  k = k1 + A k2:
 //   X[k1 + A k2] = sum_n2 W_P^{n2 k2} [ W_N2^{n2 k1} sum_n1 x[P n1 + n2] W_A^{n1 k1} ]
@@ -746,6 +885,9 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_colfwd<IN_PLAIN>, smem_bytes(kColElems));
   set_smem(k_rowmul, smem_bytes(kRowMax));
   set_smem(k_colinv, smem_bytes(kColElems));
+  set_smem(k_colfwd_b, smem_bytes(kColElems));
+  set_smem(k_rowmul_b, smem_bytes(kColElems));
+  set_smem(k_colinv_b, smem_bytes(kColElems));
   FftPlan& f = p.fft;
   const Geometry& g = p.g;
   const int64_t Lmin = g.K + f.Kout - 1;
@@ -849,6 +991,34 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
     SF_LAUNCH_CHECK();
   }
   SF_CUDA(cudaStreamSynchronize(s));  // b is released at scope exit
+}
+
+bool fft_supports_point_major(const NnfftPlanImpl& p) {
+  return !p.fft.direct && !p.fft.single;
+}
+
+void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work,
+                         int batch, cudaStream_t s) {
+  const FftPlan& f = p.fft;
+  FftBArgs x{};
+  x.a = make_args(p);
+  x.a.g = grid;
+  x.a.h = h;
+  x.a.Y = work;
+  x.B = batch;
+  int cc = 8, cr = 8;
+  while (cc > 1 && cc * f.L2 > kColElems) cc >>= 1;
+  while (cr > 1 && cr * f.L1 > kColElems) cr >>= 1;
+  x.cb_log2_col = log2i(cc);
+  x.cb_log2_row = log2i(cr);
+  const size_t smc = smem_bytes(f.L2 * cc), smr = smem_bytes(f.L1 * cr);
+  const dim3 gc((unsigned)f.L1, (unsigned)ceil_div(batch, cc));
+  k_colfwd_b<<<gc, 256, smc, s>>>(x);
+  SF_LAUNCH_CHECK();
+  k_rowmul_b<<<dim3((unsigned)f.L2, (unsigned)ceil_div(batch, cr)), 256, smr, s>>>(x);
+  SF_LAUNCH_CHECK();
+  k_colinv_b<<<gc, 256, smc, s>>>(x);
+  SF_LAUNCH_CHECK();
 }
 
 void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work, int batch,

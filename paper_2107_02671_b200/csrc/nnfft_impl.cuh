@@ -139,6 +139,10 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t stream);
 // grid[batch][K] -> h[batch][Kout] (work: batch*L complex scratch)
 void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work, int batch,
              cudaStream_t stream);
+// point-major variant: grid[K][batch] -> h[Kout][batch] (Bluestein path only)
+bool fft_supports_point_major(const NnfftPlanImpl& p);
+void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work,
+                         int batch, cudaStream_t stream);
 
 // ----- spread.cu / gather.cu
 // f: (M1, batch) row-major; grid[batch][K] is zeroed and accumulated.
