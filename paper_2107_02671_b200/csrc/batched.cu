@@ -194,24 +194,31 @@ __global__ void __launch_bounds__(kThreadsB, 4) k_gather_b(GatherBArgs a, WinCoe
     }
     __syncwarp();
     const int n = (int)min((int64_t)32, j1 - jb);
-    for (int s = 0; s < n; ++s) {
-      const int k0 = __shfl_sync(0xffffffffu, kl, s);
-      const int d = __shfl_sync(0xffffffffu, dst, s);
-      const double scs = __shfl_sync(0xffffffffu, sc, s);
-      if (k0 != kbase) {
-        if (k0 < kbase || k0 >= kbase + 2 * M) {  // (re)load the whole window
+    // runs of targets sharing one window start k0: the register window only
+    // moves between runs, so the inner loop leaves hr untouched (a window
+    // update inside every iteration made ptxas copy all of hr per target)
+    const int kprev = __shfl_up_sync(0xffffffffu, kl, 1);
+    unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || kl != kprev) & ((n < 32) ? ((1u << n) - 1u) : 0xffffffffu);
+    while (starts) {
+      const int s0 = __ffs(starts) - 1;
+      starts &= starts - 1;
+      const int s1 = starts ? __ffs(starts) - 1 : n;
+      const int k0 = __shfl_sync(0xffffffffu, kl, s0);
+      if (k0 < kbase || k0 >= kbase + 2 * M) {  // (re)load the whole window
 #pragma unroll
-          for (int i = 0; i < 2 * M; ++i) hr[i] = row(k0 + i);
-          kbase = k0;
-        } else {
-          do {  // warp-uniform, < 2M steps
+        for (int i = 0; i < 2 * M; ++i) hr[i] = row(k0 + i);
+        kbase = k0;
+      } else {
+        while (kbase < k0) {  // warp-uniform, < 2M steps
 #pragma unroll
-            for (int i = 0; i < 2 * M - 1; ++i) hr[i] = hr[i + 1];
-            hr[2 * M - 1] = row(kbase + 2 * M);
-            ++kbase;
-          } while (kbase < k0);
+          for (int i = 0; i < 2 * M - 1; ++i) hr[i] = hr[i + 1];
+          hr[2 * M - 1] = row(kbase + 2 * M);
+          ++kbase;
         }
       }
+      for (int s = s0; s < s1; ++s) {
+      const int d = __shfl_sync(0xffffffffu, dst, s);
+      const double scs = __shfl_sync(0xffffffffu, sc, s);
       const double* wr = wl + s * WS;
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
@@ -221,6 +228,7 @@ __global__ void __launch_bounds__(kThreadsB, 4) k_gather_b(GatherBArgs a, WinCoe
         acc.y = fma(hr[i].y, wi, acc.y);
       }
       if (colok) ocol[(int64_t)d * a.B] = make_double2(acc.x * scs, acc.y * scs);
+      }
     }
     __syncwarp();
   }
