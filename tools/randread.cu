@@ -1,0 +1,88 @@
+// randread.cu -- microbenchmark: cost of the spread's random f gather.
+// Reads n double2 from a 256 MiB array through an index vector that is
+// (a) a full random permutation, (b) random inside windows of W elements
+// (the "slice" orderings), (c) sequential; and fp64 RED throughput into a
+// 33.5 MB grid.  Prints ms per pass; run under ncu for dram bytes.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
+#include <numeric>
+#include <random>
+#include <cuda_runtime.h>
+
+__global__ void k_read(const double2* __restrict__ f, const int* __restrict__ idx, int n,
+                       double2* out) {
+  double2 acc = make_double2(0, 0);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double2 v = __ldg(f + idx[i]);
+    acc.x += v.x;
+    acc.y += v.y;
+  }
+  if (acc.x == 12345.0) out[0] = acc;
+}
+
+__global__ void k_red(double* g, const int* __restrict__ idx, int n, int K) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int p = idx[i] % K;
+    atomicAdd(g + 2 * (size_t)p, 1.0);
+    atomicAdd(g + 2 * (size_t)p + 1, 1.0);
+  }
+}
+
+int main() {
+  const int n = 1 << 24;
+  std::vector<int> h(n);
+  double2* f;
+  int* idx;
+  double2* out;
+  double* g;
+  const int K = 2097184;
+  cudaMalloc(&f, sizeof(double2) * n);
+  cudaMalloc(&idx, sizeof(int) * n);
+  cudaMalloc(&out, 16);
+  cudaMalloc(&g, 16 * (size_t)K);
+  cudaMemset(f, 0, sizeof(double2) * n);
+  cudaMemset(g, 0, 16 * (size_t)K);
+  std::mt19937 rng(1);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const long windows[] = {0, 1L << 24, 1L << 23, 1L << 22, 1L << 21, 1L << 20, 1L << 16};
+  for (long W : windows) {
+    std::iota(h.begin(), h.end(), 0);
+    if (W > 0)
+      for (long s = 0; s < n; s += W) std::shuffle(h.begin() + s, h.begin() + std::min<long>(n, s + W), rng);
+    cudaMemcpy(idx, h.data(), sizeof(int) * n, cudaMemcpyHostToDevice);
+    float best = 1e9;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(a);
+      k_read<<<148 * 8, 256>>>(f, idx, n, out);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      best = std::min(best, ms);
+    }
+    printf("read window=%ld ms=%.4f  (%.1f GB/s useful)\n", W, best, 16.0 * n / best / 1e6);
+  }
+  // RED: coalesced-ish (index i) vs random over the grid
+  for (int mode = 0; mode < 2; ++mode) {
+    std::iota(h.begin(), h.end(), 0);
+    if (mode) std::shuffle(h.begin(), h.end(), rng);
+    cudaMemcpy(idx, h.data(), sizeof(int) * n, cudaMemcpyHostToDevice);
+    float best = 1e9;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(a);
+      k_red<<<148 * 8, 256>>>(g, idx, n, K);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      best = std::min(best, ms);
+    }
+    printf("red mode=%s n=%d x2 ms=%.4f  (%.1f G red/s)\n", mode ? "random" : "sequential", n, best,
+           2.0 * n / best / 1e6);
+  }
+  return 0;
+}
