@@ -389,9 +389,10 @@ def run_b200(args, cfg):
 
     # end to end through the C ABI with pinned HOST buffers: every step copies
     # its f from pinned host memory and its output back (SINCFFT_PTR_HOST_ASYNC);
-    # successive steps alternate between two streams so the H2D of step k+1,
-    # the kernels and the D2H of step k overlap (full-duplex PCIe)
-    nbuf = 2
+    # successive steps rotate over --e2e-streams streams so the H2D of step
+    # k+1, the kernels of step k and the D2H of step k-1 overlap (full-duplex
+    # PCIe; 4 streams measured 5.95 ms vs 6.42 with 2 at config 3)
+    nbuf = args.e2e_streams
     h_f = [torch.from_numpy(fshard).pin_memory() for _ in range(nbuf)]
     h_out = [torch.empty(tuple(d_out.shape), dtype=torch.complex128).pin_memory()
              for _ in range(nbuf)]
@@ -445,6 +446,33 @@ def run_b200(args, cfg):
         print(f"WARNING: e2e output deviates from the device-resident output by {e2e_dev:.3e}",
               file=sys.stderr)
 
+    # the link floor of that pipeline: the same H2D and D2H bytes copied
+    # concurrently on two streams with no kernels (PCIe full duplex)
+    pcie_ms = None
+    if world == 1:
+        cs = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        d_in = torch.empty_like(d_f)
+
+        def copies():
+            with torch.cuda.stream(cs[0]):
+                d_in.copy_(h_f[0], non_blocking=True)
+            with torch.cuda.stream(cs[1]):
+                h_out.copy_(d_out, non_blocking=True)  # already checked above
+
+        copies()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for c in cs:
+            c.wait_event(ev0)
+        for _ in range(5):
+            copies()
+        for c in cs:
+            stream.wait_stream(c)
+        ev1.record(stream)
+        ev1.synchronize()
+        pcie_ms = ev0.elapsed_time(ev1) / 5
+        del d_in
+
     launches = L.sincfft_nnfft_launches_per_execute(ph, B) * args.steps
     fp64_peak, fp64_note = 148 * 64 * 2 * (clk.max_mhz or 1965) * 1e6 / 1e12, \
         "derived: 148 SMs x 64 DFMA/clk x 2 flops x max SM clock"
@@ -486,8 +514,9 @@ def run_b200(args, cfg):
             "plan_ms": plan_ms,
             "e2e": {"value": e2e_val, "unit": "nodes/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                    "mode": "sincfft_nnfft_execute(host pinned, PTR_HOST_ASYNC), 2 streams "
-                            "alternating: H2D(k+1) || kernels || D2H(k)"},
+                    "pcie_floor_ms": pcie_ms,
+                    "mode": f"sincfft_nnfft_execute(host pinned, PTR_HOST_ASYNC), {nbuf} streams "
+                            "round-robin: H2D(k+1) || kernels(k) || D2H(k-1)"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
@@ -509,6 +538,8 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="3")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--e2e-streams", type=int, default=4,
+                    help="host-buffer pipeline depth of the e2e leg (streams in flight)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: functional tests)")
     ap.add_argument("--same-device", action="store_true",
