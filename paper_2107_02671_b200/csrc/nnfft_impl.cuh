@@ -29,29 +29,29 @@ struct Geometry {
 // Sources, sorted by cell c = floor(N1 v) + K/2 and grouped into "chunks" of
 // at most kChunk sources of one cell.  Chunks of a tile of kTile cells are
 // ordered rank-major (chunk rank within its cell, then cell), so a warp's 32
-// consecutive chunks almost always have pairwise distinct cells.  Work units
-// (one CTA each) are ranges of at most kUnitChunks chunks of one tile.  The
-// sources are stored in chunk-slot order (chunk c owns slots [4c, 4c+4)), so
-// a lane's positions and permutation load as two vectors without first
-// reading a descriptor.
+// consecutive chunks almost always have pairwise distinct cells, and padded
+// with empty chunks to whole "blocks" of 32 (one chunk per lane), so a block
+// belongs to one tile.  The sources are stored in chunk-slot order (chunk c
+// owns slots [4c, 4c+4)), so a lane's positions and permutation are two
+// contiguous 16-byte records.  The spread kernel is persistent: each warp
+// walks a contiguous range of blocks (spread.cu).
 #ifndef SFB_SPREAD_TILE
 #define SFB_SPREAD_TILE 256
 #endif
 constexpr int kTile = SFB_SPREAD_TILE;
 constexpr int kChunk = 4;
-#ifndef SFB_UNIT_CHUNKS
-#define SFB_UNIT_CHUNKS 1024
-#endif
-constexpr int kUnitChunks = SFB_UNIT_CHUNKS;
-constexpr int kSpreadThreads = 256;
+constexpr int kBlockChunks = 32;  // chunks per block = lanes per warp
+constexpr int kSpreadWarps = 8;   // warps per spread CTA (independent workers)
 
 struct SpreadPlan {
-  DevArray<double> pos;   // fl(N1 * v) in chunk-slot order    [n_chunks * kChunk]
-  DevArray<int> perm;     // original source index, slot order [n_chunks * kChunk]
-  DevArray<int> info;     // (local cell << 8) | count          [n_chunks]
-  DevArray<int2> chunks;  // plan-time only: {first sorted index, info}
-  DevArray<int4> units;   // {tile, chunk begin, chunk end, 0}
-  int64_t n_chunks = 0, n_units = 0;
+  DevArray<double> pos;    // fl(N1 * v) in chunk-slot order    [n_blocks * 32 * kChunk]
+  DevArray<int> perm;      // original source index, slot order [n_blocks * 32 * kChunk]
+  DevArray<int> info;      // (local cell << 8) | count, 0 = empty [n_blocks * 32]
+  DevArray<int> blk_tile;  // tile of each block                  [n_blocks]
+  DevArray<int2> chunks;   // plan-time only: {first sorted index, info}
+  DevArray<int64_t> wstart; // first block of each spread warp         [n_ctas * 8 + 1]
+  int64_t n_chunks = 0, n_blocks = 0;
+  int n_sms = 148, n_ctas = 1;
   // batched path (batched.cu): cell-sorted sources and per-128-cell tile starts
   DevArray<double> bpos;
   DevArray<int> bperm;

@@ -146,16 +146,21 @@ __global__ void k_chunk_emit(const int* start, const int* nch, const int* off, i
   }
 }
 
-__global__ void k_chunk_slots(const int2* chunks, int64_t n, const double* pos, const int* perm,
-                              double* spos, int* sperm, int* info) {
+// chunk c (sorted order, tile t = key >> kTileKeyShift) goes to padded chunk
+// boff[t] * 32 + (c - tstart[t]); padding chunks stay zero (count 0)
+__global__ void k_chunk_slots(const int2* chunks, const unsigned long long* key, int64_t n,
+                              const int* tstart, const int* boff, const double* pos,
+                              const int* perm, double* spos, int* sperm, int* info) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
+  const int t = (int)(key[c] >> kTileKeyShift);
+  const int64_t q = (int64_t)boff[t] * kBlockChunks + (c - tstart[t]);
   const int2 d = chunks[c];
   const int cnt = d.y & 255;
-  info[c] = d.y;
+  info[q] = d.y;
   for (int s = 0; s < kChunk; ++s) {
-    spos[c * kChunk + s] = s < cnt ? pos[d.x + s] : 0.5;
-    sperm[c * kChunk + s] = s < cnt ? perm[d.x + s] : 0;
+    spos[q * kChunk + s] = s < cnt ? pos[d.x + s] : 0.5;
+    sperm[q * kChunk + s] = s < cnt ? perm[d.x + s] : 0;
   }
 }
 
@@ -178,20 +183,53 @@ __global__ void k_tile_bounds(const unsigned long long* key, int64_t n, int64_t 
   tstart[t] = (int)lo;
 }
 
-__global__ void k_unit_counts(const int* tstart, int64_t ntile, int* nu) {
+__global__ void k_block_counts(const int* tstart, int64_t ntile, int* nb) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= ntile) return;
-  nu[t] = (tstart[t + 1] - tstart[t] + kUnitChunks - 1) / kUnitChunks;
+  nb[t] = (tstart[t + 1] - tstart[t] + kBlockChunks - 1) / kBlockChunks;
 }
 
-__global__ void k_unit_emit(const int* tstart, const int* nu, const int* off, int64_t ntile,
-                            int4* units) {
+__global__ void k_block_emit(const int* nb, const int* boff, int64_t ntile, int* blk_tile) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= ntile) return;
-  for (int u = 0; u < nu[t]; ++u) {
-    const int b = tstart[t] + u * kUnitChunks;
-    units[off[t] + u] = make_int4((int)t, b, min(b + kUnitChunks, tstart[t + 1]), 0);
+  for (int j = 0; j < nb[t]; ++j) blk_tile[boff[t] + j] = (int)t;
+}
+
+// Estimated cost of each 32-chunk block for the spread's static warp ranges
+// (spread.cu): window pairs (4 units each for the lane that needs the most)
+// plus accumulator rounds (1 unit each; a single-cell block is one butterfly).
+// One warp per block.
+__global__ void k_block_cost(const int* info, int64_t nblk, long long* cost) {
+  const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= nblk) return;
+  const int in = info[b * kBlockChunks + lane];
+  const int cnt = in & 255, lc = in >> 8;
+  const int pairs = __reduce_max_sync(0xffffffffu, cnt > 2 ? 2 : cnt > 0 ? 1 : 0);
+  int same = 0;
+  __match_all_sync(0xffffffffu, cnt > 0 ? lc : -1 - lane, &same);
+  const unsigned peers = __match_any_sync(0xffffffffu, cnt > 0 ? lc : -1 - lane);
+  const int rounds = same ? 2 : __reduce_max_sync(0xffffffffu, __popc(peers));
+  if (lane == 0) cost[b] = 4 * pairs + rounds;
+}
+
+// first block of warp w: the first b with prefix cost[0..b] > w * total / W
+__global__ void k_warp_starts(const long long* incl, int64_t nblk, int64_t W, int64_t* wstart) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w > W) return;
+  if (w == W) {
+    wstart[w] = nblk;
+    return;
   }
+  const long long total = incl[nblk - 1];
+  const long long target = (long long)((double)total * (double)w / (double)W);
+  int64_t lo = 0, hi = nblk;  // first b with incl[b] > target
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (incl[mid] <= target) lo = mid + 1;
+    else hi = mid;
+  }
+  wstart[w] = w == 0 ? 0 : lo;
 }
 
 // target keys: (original-index slice, floor(N2 * xs) + N2), xs = x * (N/N1)
@@ -428,17 +466,18 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
                                               ckey2.as<unsigned long long>(), cdesc.as<int2>(),
                                               p.sp.chunks.p, (int)nchunks, 0, kb, s));
     }
-    Scratch tstart(sizeof(int) * (ntile + 1), s), nu(sizeof(int) * ntile, s),
-        uoff(sizeof(int) * (ntile + 1), s);
+    Scratch tstart(sizeof(int) * (ntile + 1), s), nb(sizeof(int) * ntile, s),
+        boff(sizeof(int) * (ntile + 1), s);
     k_tile_bounds<<<blocks(ntile + 1), 256, 0, s>>>(ckey2.as<unsigned long long>(), nchunks, ntile,
                                                     tstart.as<int>());
-    k_unit_counts<<<blocks(ntile), 256, 0, s>>>(tstart.as<int>(), ntile, nu.as<int>());
+    k_block_counts<<<blocks(ntile), 256, 0, s>>>(tstart.as<int>(), ntile, nb.as<int>());
     SF_LAUNCH_CHECK();
-    p.sp.n_units = exclusive_scan(nu.as<int>(), uoff.as<int>(), ntile, s);
-    p.sp.units.alloc(p.sp.n_units);
-    k_unit_emit<<<blocks(ntile), 256, 0, s>>>(tstart.as<int>(), nu.as<int>(), uoff.as<int>(), ntile,
-                                              p.sp.units.p);
+    p.sp.n_blocks = exclusive_scan(nb.as<int>(), boff.as<int>(), ntile, s);
+    p.sp.blk_tile.alloc(std::max<int64_t>(p.sp.n_blocks, 1));
+    k_block_emit<<<blocks(ntile), 256, 0, s>>>(nb.as<int>(), boff.as<int>(), ntile,
+                                               p.sp.blk_tile.p);
     SF_LAUNCH_CHECK();
+    SF_CUDA(cudaDeviceGetAttribute(&p.sp.n_sms, cudaDevAttrMultiProcessorCount, p.device));
     // batched path: keep the cell-sorted arrays and the 128-cell tile starts
     {
       const int64_t ntb = ceil_div(K, 128);
@@ -446,13 +485,48 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
       k_tile_starts<<<blocks(ntb + 1), 256, 0, s>>>(cstart.as<int>(), K, 128, ntb, p.sp.btile.p);
       SF_LAUNCH_CHECK();
     }
-    // re-lay the sorted sources out in chunk-slot order (kChunk slots per chunk)
-    DevArray<double> spos(nchunks * kChunk);
-    DevArray<int> sperm(nchunks * kChunk);
-    p.sp.info.alloc(nchunks);
-    k_chunk_slots<<<blocks(nchunks), 256, 0, s>>>(p.sp.chunks.p, nchunks, p.sp.pos.p, p.sp.perm.p,
-                                                  spos.p, sperm.p, p.sp.info.p);
+    // re-lay the sorted sources out in chunk-slot order (kChunk slots per
+    // chunk, 32 chunks per block, blocks padded with empty chunks)
+    const int64_t npad = std::max<int64_t>(p.sp.n_blocks, 1) * kBlockChunks;
+    DevArray<double> spos(npad * kChunk);
+    DevArray<int> sperm(npad * kChunk);
+    p.sp.info.alloc(npad);
+    SF_CUDA(cudaMemsetAsync(spos.p, 0, sizeof(double) * npad * kChunk, s));
+    SF_CUDA(cudaMemsetAsync(sperm.p, 0, sizeof(int) * npad * kChunk, s));
+    SF_CUDA(cudaMemsetAsync(p.sp.info.p, 0, sizeof(int) * npad, s));
+    k_chunk_slots<<<blocks(nchunks), 256, 0, s>>>(p.sp.chunks.p, ckey2.as<unsigned long long>(),
+                                                  nchunks, tstart.as<int>(), boff.as<int>(),
+                                                  p.sp.pos.p, p.sp.perm.p, spos.p, sperm.p,
+                                                  p.sp.info.p);
     SF_LAUNCH_CHECK();
+    // static cost-balanced warp ranges of the persistent spread kernel
+    {
+      const int64_t nblk = p.sp.n_blocks;
+      const char* e1 = getenv("SFB_SPREAD_CTAS_PER_SM");
+      const char* e2 = getenv("SFB_SPREAD_BLOCKS_PER_WARP");
+      const int cps = e1 ? std::max(1, atoi(e1)) : 2;
+      const int bpw = e2 ? std::max(1, atoi(e2)) : 1;  // 1 measured best (configs 1-3, 5)
+      p.sp.n_ctas = (int)std::max<int64_t>(
+          1, std::min<int64_t>(cps * (int64_t)p.sp.n_sms, ceil_div(nblk, bpw * kSpreadWarps)));
+      const int64_t W = (int64_t)p.sp.n_ctas * kSpreadWarps;
+      p.sp.wstart.alloc(W + 1);
+      if (nblk > 0) {
+        Scratch cost(sizeof(long long) * nblk, s), incl(sizeof(long long) * nblk, s);
+        k_block_cost<<<blocks(nblk * 32), 256, 0, s>>>(p.sp.info.p, nblk, cost.as<long long>());
+        SF_LAUNCH_CHECK();
+        size_t tb3 = 0;
+        SF_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb3, cost.as<long long>(),
+                                              incl.as<long long>(), (int)nblk, s));
+        Scratch t(tb3, s);
+        SF_CUDA(cub::DeviceScan::InclusiveSum(t.p, tb3, cost.as<long long>(),
+                                              incl.as<long long>(), (int)nblk, s));
+        k_warp_starts<<<blocks(W + 1), 256, 0, s>>>(incl.as<long long>(), nblk, W,
+                                                    p.sp.wstart.p);
+        SF_LAUNCH_CHECK();
+      } else {
+        SF_CUDA(cudaMemsetAsync(p.sp.wstart.p, 0, sizeof(int64_t) * (W + 1), s));
+      }
+    }
     SF_CUDA(cudaStreamSynchronize(s));
     p.sp.bpos = std::move(p.sp.pos);
     p.sp.bperm = std::move(p.sp.perm);

@@ -11,167 +11,238 @@
 //   * sources are sorted by cell at plan time and cut into chunks of <= 4
 //     sources of ONE cell; a lane owns a chunk and accumulates its 2m taps in
 //     registers (window from the per-tap polynomials, window.cuh);
-//   * a CTA owns a work unit (<= 1024 chunks of one 256-cell tile); each warp
-//     has a private shared-memory accumulator for the tile plus halo and adds
-//     its lanes' registers there; lanes with equal cells (rare by the
-//     rank-major chunk order) are serialised by __match_any_sync rounds;
-//   * warps' accumulators are summed and flushed with one fp64 RED per grid
-//     point (REDG.ADD.F64, native on sm_100a) into the zeroed K-grid.
+//   * chunks come in blocks of 32 (one per lane) of one 256-cell tile; the
+//     kernel is persistent and every warp is an independent worker over a
+//     contiguous range of blocks, with a private shared-memory accumulator
+//     for its current tile (plus halo) that it flushes with one fp64 RED per
+//     touched grid point (REDG.ADD.F64, native on sm_100a) when the tile
+//     changes -- a tile is flushed by the one or two warps that cover it;
+//   * lanes with equal cells in one block (rare by the rank-major chunk
+//     order) are serialised by __match_any_sync rounds;
+//   * the loads are a cp.async pipeline into per-warp shared-memory rings:
+//     block descriptors (positions, permutation, counts) two blocks ahead and
+//     the random 16-byte f gather one block ahead, so the f latency (the
+//     spread's floor: ~97 DRAM bytes per 16-byte read at config 3, see
+//     tools/randread.cu) overlaps a whole block of window arithmetic and no
+//     registers are held for prefetching.
 #include "nnfft_impl.cuh"
 
-#ifndef SFB_SPREAD_WARP_FLUSH
-#define SFB_SPREAD_WARP_FLUSH 1  // measured: 0.479 -> 0.472 ms at config 3
-#endif
+#include <atomic>
+#include <type_traits>
 
 namespace sfb {
 
 struct SpreadArgs {
-  const double* pos;    // slot order
-  const int* perm;      // slot order
-  const int* info;      // per chunk
-  const int4* units;
-  const void* f;        // complex (M1, batch) row-major, or real (M1)
-  double2* grid;        // [batch][K]
-  int64_t K;
+  const double* pos;     // slot order, [n_blocks * 32 * 4]
+  const int* perm;       // slot order
+  const int* info;       // per chunk
+  const int* blk_tile;   // per block
+  const int64_t* wstart; // first block of each warp
+  const void* f;         // complex (M1, batch) row-major, or real (M1)
+  double2* grid;         // [batch][K]
+  int64_t K, n_blocks;
   int batch;
 };
 
-static_assert(kChunk == 4, "slot loads assume 4 sources per chunk");
+static_assert(kChunk == 4, "slot records assume 4 sources per chunk");
+static_assert(kBlockChunks == 32, "one chunk per lane");
 
-struct ChunkLoad {
-  int info;
-  double2 p01, p23;  // positions of slots 0..3
-  int4 perm;
+constexpr int kDescStages = 3;  // descriptor ring depth (blocks)
+constexpr int kFStages = 2;     // f ring depth (blocks)
+
+// per-warp shared-memory state; slot-major so every lane access is a
+// conflict-free consecutive 16-byte (or 8/4-byte) record
+template <int M, bool REAL>
+struct WarpSmem {
+  using FT = typename std::conditional<REAL, double, double2>::type;
+  static constexpr int SPAN = kTile + 2 * M - 1;
+  double2 acc[SPAN];
+  double2 pos[kDescStages][2][32];  // slots {0,1}, {2,3}
+  int4 perm[kDescStages][32];
+  int info[kDescStages][32];
+  FT f[kFStages][kChunk][32];
 };
 
-__device__ __forceinline__ ChunkLoad load_chunk(const SpreadArgs& a, int ci, bool valid) {
-  ChunkLoad c;
-  c.info = 0;
-  c.p01 = c.p23 = make_double2(0.5, 0.5);
-  c.perm = make_int4(0, 0, 0, 0);
-  if (valid) {
-    c.info = __ldg(a.info + ci);
-    const double2* pp = reinterpret_cast<const double2*>(a.pos) + 2 * (int64_t)ci;
-    c.p01 = __ldg(pp);
-    c.p23 = __ldg(pp + 1);
-    c.perm = __ldg(reinterpret_cast<const int4*>(a.perm) + ci);
+template <bool REAL, class W>
+__device__ __forceinline__ void issue_desc(const SpreadArgs& a, W& S, int64_t b, int64_t b1,
+                                           int st, int lane) {
+  if (b < b1) {
+    const int64_t ci = b * kBlockChunks + lane;
+    cp_async16(&S.pos[st][0][lane], a.pos + ci * kChunk);
+    cp_async16(&S.pos[st][1][lane], a.pos + ci * kChunk + 2);
+    cp_async16(&S.perm[st][lane], a.perm + ci * kChunk);
+    cp_async4(&S.info[st][lane], a.info + ci);
   }
-  return c;
+  cp_async_commit();
+}
+
+template <bool REAL, class W>
+__device__ __forceinline__ void issue_f(const SpreadArgs& a, W& S, bool live, int st_d, int st_f,
+                                        int col, int lane) {
+  if (live) {
+    const int cnt = S.info[st_d][lane] & 255;
+    const int4 pm = S.perm[st_d][lane];
+    const int src[kChunk] = {pm.x, pm.y, pm.z, pm.w};
+#pragma unroll
+    for (int s = 0; s < kChunk; ++s) {
+      if (REAL) {
+        const double* fp = static_cast<const double*>(a.f) + (s < cnt ? src[s] : 0);
+        cp_async8z(&S.f[st_f][s][lane], fp, s < cnt ? 8 : 0);
+      } else {
+        const double2* fp =
+            static_cast<const double2*>(a.f) + (s < cnt ? (int64_t)src[s] * a.batch + col : 0);
+        cp_async16z(&S.f[st_f][s][lane], fp, s < cnt ? 16 : 0);
+      }
+    }
+  }
+  cp_async_commit();
+}
+
+template <int M, class W>
+__device__ __forceinline__ void flush_tile(const SpreadArgs& a, W& S, int tile, int col,
+                                           int lane) {
+  constexpr int SPAN = W::SPAN;
+  double2* grid = a.grid + (int64_t)col * a.K;
+  const int64_t base = (int64_t)tile * kTile - (M - 1);  // grid index of slot 0
+  __syncwarp();
+  for (int p = lane; p < SPAN; p += 32) {
+    const double2 t = S.acc[p];
+    const int64_t gi = base + p;
+    if (gi >= 0 && gi < a.K && (t.x != 0.0 || t.y != 0.0)) {
+      atomicAdd(&grid[gi].x, t.x);
+      atomicAdd(&grid[gi].y, t.y);
+    }
+    S.acc[p] = make_double2(0.0, 0.0);
+  }
+  __syncwarp();
 }
 
 template <int M, bool REAL>
-__global__ void __launch_bounds__(kSpreadThreads, 2) k_spread(SpreadArgs a, WinCoef C) {
-  constexpr int SPAN = kTile + 2 * M - 1;
-  extern __shared__ double2 acc[];
+__global__ void __launch_bounds__(kSpreadWarps * 32, 2) k_spread(SpreadArgs a, WinCoef C) {
+  using W = WarpSmem<M, REAL>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int nwarp = blockDim.x >> 5;
+  W& S = reinterpret_cast<W*>(smem_raw)[warp];
   const int col = blockIdx.y;
-  double2* my = acc + warp * SPAN;
-#if SFB_SPREAD_WARP_FLUSH
-  // warps are independent: each zeroes and flushes its own accumulator, so a
-  // warp that runs out of blocks never waits for the slowest one of the CTA
-  for (int i = lane; i < SPAN; i += 32) my[i] = make_double2(0.0, 0.0);
-  __syncwarp();
-#else
-  for (int i = threadIdx.x; i < SPAN * nwarp; i += blockDim.x) acc[i] = make_double2(0.0, 0.0);
-  __syncthreads();
-#endif
-  const int4 u = a.units[blockIdx.x];
-  const int stride = nwarp * 32;
-  int cb = u.y + warp * 32;
-  ChunkLoad nxt = load_chunk(a, cb + lane, cb + lane < u.z);
-  for (; cb < u.z; cb += stride) {
-    const ChunkLoad cur = nxt;
-    const bool valid = cb + lane < u.z;
-    const int cnt = cur.info & 255;
-    const int lcell = cur.info >> 8;
-    // the random f gather of this block (all four issued back to back) ...
-    double2 fv[kChunk];
-    const int src[kChunk] = {cur.perm.x, cur.perm.y, cur.perm.z, cur.perm.w};
-#pragma unroll
-    for (int s = 0; s < kChunk; ++s) {
-      fv[s] = make_double2(0.0, 0.0);
-      if (s < cnt) {
-        if (REAL) {
-          fv[s].x = __ldg(static_cast<const double*>(a.f) + src[s]);
-        } else {
-          fv[s] = __ldg(static_cast<const double2*>(a.f) + (int64_t)src[s] * a.batch + col);
-        }
-      }
+  // contiguous, cost-balanced block range of this warp (plan time)
+  const int64_t gw = (int64_t)blockIdx.x * kSpreadWarps + warp;
+  const int64_t b0 = a.wstart[gw], b1 = a.wstart[gw + 1];
+  if (b0 >= b1) return;
+  for (int p = lane; p < W::SPAN; p += 32) S.acc[p] = make_double2(0.0, 0.0);
+
+  // prologue: descriptors of blocks b0, b0+1; f of block b0
+  issue_desc<REAL>(a, S, b0, b1, 0, lane);
+  issue_desc<REAL>(a, S, b0 + 1, b1, 1, lane);
+  cp_async_wait<1>();
+  issue_f<REAL>(a, S, true, 0, 0, col, lane);
+  int tile = -1;
+  int next_tile = __ldg(a.blk_tile + b0);
+  for (int64_t b = b0; b < b1; ++b) {
+    const int i = (int)(b - b0);
+    const int sd = i % kDescStages, sf = i & 1;
+    issue_desc<REAL>(a, S, b + 2, b1, (i + 2) % kDescStages, lane);
+    cp_async_wait<2>();  // descriptors of b+1 have landed
+    issue_f<REAL>(a, S, b + 1 < b1, (i + 1) % kDescStages, (i + 1) & 1, col, lane);
+    const int btile = next_tile;
+    if (b + 1 < b1) next_tile = __ldg(a.blk_tile + b + 1);
+    if (btile != tile) {
+      if (tile >= 0) flush_tile<M>(a, S, tile, col, lane);
+      tile = btile;
     }
-    // ... and the next block's descriptors, in flight during this block's math
-    nxt = load_chunk(a, cb + stride + lane, cb + stride + lane < u.z);
-    const double pos[kChunk] = {cur.p01.x, cur.p01.y, cur.p23.x, cur.p23.y};
+    cp_async_wait<2>();  // f of b has landed
+    const int info = S.info[sd][lane];
+    const int cnt = info & 255;
+    const int lcell = info >> 8;
+    const double2 p01 = S.pos[sd][0][lane], p23 = S.pos[sd][1][lane];
     double2 r[2 * M];
 #pragma unroll
-    for (int i = 0; i < 2 * M; ++i) r[i] = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int s = 0; s < kChunk; s += 2) {
-      // a padding slot has f = 0 and a harmless position, so pairs may run
-      // with a dead second node; skip only fully empty pairs
-      if (s < cnt)
-        window_accumulate2<M, REAL>(C, pos[s] - floor(pos[s]), fv[s], pos[s + 1] - floor(pos[s + 1]),
-                                    fv[s + 1], r);
+    for (int k = 0; k < 2 * M; ++k) r[k] = make_double2(0.0, 0.0);
+    if (cnt > 0) {
+      if (REAL) {
+        const double* fs = reinterpret_cast<const double*>(&S.f[sf][0][0]);
+        window_accumulate2<M, true>(C, p01.x - floor(p01.x), make_double2(fs[lane], 0.0),
+                                    p01.y - floor(p01.y), make_double2(fs[32 + lane], 0.0), r);
+        if (cnt > 2)
+          window_accumulate2<M, true>(C, p23.x - floor(p23.x), make_double2(fs[64 + lane], 0.0),
+                                      p23.y - floor(p23.y), make_double2(fs[96 + lane], 0.0), r);
+      } else {
+        const double2* fs = reinterpret_cast<const double2*>(&S.f[sf][0][0]);
+        // a padding slot has f = 0 (zero-filled) and a harmless position, so
+        // pairs may run with a dead second node
+        window_accumulate2<M, false>(C, p01.x - floor(p01.x), fs[lane], p01.y - floor(p01.y),
+                                     fs[32 + lane], r);
+        if (cnt > 2)
+          window_accumulate2<M, false>(C, p23.x - floor(p23.x), fs[64 + lane],
+                                       p23.y - floor(p23.y), fs[96 + lane], r);
+      }
     }
-    // add into the warp-private tile accumulator; equal cells in one warp
-    // would race, so leaders of each cell group go first, round by round
-    unsigned pending = __ballot_sync(0xffffffffu, valid && cnt > 0);
+    // add into the warp-private tile accumulator.  A block whose 32 chunks
+    // all share one cell (the densest cells of clustered inputs: thousands of
+    // sources in one cell) is summed across lanes first (butterfly) and added
+    // once; otherwise equal cells in one block would race, so leaders of each
+    // cell group go first, round by round (rarely more than one round)
+    int same = 0;
+    __match_all_sync(0xffffffffu, cnt > 0 ? lcell : -1 - lane, &same);
+    if (same) {
+#pragma unroll
+      for (int k = 0; k < 2 * M; ++k) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          r[k].x += __shfl_xor_sync(0xffffffffu, r[k].x, o);
+          r[k].y += __shfl_xor_sync(0xffffffffu, r[k].y, o);
+        }
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 2 * M; ++k) {
+          double2 t = S.acc[lcell + k];
+          t.x += r[k].x;
+          t.y += r[k].y;
+          S.acc[lcell + k] = t;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    unsigned pending = __ballot_sync(0xffffffffu, cnt > 0);
     while (pending) {
       const bool mine = (pending >> lane) & 1u;
       const unsigned peers = __match_any_sync(0xffffffffu, mine ? lcell : (0x40000000 | lane));
       const bool leader = mine && ((__ffs(peers) - 1) == lane);
 #pragma unroll
-      for (int i = 0; i < 2 * M; ++i) {
+      for (int k = 0; k < 2 * M; ++k) {
         if (leader) {
-          double2 t = my[lcell + i];
-          t.x += r[i].x;
-          t.y += r[i].y;
-          my[lcell + i] = t;
+          double2 t = S.acc[lcell + k];
+          t.x += r[k].x;
+          t.y += r[k].y;
+          S.acc[lcell + k] = t;
         }
         __syncwarp();
       }
       pending &= ~__ballot_sync(0xffffffffu, leader);
     }
   }
-  // flush: grid index of accumulator slot p is tile*kTile - (M-1) + p
-  double2* grid = a.grid + (int64_t)col * a.K;
-  const int64_t base = (int64_t)u.x * kTile - (M - 1);
-#if SFB_SPREAD_WARP_FLUSH
-  __syncwarp();
-  for (int p = lane; p < SPAN; p += 32) {
-    const double2 t = my[p];
-    const int64_t gi = base + p;
-    if (gi >= 0 && gi < a.K && (t.x != 0.0 || t.y != 0.0)) {
-      atomicAdd(&grid[gi].x, t.x);
-      atomicAdd(&grid[gi].y, t.y);
-    }
-  }
-  return;
-#endif
-  __syncthreads();
-  for (int p = threadIdx.x; p < SPAN; p += blockDim.x) {
-    double2 s = make_double2(0.0, 0.0);
-    for (int w = 0; w < nwarp; ++w) {
-      const double2 t = acc[w * SPAN + p];
-      s.x += t.x;
-      s.y += t.y;
-    }
-    const int64_t gi = base + p;
-    if (gi >= 0 && gi < a.K && (s.x != 0.0 || s.y != 0.0)) {
-      atomicAdd(&grid[gi].x, s.x);
-      atomicAdd(&grid[gi].y, s.y);
-    }
-  }
+  cp_async_wait<0>();
+  flush_tile<M>(a, S, tile, col, lane);
 }
 
 template <int M, bool REAL>
 static void launch_spread_m(const NnfftPlanImpl& p, const void* f, double2* grid, int batch,
                             cudaStream_t s) {
-  const size_t smem = sizeof(double2) * (kTile + 2 * M - 1) * (kSpreadThreads / 32);
-  SpreadArgs a{p.sp.pos.p, p.sp.perm.p, p.sp.info.p, p.sp.units.p, f, grid, p.g.K, batch};
-  if (p.sp.n_units == 0) return;
-  k_spread<M, REAL><<<dim3((unsigned)p.sp.n_units, batch), kSpreadThreads, smem, s>>>(a, p.c1);
+  if (p.sp.n_blocks == 0) return;
+  const size_t smem = sizeof(WarpSmem<M, REAL>) * kSpreadWarps;
+  static std::atomic<unsigned long long> attr_set{0};  // per template instance, per device
+  const unsigned long long bit = 1ull << (p.device & 63);
+  if (!(attr_set.load() & bit)) {
+    SF_CUDA(cudaFuncSetAttribute(k_spread<M, REAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr_set.fetch_or(bit);
+  }
+  SpreadArgs a{p.sp.pos.p, p.sp.perm.p, p.sp.info.p, p.sp.blk_tile.p, p.sp.wstart.p, f, grid,
+               p.g.K, p.sp.n_blocks, batch};
+  // persistent: n_ctas = min(2 per SM, blocks / 32) CTAs, warp ranges from the plan
+  k_spread<M, REAL><<<dim3((unsigned)p.sp.n_ctas, batch), kSpreadWarps * 32, smem, s>>>(a, p.c1);
   SF_LAUNCH_CHECK();
 }
 
