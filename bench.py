@@ -473,6 +473,26 @@ def run_b200(args, cfg):
         pcie_ms = ev0.elapsed_time(ev1) / 5
         del d_in
 
+    # the spread's memory floor: its f reads are a random 16-byte gather over
+    # all of f (sources are cell-sorted, f is in caller order).  Time torch's
+    # own gather f[perm] of the same M1 complex128 values through a random
+    # permutation (random 16-byte reads plus a sequential write; no window
+    # math, no grid) -- what the spread's f traffic costs by itself
+    gather_floor_ms = None
+    if world == 1 and B == 1:
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(0)
+        rp = torch.randperm(d_f.shape[0], device=dev, generator=gen)
+        tmp = d_f[rp]
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(5):
+            tmp = d_f[rp]
+        ev1.record(stream)
+        ev1.synchronize()
+        gather_floor_ms = ev0.elapsed_time(ev1) / 5
+        del rp, tmp
+
     launches = L.sincfft_nnfft_launches_per_execute(ph, B) * args.steps
     fp64_peak, fp64_note = 148 * 64 * 2 * (clk.max_mhz or 1965) * 1e6 / 1e12, \
         "derived: 148 SMs x 64 DFMA/clk x 2 flops x max SM clock"
@@ -504,6 +524,8 @@ def run_b200(args, cfg):
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "alg_bytes_per_launch": alg[dom],
                          "launch_ms": t_dom * 1e3,
+                         "random_gather_floor_ms": gather_floor_ms
+                         if dom == "spread" else None,
                          "fp64": None if flops[dom] is None else {
                              "achieved_tflops": flops[dom] / t_dom / 1e12,
                              "peak_tflops": fp64_peak,
