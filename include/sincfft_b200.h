@@ -155,6 +155,24 @@ SINCFFT_API int sincfft_sinc_plan_geometry(sincfft_sinc_plan plan, sincfft_geome
 SINCFFT_API int sincfft_sinc_execute(sincfft_sinc_plan plan, const double *c, int32_t c_is_real,
                          double *out, int32_t ptr_kind, void *stream);
 
+/* --- exact quadratic-cost sums ---------------------
+ * The reference's oracles (pkg/src/sincfft/direct.py), fp64 on the GPU, with
+ * the phase carried in two doubles and compensated sums (at least as
+ * accurate as the reference's).  Inputs/outputs follow `ptr_kind`; the call
+ * synchronizes `stream` for host pointers.  Replace, in order:
+ *   nndft_direct          direct.py:28-64   out_j = sum_k f_k e^{-2 pi i N v_k x_j}
+ *   ndft_direct           direct.py:67-90   out_j = sum_{k in I_Nc} c_k e^{2 pi i k x_j}
+ *                                           (Nc even, k = -Nc/2 .. Nc/2-1)
+ *   sinc_transform_direct direct.py:93-112  out_j = sum_k c_k sinc(N pi (b_j - a_k)) */
+SINCFFT_API int sincfft_nndft_direct(const double *f, const double *v, int64_t M1, const double *x,
+                                     int64_t M2, int64_t N, double *out, int32_t ptr_kind,
+                                     int32_t device, void *stream);
+SINCFFT_API int sincfft_ndft_direct(const double *c, int64_t Nc, const double *x, int64_t M,
+                                    double *out, int32_t ptr_kind, int32_t device, void *stream);
+SINCFFT_API int sincfft_sinc_direct(const double *c, const double *a, int64_t L1, const double *b,
+                                    int64_t L2, int64_t N, double *out, int32_t ptr_kind,
+                                    int32_t device, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

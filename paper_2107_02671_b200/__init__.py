@@ -8,7 +8,8 @@ by hand-written sm_100a CUDA kernels behind the C ABI in
 fails loudly if it has not been built; there is no CPU fallback.
 """
 
-from . import bounds
+from . import bounds, direct
+from .direct import ndft_direct, nndft_direct, sinc_transform_direct
 from .errors import ParameterError, PositivityError
 from .fast_sinc import SincMode, SincPlan, fast_sinc_transform, sinc_plan
 from .nnfft import (NnfftGeometry, NnfftPlan, WindowSpec, nnfft_plan, nnfft_trafo,
@@ -23,5 +24,6 @@ __all__ = [
     "rescale_frequencies",
     "CcQuadrature", "cc_quadrature", "cc_weights_direct", "cc_weights_fast",
     "SincMode", "SincPlan", "sinc_plan", "fast_sinc_transform",
-    "bounds", "__version__",
+    "nndft_direct", "ndft_direct", "sinc_transform_direct",
+    "bounds", "direct", "__version__",
 ]

@@ -578,4 +578,81 @@ int sincfft_sinc_execute(sincfft_sinc_plan plan, const double* c, int32_t c_is_r
   });
 }
 
+// ---------------------------------------------------------------- direct sums
+namespace {
+struct OutBuf {  // device output, copied back to a host `out` at finish()
+  std::unique_ptr<sfb::Scratch> tmp;
+  void* user;
+  size_t bytes;
+  int32_t kind;
+  void* ptr;
+  OutBuf(void* u, size_t b, int32_t k, cudaStream_t s) : user(u), bytes(b), kind(k) {
+    if (kind == SINCFFT_PTR_DEVICE) {
+      ptr = user;
+    } else {
+      tmp.reset(new sfb::Scratch(bytes, s));
+      ptr = tmp->p;
+    }
+  }
+  void finish(cudaStream_t s) {
+    if (kind == SINCFFT_PTR_DEVICE) return;
+    if (bytes) SF_CUDA(cudaMemcpyAsync(user, ptr, bytes, cudaMemcpyDeviceToHost, s));
+    if (kind == SINCFFT_PTR_HOST) SF_CUDA(cudaStreamSynchronize(s));
+  }
+};
+}  // namespace
+
+int sincfft_nndft_direct(const double* f, const double* v, int64_t M1, const double* x,
+                         int64_t M2, int64_t N, double* out, int32_t ptr_kind, int32_t device,
+                         void* stream) {
+  return guarded([&] {
+    if (!f || !v || !x || !out) sfb::fail(1, "NULL argument");
+    if (M1 <= 0 || M2 <= 0) sfb::fail(1, "f and x must be nonempty 1-d arrays");
+    check_ptr_kind(ptr_kind);
+    set_device(device);
+    cudaStream_t s = as_stream(stream);
+    InBuf fb(f, sizeof(double2) * M1, ptr_kind, s), vb(v, sizeof(double) * M1, ptr_kind, s),
+        xb(x, sizeof(double) * M2, ptr_kind, s);
+    OutBuf ob(out, sizeof(double2) * M2, ptr_kind, s);
+    sfb::run_nndft_direct((const double2*)fb.ptr, (const double*)vb.ptr, M1,
+                          (const double*)xb.ptr, M2, (double)N, (double2*)ob.ptr, s);
+    ob.finish(s);
+  });
+}
+
+int sincfft_ndft_direct(const double* c, int64_t Nc, const double* x, int64_t M, double* out,
+                        int32_t ptr_kind, int32_t device, void* stream) {
+  return guarded([&] {
+    if (!c || !x || !out) sfb::fail(1, "NULL argument");
+    if (Nc <= 0 || M <= 0) sfb::fail(1, "c and x must be nonempty 1-d arrays");
+    if (Nc % 2) sfb::fail(1, "ndft_direct: len(c) must be even");
+    check_ptr_kind(ptr_kind);
+    set_device(device);
+    cudaStream_t s = as_stream(stream);
+    InBuf cb(c, sizeof(double2) * Nc, ptr_kind, s), xb(x, sizeof(double) * M, ptr_kind, s);
+    OutBuf ob(out, sizeof(double2) * M, ptr_kind, s);
+    sfb::run_ndft_direct((const double2*)cb.ptr, Nc, (const double*)xb.ptr, M, (double2*)ob.ptr,
+                         s);
+    ob.finish(s);
+  });
+}
+
+int sincfft_sinc_direct(const double* c, const double* a, int64_t L1, const double* b,
+                        int64_t L2, int64_t N, double* out, int32_t ptr_kind, int32_t device,
+                        void* stream) {
+  return guarded([&] {
+    if (!c || !a || !b || !out) sfb::fail(1, "NULL argument");
+    if (L1 <= 0 || L2 <= 0) sfb::fail(1, "c and b must be nonempty 1-d arrays");
+    check_ptr_kind(ptr_kind);
+    set_device(device);
+    cudaStream_t s = as_stream(stream);
+    InBuf cb(c, sizeof(double2) * L1, ptr_kind, s), ab(a, sizeof(double) * L1, ptr_kind, s),
+        bb(b, sizeof(double) * L2, ptr_kind, s);
+    OutBuf ob(out, sizeof(double2) * L2, ptr_kind, s);
+    sfb::run_sinc_direct((const double2*)cb.ptr, (const double*)ab.ptr, L1,
+                         (const double*)bb.ptr, L2, (double)N, (double2*)ob.ptr, s);
+    ob.finish(s);
+  });
+}
+
 }  // extern "C"

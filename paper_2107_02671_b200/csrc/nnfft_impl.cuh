@@ -157,6 +157,13 @@ void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batc
 // whole transform with device pointers (scratch allocated stream-ordered)
 void run_execute(const NnfftPlanImpl& p, const double2* f, double2* out, int batch,
                  cudaStream_t stream);
+// ----- direct.cu: exact O(M1 M2) sums (reference direct.py), device pointers
+void run_nndft_direct(const double2* f, const double* v, int64_t M1, const double* x,
+                      int64_t M2, double N, double2* out, cudaStream_t stream);
+void run_ndft_direct(const double2* c, int64_t Nc, const double* x, int64_t M, double2* out,
+                     cudaStream_t stream);
+void run_sinc_direct(const double2* c, const double* a, int64_t L1, const double* b, int64_t L2,
+                     double N, double2* out, cudaStream_t stream);
 // ----- batched.cu: batch >= kBatchedMin columns, columns across lanes
 // ev (optional): 4 events recorded around spread | transpose+FFT+transpose | gather
 void run_execute_batched(const NnfftPlanImpl& p, const double2* f, double2* out, int batch,

@@ -37,7 +37,12 @@ for k in names:
     rows = list(csv.reader(io.StringIO(src)))
     hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
     hh = rows[hdr_i]
-    data = [r for r in rows[hdr_i + 1:] if len(r) == len(hh)]
+    data = []
+    for r in rows[hdr_i + 1:]:
+        if r and r[0] == "Address":  # next kernel instance of the same name
+            break
+        if len(r) == len(hh):
+            data.append(r)
     ix = {c: i for i, c in enumerate(hh)}
     S = lambda c: sum(float(r[ix[c]] or 0) for r in data)
     tot = S("Warp Stall Sampling (All Samples)") or 1
