@@ -200,5 +200,77 @@ def main():
     save("sinc_cases.npz", **sc)
 
 
+def main_nfft():
+    """Classical NFFT (nfft.py) and the equispaced fast-sinc routes
+    (fast_sinc.py:200-248): SURVEY.md 8f row f1."""
+    nf = {}
+    k = 0
+    # (N, M, sigma, m, seed): reference-test shapes (tests/test_nfft.py),
+    # sigma 5/4 and 3/2, nodes at +-1/2 and on grid points, larger sizes
+    for (N, M, sigma, m, seed) in [(64, 129, 2.0, 2, 102), (64, 129, 2.0, 4, 104),
+                                   (64, 129, 2.0, 6, 106), (12, 29, 2.0, 6, 17),
+                                   (32, 47, 2.0, 4, 0), (16, 3, 2.0, 4, 1), (128, 200, 1.5, 5, 3),
+                                   (160, 333, 1.25, 3, 4), (4096, 16385, 2.0, 8, 9),
+                                   (1024, 5000, 2.0, 10, 10)]:
+        rng = np.random.default_rng(seed)
+        x = rng.uniform(-0.5, 0.5, M)
+        if M == 3:
+            x = np.array([0.0, 0.24, -0.5])
+        if M == 333:
+            x[:4] = [-0.5, 0.5, 0.0, 1.0 / (sigma * N)]
+        c = rng.uniform(-1, 1, N) + 1j * rng.uniform(-1, 1, N)
+        y = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+        plan = sincfft.nfft_plan(N, x, sigma=sigma, m=m)
+        nf[f"c{k}_N"] = N
+        nf[f"c{k}_sigma"] = sigma
+        nf[f"c{k}_m"] = m
+        nf[f"c{k}_x"] = x
+        nf[f"c{k}_c"] = c
+        nf[f"c{k}_y"] = y
+        nf[f"c{k}_trafo"] = sincfft.nfft_trafo(plan, c)
+        nf[f"c{k}_adjoint"] = sincfft.nfft_adjoint(plan, y)
+        nf[f"c{k}_hat"] = plan.hat
+        if M * 2 * m <= 4096:
+            nf[f"c{k}_spread_idx"] = plan.spread_idx.astype(np.int32)
+            nf[f"c{k}_spread_val"] = plan.spread_val
+        k += 1
+    nf["ncases"] = k
+    save("nfft_cases.npz", **nf)
+
+    # --- fast sinc: all four layouts on grid node sets
+    sm = {}
+    k = 0
+    # (N, L1, L2, m, seed, a on grid, b on grid, forced modes)
+    for (N, L1, L2, m, seed, agrid, bgrid, modes) in [
+            (32, 24, 32, 6, 21, True, True, None), (48, 16, 40, 6, 22, True, False, None),
+            (64, 50, 64, 8, 23, False, True, None), (256, 512, 256, 8, 24, True, True, None),
+            (40, 40, 30, 6, 25, False, False, None),
+            (64, 64, 64, 8, 26, True, True,
+             ("general", "equispaced-sources", "equispaced-targets", "equispaced-both"))]:
+        rng = np.random.default_rng(seed)
+        a = (np.arange(L1) - L1 // 2) / L1 if agrid else rng.uniform(-0.5, 0.5, L1)
+        b = (np.arange(L2) - L2 // 2) / L2 if bgrid else rng.uniform(-0.5, 0.5, L2)
+        c = rng.standard_normal(L1) + (1j * rng.standard_normal(L1) if seed % 2 else 0.0)
+        for mode in (modes or (None,)):
+            plan = sincfft.sinc_plan(N, a, b, m1=m, m2=m, mode=mode)
+            sm[f"s{k}_N"] = N
+            sm[f"s{k}_m"] = m
+            sm[f"s{k}_a"] = a
+            sm[f"s{k}_b"] = b
+            sm[f"s{k}_c"] = c
+            sm[f"s{k}_mode"] = plan.mode.value
+            sm[f"s{k}_forced"] = mode or ""
+            sm[f"s{k}_out"] = sincfft.fast_sinc_transform(plan, c)
+            sm[f"s{k}_direct"] = sincfft.sinc_transform_direct(c, a, b, N)
+            sm[f"s{k}_bound_full"] = plan.error_bound()["full"]
+            k += 1
+    sm["ncases"] = k
+    save("sinc_modes.npz", **sm)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["nfft"]:
+        main_nfft()
+    else:
+        main()
+        main_nfft()

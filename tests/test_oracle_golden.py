@@ -95,3 +95,34 @@ def test_sinc_cases(golden):
     assert np.array_equal(z, g["cc16384_z"])
     assert np.max(np.abs(w - g["cc16384_w"])) <= 1e-16
     assert np.max(np.abs(O.cc_quadrature(6)[1] - g["cc_w6"])) <= 1e-16
+
+
+def test_nfft_cases(golden):
+    """Classical NFFT restatement (ref:nfft.py) against the reference's own
+    trafo / adjoint outputs, plan tables and hat values."""
+    g = golden("nfft_cases.npz")
+    for k in range(int(g["ncases"])):
+        c = lambda key: g[f"c{k}_{key}"]  # noqa: E731
+        t = O.nfft_plan(int(c("N")), c("x"), float(c("sigma")), int(c("m")))
+        assert np.array_equal(t.hat, c("hat")), k
+        if f"c{k}_spread_idx" in g.files:
+            assert np.array_equal(t.spread_idx, c("spread_idx")), k
+            assert np.array_equal(t.spread_val, c("spread_val")), k
+        assert rel(O.nfft_trafo(t, c("c")), c("trafo"), c("c")) <= 1e-15, k
+        assert rel(O.nfft_adjoint(t, c("y")), c("adjoint"), c("y")) <= 1e-15, k
+
+
+def test_sinc_modes(golden):
+    """All four fast-sinc layouts (ref:fast_sinc.py:171-248)."""
+    g = golden("sinc_modes.npz")
+    for k in range(int(g["ncases"])):
+        s = lambda key: g[f"s{k}_{key}"]  # noqa: E731
+        N = int(s("N"))
+        assert O.sinc_mode(N, s("a"), s("b")) == str(s("mode")) or str(s("forced")), k
+        st = O.sinc_plan(N, s("a"), s("b"), m1=int(s("m")), m2=int(s("m")),
+                         mode=str(s("forced")) or None)
+        assert st.mode == str(s("mode")), k
+        out = O.sinc_transform(st, s("c"))
+        assert rel(out, s("out"), s("c")) <= 1e-15, k
+        err = np.max(np.abs(out - s("direct"))) / np.sum(np.abs(s("c")))
+        assert err <= float(s("bound_full")), k
