@@ -131,6 +131,17 @@ Geometry make_geometry(int64_t N, int64_t M1, int64_t M2, double sigma1, double 
                        int m2);
 // v, x are device pointers (original order, unclipped) on `stream`.
 void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cudaStream_t stream);
+// the two halves of build_plan, reused by the classical NFFT (nfft.cu)
+struct TargetScale {
+  bool hat1 = false;  // scale = 1/phi_hat_1(N x) (NNFFT) or 1 (NFFT)
+  double N = 0.0, beta1 = 0.0;
+  int m1 = 0;
+  int64_t N1 = 0;
+};
+void build_sources(NnfftPlanImpl& p, const double* v, int64_t M1, double N1, int64_t K,
+                   cudaStream_t stream);
+void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, int64_t N2,
+                   int m2, const TargetScale& ts, cudaStream_t stream);
 // multiply the gather scale by per-target weights (device, original order)
 void fuse_target_weights(NnfftPlanImpl& p, const double* w_dev, cudaStream_t stream);
 

@@ -252,12 +252,16 @@ __global__ void k_tgt_keys(const double* x, int64_t n, double ratio, double N2d,
 
 // sorted target positions and 1/phi_hat_1(N x) (nnfft.py:175, 243)
 __global__ void k_tgt_tables(const double* x, const int* perm, int64_t n, double ratio, double N2d,
-                             double Nd, double beta1, int m1, int64_t N1, double* pos,
-                             double* scale, unsigned long long* min_hat_bits) {
+                             int with_hat, double Nd, double beta1, int m1, int64_t N1,
+                             double* pos, double* scale, unsigned long long* min_hat_bits) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
   const double xv = x[perm[j]];
   pos[j] = N2d * (xv * ratio);
+  if (!with_hat) {
+    scale[j] = 1.0;
+    return;
+  }
   const double hat = phi_hat_sinh(beta1, m1, N1, Nd * xv);
   scale[j] = 1.0 / hat;
   if (!(hat > 0.0)) atomicAdd(min_hat_bits, 1ull);
@@ -382,50 +386,16 @@ int64_t exclusive_scan(const int* in, int* off, int64_t n, cudaStream_t s) {
 
 }  // namespace
 
-void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cudaStream_t s) {
-  const Geometry& g = p.g;
-  // --- domain checks and clipping (nnfft.py:162-170)
-  const double vlim = 0.5 / g.a;
-  const double vmax = device_absmax(v_dev, g.M1, s);
-  if (!(vmax <= vlim + 1e-12)) {
-    char buf[256];
-    snprintf(buf, sizeof(buf),
-             "nnfft_plan: frequencies exceed 1/(2a) = %.6g; apply rescale_frequencies to map "
-             "[-1/2, 1/2] data into the band",
-             vlim);
-    fail(1, buf);
-  }
-  const double xmax = device_absmax(x_dev, g.M2, s);
-  if (!(xmax <= 0.5 + 1e-12)) fail(1, "nnfft_plan: spatial nodes must lie in [-1/2, 1/2]");
-  p.v_clip.alloc(g.M1);
-  p.x_clip.alloc(g.M2);
-  k_clip<<<blocks(g.M1), 256, 0, s>>>(v_dev, p.v_clip.p, g.M1, vlim);
-  k_clip<<<blocks(g.M2), 256, 0, s>>>(x_dev, p.x_clip.p, g.M2, 0.5);
-  SF_LAUNCH_CHECK();
-
-  // --- window polynomials (window.cu); sigma of window 2 is N2/K (nnfft.py:173)
-  p.c1 = fit_window(g.m1, g.beta1);
-  p.c2 = fit_window(g.m2, g.beta2);
-
-  // --- phi_hat_2 at l - K/2 (nnfft.py:180-183)
-  p.hat2.alloc(g.K);
-  {
-    Scratch bad(sizeof(unsigned long long), s);
-    SF_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
-    k_hat2<<<blocks(g.K), 256, 0, s>>>(p.hat2.p, g.K, g.beta2, g.m2, g.N2,
-                                       bad.as<unsigned long long>());
-    SF_LAUNCH_CHECK();
-    if (read1(bad.as<unsigned long long>(), s))
-      fail(2, "nnfft_plan: phi_hat_2 must be strictly positive on the coarse grid");
-  }
-
-  // --- sources: sort by cell, chunk, tile into work units
-  {
-    const int64_t M1 = g.M1, K = g.K;
+// Spread structure (SpreadPlan) for M1 sources at positions N1 * v (v clipped,
+// device, original order) on a K-point grid, cell floor(N1 v) + K/2:
+// cell-sorted sources cut into chunks, blocks and cost-balanced warp ranges
+// (spread.cu), plus the cell-sorted copies the batched path reads.
+void build_sources(NnfftPlanImpl& p, const double* v, int64_t M1, double N1, int64_t K,
+                   cudaStream_t s) {
     Scratch kin(sizeof(unsigned) * M1, s), kout(sizeof(unsigned) * M1, s);
     Scratch iin(sizeof(int) * M1, s);
     p.sp.perm.alloc(M1);
-    k_src_keys<<<blocks(M1), 256, 0, s>>>(p.v_clip.p, M1, (double)g.N1, K / 2, kin.as<unsigned>(),
+    k_src_keys<<<blocks(M1), 256, 0, s>>>(v, M1, N1, K / 2, kin.as<unsigned>(),
                                           iin.as<int>());
     SF_LAUNCH_CHECK();
     size_t tb = 0;
@@ -438,7 +408,7 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
                                               iin.as<int>(), p.sp.perm.p, (int)M1, 0, bits, s));
     }
     p.sp.pos.alloc(M1);
-    k_take_scaled<<<blocks(M1), 256, 0, s>>>(p.v_clip.p, p.sp.perm.p, M1, (double)g.N1,
+    k_take_scaled<<<blocks(M1), 256, 0, s>>>(v, p.sp.perm.p, M1, N1,
                                              p.sp.pos.p);
     SF_LAUNCH_CHECK();
     Scratch cstart(sizeof(int) * (K + 1), s), nch(sizeof(int) * K, s),
@@ -533,19 +503,21 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
     p.sp.pos = std::move(spos);
     p.sp.perm = std::move(sperm);
     p.sp.chunks.release();
-  }
+}
 
-  // --- targets: sort by (original-index slice, fine-grid cell), 1/phi_hat_1,
-  //     and the output window [s_lo, s_hi] the gather reads
-  {
-    const int64_t M2 = g.M2;
-    const double ratio = (double)g.N / (double)g.N1;  // x/sigma1 (nnfft.py:200)
+// Gather structure (GatherPlan) for M2 targets at positions N2 * xs,
+// xs = ratio * x (x clipped, device, original order): targets sorted by
+// (original-index slice, cell), the per-target scale (1/phi_hat_1(N x) for
+// the NNFFT, 1 for the NFFT), the per-CTA h spans and the output window
+// [s_lo, s_lo + Kout) the gather reads (Kout <= N2; wider windows wrap).
+void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, int64_t N2,
+                   int m2, const TargetScale& ts, cudaStream_t s) {
     Scratch kin(sizeof(unsigned long long) * M2, s), kout(sizeof(unsigned long long) * M2, s);
     Scratch iin(sizeof(int) * M2, s);
     p.gp.perm.alloc(M2);
-    const int cbits = key_bits((uint64_t)(2 * g.N2 + 2));
+    const int cbits = key_bits((uint64_t)(2 * N2 + 2));
     const int64_t slice = gather_slice();
-    k_tgt_keys<<<blocks(M2), 256, 0, s>>>(p.x_clip.p, M2, ratio, (double)g.N2, g.N2, cbits, slice,
+    k_tgt_keys<<<blocks(M2), 256, 0, s>>>(x, M2, ratio, (double)N2, N2, cbits, slice,
                                           kin.as<unsigned long long>(), iin.as<int>());
     SF_LAUNCH_CHECK();
     size_t tb = 0;
@@ -563,23 +535,73 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
     p.gp.scale.alloc(M2);
     Scratch bad(sizeof(unsigned long long), s);
     SF_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
-    k_tgt_tables<<<blocks(M2), 256, 0, s>>>(p.x_clip.p, p.gp.perm.p, M2, ratio, (double)g.N2,
-                                            (double)g.N, g.beta1, g.m1, g.N1, p.gp.pos.p,
+    k_tgt_tables<<<blocks(M2), 256, 0, s>>>(x, p.gp.perm.p, M2, ratio, (double)N2, ts.hat1 ? 1 : 0,
+                                            ts.N, ts.beta1, ts.m1, ts.N1, p.gp.pos.p,
                                             p.gp.scale.p, bad.as<unsigned long long>());
     SF_LAUNCH_CHECK();
     if (read1(bad.as<unsigned long long>(), s))
       fail(2, "nnfft_plan: phi_hat_1(N x_j) must be strictly positive at every node");
     double plo, phi;
     device_minmax(p.gp.pos.p, M2, s, &plo, &phi);
-    const int64_t s_lo = (int64_t)std::floor(plo) + 1 - g.m2;
-    const int64_t s_hi = (int64_t)std::floor(phi) + g.m2;
+    const int64_t s_lo = (int64_t)std::floor(plo) + 1 - m2;
+    const int64_t s_hi = (int64_t)std::floor(phi) + m2;
     p.fft.s_lo = s_lo;
-    p.fft.Kout = std::min<int64_t>(s_hi - s_lo + 1, g.N2);
+    p.fft.Kout = std::min<int64_t>(s_hi - s_lo + 1, N2);
     const int64_t nblk = ceil_div(M2, kGatherThreads);
     p.gp.span.alloc(nblk);
-    k_gather_spans<<<blocks(nblk), 256, 0, s>>>(p.gp.pos.p, M2, nblk, g.m2, s_lo, p.gp.span.p);
+    k_gather_spans<<<blocks(nblk), 256, 0, s>>>(p.gp.pos.p, M2, nblk, m2, s_lo, p.gp.span.p);
     SF_LAUNCH_CHECK();
+}
+
+void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cudaStream_t s) {
+  const Geometry& g = p.g;
+  // --- domain checks and clipping (nnfft.py:162-170)
+  const double vlim = 0.5 / g.a;
+  const double vmax = device_absmax(v_dev, g.M1, s);
+  if (!(vmax <= vlim + 1e-12)) {
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "nnfft_plan: frequencies exceed 1/(2a) = %.6g; apply rescale_frequencies to map "
+             "[-1/2, 1/2] data into the band",
+             vlim);
+    fail(1, buf);
   }
+  const double xmax = device_absmax(x_dev, g.M2, s);
+  if (!(xmax <= 0.5 + 1e-12)) fail(1, "nnfft_plan: spatial nodes must lie in [-1/2, 1/2]");
+  p.v_clip.alloc(g.M1);
+  p.x_clip.alloc(g.M2);
+  k_clip<<<blocks(g.M1), 256, 0, s>>>(v_dev, p.v_clip.p, g.M1, vlim);
+  k_clip<<<blocks(g.M2), 256, 0, s>>>(x_dev, p.x_clip.p, g.M2, 0.5);
+  SF_LAUNCH_CHECK();
+
+  // --- window polynomials (window.cu); sigma of window 2 is N2/K (nnfft.py:173)
+  p.c1 = fit_window(g.m1, g.beta1);
+  p.c2 = fit_window(g.m2, g.beta2);
+
+  // --- phi_hat_2 at l - K/2 (nnfft.py:180-183)
+  p.hat2.alloc(g.K);
+  {
+    Scratch bad(sizeof(unsigned long long), s);
+    SF_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
+    k_hat2<<<blocks(g.K), 256, 0, s>>>(p.hat2.p, g.K, g.beta2, g.m2, g.N2,
+                                       bad.as<unsigned long long>());
+    SF_LAUNCH_CHECK();
+    if (read1(bad.as<unsigned long long>(), s))
+      fail(2, "nnfft_plan: phi_hat_2 must be strictly positive on the coarse grid");
+  }
+
+  // --- sources: sort by cell, chunk, tile into blocks
+  build_sources(p, p.v_clip.p, g.M1, (double)g.N1, g.K, s);
+
+  // --- targets: sort by (original-index slice, fine-grid cell), 1/phi_hat_1,
+  //     and the output window [s_lo, s_hi] the gather reads
+  TargetScale ts;
+  ts.hat1 = true;
+  ts.N = (double)g.N;
+  ts.beta1 = g.beta1;
+  ts.m1 = g.m1;
+  ts.N1 = g.N1;
+  build_targets(p, p.x_clip.p, g.M2, (double)g.N / (double)g.N1, g.N2, g.m2, ts, s);
 
   build_fft(p, s);
   SF_CUDA(cudaStreamSynchronize(s));
