@@ -58,6 +58,13 @@ extern "C" {
 
 typedef struct sincfft_nnfft_plan_s *sincfft_nnfft_plan;
 typedef struct sincfft_sinc_plan_s *sincfft_sinc_plan;
+typedef struct sincfft_nfft_plan_s *sincfft_nfft_plan;
+
+/* fast sinc layouts (sincfft.fast_sinc.SincMode, fast_sinc.py:32-38) */
+#define SINCFFT_SINC_GENERAL 0
+#define SINCFFT_SINC_EQUISPACED_SOURCES 1
+#define SINCFFT_SINC_EQUISPACED_TARGETS 2
+#define SINCFFT_SINC_EQUISPACED_BOTH 3
 
 /* Geometry of a plan (ref: NnfftGeometry, pkg/src/sincfft/nnfft.py:30-89). */
 typedef struct {
@@ -129,18 +136,21 @@ SINCFFT_API int sincfft_nnfft_export_tables(sincfft_nnfft_plan plan, int64_t *sp
                                 int64_t *gather_idx, double *gather_val, double *hat1,
                                 double *hat2);
 
-/* --- fast sinc transform (Algorithm 6.3, GENERAL mode) ------------------
- * Replaces sincfft.fast_sinc.sinc_plan (fast_sinc.py:123-223) for the
- * GENERAL layout.  The caller supplies the Clenshaw-Curtis points z[n+1]
- * and weights w[n+1] (host plan-time data, sinc_approx.py:97-106) and the
- * rescaled bandwidth n_star (fast_sinc.py:97-107); the two inner NNFFT plans
- * are (n_star, a*N/n_star, z/2) and (n_star, -(N/n_star) z/2, b)
- * (fast_sinc.py:205-220). */
+/* --- fast sinc transform (Algorithm 6.3, all four layouts) ---------------
+ * Replaces sincfft.fast_sinc.sinc_plan (fast_sinc.py:123-223).  The caller
+ * supplies the Clenshaw-Curtis points z[n+1] and weights w[n+1] (host
+ * plan-time data, sinc_approx.py:97-106), the rescaled bandwidth n_star
+ * (fast_sinc.py:97-107) and the layout `mode` (SINCFFT_SINC_*, detected or
+ * forced by the caller exactly as fast_sinc.py:171-192).  Stage 1 is the
+ * NNFFT (n_star, a*N/n_star, z/2) (fast_sinc.py:205-209) or, for equispaced
+ * sources, the NFFT trafo (L1, wrap(-(N/(2 L1)) z)) (:200-203); stage 3 is
+ * the NNFFT (n_star, -(N/n_star) z/2, b) (:216-220) or, for equispaced
+ * targets (L2 = N), the NFFT adjoint (N, -z/2) (:211-214). */
 SINCFFT_API int sincfft_sinc_plan_create(sincfft_sinc_plan *plan, int64_t N, int64_t n_star, int64_t L1,
                              int64_t L2, int64_t n, const double *z, const double *w,
                              const double *a, const double *b, double sigma1, double sigma2,
-                             int32_t m1, int32_t m2, int32_t ptr_kind, int32_t device,
-                             void *stream);
+                             int32_t m1, int32_t m2, int32_t mode, int32_t ptr_kind,
+                             int32_t device, void *stream);
 
 SINCFFT_API int sincfft_sinc_plan_destroy(sincfft_sinc_plan plan);
 
@@ -154,6 +164,26 @@ SINCFFT_API int sincfft_sinc_plan_geometry(sincfft_sinc_plan plan, sincfft_geome
  * the reference promotes real input to complex128); out: L2 complex. */
 SINCFFT_API int sincfft_sinc_execute(sincfft_sinc_plan plan, const double *c, int32_t c_is_real,
                          double *out, int32_t ptr_kind, void *stream);
+
+/* --- classical NFFT ---------------------------------
+ * Replaces sincfft.nfft (nfft.py:53-123), sinh window: nfft_plan(N, x,
+ * sigma, m) -> sincfft_nfft_plan_create (N even, sigma N an even integer,
+ * 2m <= sigma N / 2, |x| <= 1/2 + 1e-12, same messages and status classes);
+ * nfft_trafo: c[N] (I_N = -N/2 .. N/2-1) -> out[M]; nfft_adjoint: y[M] ->
+ * out[N].  export_tables fills the reference plan's spread_idx / spread_val
+ * ([M x 2m], host) and hat ([N], host); NULL skips a table. */
+SINCFFT_API int sincfft_nfft_plan_create(sincfft_nfft_plan *plan, int64_t N, int64_t M, double sigma,
+                                         int32_t m, const double *x, int32_t ptr_kind,
+                                         int32_t device, void *stream);
+SINCFFT_API int sincfft_nfft_plan_destroy(sincfft_nfft_plan plan);
+SINCFFT_API int sincfft_nfft_plan_geometry(sincfft_nfft_plan plan, int64_t *n_over,
+                                           sincfft_geometry *trafo, sincfft_geometry *adjoint);
+SINCFFT_API int sincfft_nfft_trafo(sincfft_nfft_plan plan, const double *c, double *out,
+                                   int32_t ptr_kind, void *stream);
+SINCFFT_API int sincfft_nfft_adjoint(sincfft_nfft_plan plan, const double *y, double *out,
+                                     int32_t ptr_kind, void *stream);
+SINCFFT_API int sincfft_nfft_export_tables(sincfft_nfft_plan plan, int64_t *spread_idx,
+                                           double *spread_val, double *hat);
 
 /* --- exact quadratic-cost sums ---------------------
  * The reference's oracles (pkg/src/sincfft/direct.py), fp64 on the GPU, with

@@ -10,6 +10,7 @@ fails loudly if it has not been built; there is no CPU fallback.
 
 from . import bounds, direct
 from .direct import ndft_direct, nndft_direct, sinc_transform_direct
+from .nfft import NfftPlan, nfft_adjoint, nfft_plan, nfft_trafo
 from .errors import ParameterError, PositivityError
 from .fast_sinc import SincMode, SincPlan, fast_sinc_transform, sinc_plan
 from .nnfft import (NnfftGeometry, NnfftPlan, WindowSpec, nnfft_plan, nnfft_trafo,
@@ -24,6 +25,7 @@ __all__ = [
     "rescale_frequencies",
     "CcQuadrature", "cc_quadrature", "cc_weights_direct", "cc_weights_fast",
     "SincMode", "SincPlan", "sinc_plan", "fast_sinc_transform",
+    "NfftPlan", "nfft_plan", "nfft_trafo", "nfft_adjoint",
     "nndft_direct", "ndft_direct", "sinc_transform_direct",
     "bounds", "direct", "__version__",
 ]

@@ -13,7 +13,7 @@
 #include <string>
 
 #include "../../include/sincfft_b200.h"
-#include "nnfft_impl.cuh"
+#include "nfft_impl.cuh"
 
 // Small transforms are launch-bound (configs 1-2: microseconds of GPU work
 // behind ~10 runtime calls), so device-pointer executes of small plans are
@@ -39,9 +39,14 @@ struct sincfft_nnfft_plan_s {
 };
 
 struct sincfft_sinc_plan_s {
-  sfb::NnfftPlanImpl st1, st3;
+  sfb::NnfftPlanImpl st1, st3;                  // NNFFT stages (non-grid node sets)
+  std::unique_ptr<sfb::NfftPlanImpl> nf1, nf3;  // NFFT trafo / adjoint stages (grid sets)
   int64_t N = 0, n_star = 0, L1 = 0, L2 = 0, n = 0;
-  int device = 0;
+  int device = 0, mode = 0;
+};
+
+struct sincfft_nfft_plan_s {
+  sfb::NfftPlanImpl impl;
 };
 
 namespace {
@@ -88,6 +93,27 @@ struct InBuf {
   }
 };
 
+struct OutBuf {  // device output, copied back to a host `out` at finish()
+  std::unique_ptr<sfb::Scratch> tmp;
+  void* user;
+  size_t bytes;
+  int32_t kind;
+  void* ptr;
+  OutBuf(void* u, size_t b, int32_t k, cudaStream_t s) : user(u), bytes(b), kind(k) {
+    if (kind == SINCFFT_PTR_DEVICE) {
+      ptr = user;
+    } else {
+      tmp.reset(new sfb::Scratch(bytes, s));
+      ptr = tmp->p;
+    }
+  }
+  void finish(cudaStream_t s) {
+    if (kind == SINCFFT_PTR_DEVICE) return;
+    if (bytes) SF_CUDA(cudaMemcpyAsync(user, ptr, bytes, cudaMemcpyDeviceToHost, s));
+    if (kind == SINCFFT_PTR_HOST) SF_CUDA(cudaStreamSynchronize(s));
+  }
+};
+
 void set_device(int dev) {
   int cur = -1;
   SF_CUDA(cudaGetDevice(&cur));
@@ -108,6 +134,25 @@ void set_device(int dev) {
 __global__ void k_scale_copy(const double* in, double* out, int64_t n, double s) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) out[i] = s * in[i];
+}
+
+// t = np.mod(q z + 0.5, 1.0) - 0.5 with numpy's float mod (fast_sinc.py:118-120)
+__global__ void k_wrap_half(const double* z, double* out, int64_t n, double q) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double a = q * z[i] + 0.5;
+  double r = fmod(a, 1.0);
+  if (r != 0.0) {
+    if (r < 0.0) r += 1.0;
+  } else {
+    r = 0.0;
+  }
+  out[i] = r - 0.5;
+}
+
+__global__ void k_real_to_complex(const double* in, double2* out, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_double2(in[i], 0.0);
 }
 
 void fill_geometry(const sfb::NnfftPlanImpl& p, sincfft_geometry* g) {
@@ -488,8 +533,8 @@ int sincfft_nnfft_export_tables(sincfft_nnfft_plan plan, int64_t* spread_idx, do
 int sincfft_sinc_plan_create(sincfft_sinc_plan* plan, int64_t N, int64_t n_star, int64_t L1,
                              int64_t L2, int64_t n, const double* z, const double* w,
                              const double* a, const double* b, double sigma1, double sigma2,
-                             int32_t m1, int32_t m2, int32_t ptr_kind, int32_t device,
-                             void* stream) {
+                             int32_t m1, int32_t m2, int32_t mode, int32_t ptr_kind,
+                             int32_t device, void* stream) {
   return guarded([&] {
     if (!plan) sfb::fail(1, "plan pointer is NULL");
     *plan = nullptr;
@@ -497,11 +542,17 @@ int sincfft_sinc_plan_create(sincfft_sinc_plan* plan, int64_t N, int64_t n_star,
     if (!z || !w || !a || !b) sfb::fail(1, "sinc_plan: NULL node/weight array");
     if (N <= 0 || n_star < N || n < 2 || L1 <= 0 || L2 <= 0)
       sfb::fail(1, "sinc_plan: invalid sizes");
+    if (mode < SINCFFT_SINC_GENERAL || mode > SINCFFT_SINC_EQUISPACED_BOTH)
+      sfb::fail(1, "sinc_plan: unknown mode");
+    const bool nfft1 = mode == SINCFFT_SINC_EQUISPACED_SOURCES || mode == SINCFFT_SINC_EQUISPACED_BOTH;
+    const bool nfft3 = mode == SINCFFT_SINC_EQUISPACED_TARGETS || mode == SINCFFT_SINC_EQUISPACED_BOTH;
+    if (nfft3 && L2 != N) sfb::fail(1, "sinc_plan: equispaced-targets mode requires L2 = N");
     set_device(device);
     cudaStream_t s = as_stream(stream);
     auto* h = new sincfft_sinc_plan_s();
     try {
       h->N = N, h->n_star = n_star, h->L1 = L1, h->L2 = L2, h->n = n, h->device = device;
+      h->mode = mode;
       const int64_t nz = n + 1;
       InBuf zb(z, sizeof(double) * nz, ptr_kind, s), wb(w, sizeof(double) * nz, ptr_kind, s),
           ab(a, sizeof(double) * L1, ptr_kind, s), bb(b, sizeof(double) * L2, ptr_kind, s);
@@ -513,14 +564,35 @@ int sincfft_sinc_plan_create(sincfft_sinc_plan* plan, int64_t N, int64_t n_star,
       k_scale_copy<<<gz, 256, 0, s>>>((const double*)zb.ptr, x1.as<double>(), nz, 0.5);
       k_scale_copy<<<gz, 256, 0, s>>>((const double*)zb.ptr, v3.as<double>(), nz, -0.5 * scale);
       SF_LAUNCH_CHECK();
-      // plan1 = nnfft_plan(n_star, a*scale, z/2)      (fast_sinc.py:205-209)
-      build_nnfft(h->st1, n_star, L1, nz, sigma1, sigma2, m1, m2, v1.as<double>(),
-                  x1.as<double>(), device, s);
-      // alpha = w * g fused into stage-1's gather scale (fast_sinc.py:246)
-      sfb::fuse_target_weights(h->st1, (const double*)wb.ptr, s);
-      // plan3 = nnfft_plan(n_star, -(scale/2) z, b)   (fast_sinc.py:216-220)
-      build_nnfft(h->st3, n_star, nz, L2, sigma1, sigma2, m1, m2, v3.as<double>(),
-                  (const double*)bb.ptr, device, s);
+      if (nfft1) {
+        // plan1 = nfft_plan(L1, wrap(-(N/(2 L1)) z), sigma1, m1)  (fast_sinc.py:200-203)
+        sfb::Scratch t1(sizeof(double) * nz, s);
+        k_wrap_half<<<gz, 256, 0, s>>>((const double*)zb.ptr, t1.as<double>(), nz,
+                                       -((double)N / (2.0 * (double)L1)));
+        SF_LAUNCH_CHECK();
+        h->nf1.reset(new sfb::NfftPlanImpl());
+        sfb::build_nfft(*h->nf1, L1, nz, sigma1, m1, t1.as<double>(), device, s);
+        // alpha = w * g fused into the NFFT gather's scale (fast_sinc.py:246)
+        sfb::fuse_target_weights(h->nf1->tr, (const double*)wb.ptr, s);
+      } else {
+        // plan1 = nnfft_plan(n_star, a*scale, z/2)      (fast_sinc.py:205-209)
+        build_nnfft(h->st1, n_star, L1, nz, sigma1, sigma2, m1, m2, v1.as<double>(),
+                    x1.as<double>(), device, s);
+        // alpha = w * g fused into stage-1's gather scale (fast_sinc.py:246)
+        sfb::fuse_target_weights(h->st1, (const double*)wb.ptr, s);
+      }
+      if (nfft3) {
+        // plan3 = nfft_plan(N, -z/2, sigma1, m1), applied as the adjoint (fast_sinc.py:211-214)
+        sfb::Scratch t3(sizeof(double) * nz, s);
+        k_scale_copy<<<gz, 256, 0, s>>>((const double*)zb.ptr, t3.as<double>(), nz, -0.5);
+        SF_LAUNCH_CHECK();
+        h->nf3.reset(new sfb::NfftPlanImpl());
+        sfb::build_nfft(*h->nf3, N, nz, sigma1, m1, t3.as<double>(), device, s);
+      } else {
+        // plan3 = nnfft_plan(n_star, -(scale/2) z, b)   (fast_sinc.py:216-220)
+        build_nnfft(h->st3, n_star, nz, L2, sigma1, sigma2, m1, m2, v3.as<double>(),
+                    (const double*)bb.ptr, device, s);
+      }
       SF_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
       delete h;
@@ -542,8 +614,8 @@ int sincfft_sinc_plan_geometry(sincfft_sinc_plan plan, sincfft_geometry* stage1,
                                sincfft_geometry* stage3) {
   return guarded([&] {
     if (!plan) sfb::fail(1, "NULL plan");
-    if (stage1) fill_geometry(plan->st1, stage1);
-    if (stage3) fill_geometry(plan->st3, stage3);
+    if (stage1) fill_geometry(plan->nf1 ? plan->nf1->tr : plan->st1, stage1);
+    if (stage3) fill_geometry(plan->nf3 ? plan->nf3->ad_fft : plan->st3, stage3);
   });
 }
 
@@ -554,53 +626,141 @@ int sincfft_sinc_execute(sincfft_sinc_plan plan, const double* c, int32_t c_is_r
     check_ptr_kind(ptr_kind);
     set_device(plan->device);
     cudaStream_t s = as_stream(stream);
-    const sfb::NnfftPlanImpl& p1 = plan->st1;
-    const sfb::NnfftPlanImpl& p3 = plan->st3;
     const size_t cb = (c_is_real ? sizeof(double) : sizeof(double2)) * (size_t)plan->L1;
     InBuf cin(c, cb, ptr_kind, s);
-    sfb::Scratch g1(sizeof(double2) * (size_t)p1.g.K, s);
-    sfb::Scratch w1(sizeof(double2) * (size_t)p1.fft.work_elems(), s);
-    sfb::Scratch h1(sizeof(double2) * (size_t)p1.fft.Kout, s);
-    sfb::Scratch alpha(sizeof(double2) * (size_t)p1.g.M2, s);
-    if (c_is_real) sfb::run_spread_real(p1, (const double*)cin.ptr, g1.as<double2>(), s);
-    else sfb::run_spread(p1, (const double2*)cin.ptr, g1.as<double2>(), 1, s);
-    sfb::run_fft(p1, g1.as<double2>(), h1.as<double2>(), w1.as<double2>(), 1, s);
-    sfb::run_gather(p1, h1.as<double2>(), alpha.as<double2>(), 1, s);
+    const int64_t nz = plan->n + 1;
+    sfb::Scratch alpha(sizeof(double2) * (size_t)nz, s);
+    if (plan->nf1) {
+      // stage 1 = NFFT trafo of c (complex; real input promoted like the reference)
+      const double2* cc = (const double2*)cin.ptr;
+      sfb::Scratch cz(c_is_real ? sizeof(double2) * (size_t)plan->L1 : 1, s);
+      if (c_is_real) {
+        k_real_to_complex<<<(unsigned)sfb::ceil_div(plan->L1, 256), 256, 0, s>>>(
+            (const double*)cin.ptr, cz.as<double2>(), plan->L1);
+        SF_LAUNCH_CHECK();
+        cc = cz.as<double2>();
+      }
+      sfb::run_nfft_trafo(*plan->nf1, cc, alpha.as<double2>(), s);
+    } else {
+      const sfb::NnfftPlanImpl& p1 = plan->st1;
+      sfb::Scratch g1(sizeof(double2) * (size_t)p1.g.K, s);
+      sfb::Scratch w1(sizeof(double2) * (size_t)p1.fft.work_elems(), s);
+      sfb::Scratch h1(sizeof(double2) * (size_t)p1.fft.Kout, s);
+      if (c_is_real) sfb::run_spread_real(p1, (const double*)cin.ptr, g1.as<double2>(), s);
+      else sfb::run_spread(p1, (const double2*)cin.ptr, g1.as<double2>(), 1, s);
+      sfb::run_fft(p1, g1.as<double2>(), h1.as<double2>(), w1.as<double2>(), 1, s);
+      sfb::run_gather(p1, h1.as<double2>(), alpha.as<double2>(), 1, s);
+    }
     const size_t ob = sizeof(double2) * (size_t)plan->L2;
+    auto stage3 = [&](double2* dst) {
+      if (plan->nf3) sfb::run_nfft_adjoint(*plan->nf3, alpha.as<double2>(), dst, s);
+      else sfb::run_execute(plan->st3, alpha.as<double2>(), dst, 1, s);
+    };
     if (ptr_kind == SINCFFT_PTR_DEVICE) {
-      sfb::run_execute(p3, alpha.as<double2>(), (double2*)out, 1, s);
+      stage3((double2*)out);
     } else {
       sfb::Scratch o(ob, s);
-      sfb::run_execute(p3, alpha.as<double2>(), o.as<double2>(), 1, s);
+      stage3(o.as<double2>());
       SF_CUDA(cudaMemcpyAsync(out, o.p, ob, cudaMemcpyDeviceToHost, s));
       if (ptr_kind == SINCFFT_PTR_HOST) SF_CUDA(cudaStreamSynchronize(s));
     }
   });
 }
 
-// ---------------------------------------------------------------- direct sums
-namespace {
-struct OutBuf {  // device output, copied back to a host `out` at finish()
-  std::unique_ptr<sfb::Scratch> tmp;
-  void* user;
-  size_t bytes;
-  int32_t kind;
-  void* ptr;
-  OutBuf(void* u, size_t b, int32_t k, cudaStream_t s) : user(u), bytes(b), kind(k) {
-    if (kind == SINCFFT_PTR_DEVICE) {
-      ptr = user;
-    } else {
-      tmp.reset(new sfb::Scratch(bytes, s));
-      ptr = tmp->p;
+// ------------------------------------------------------------- classical NFFT
+int sincfft_nfft_plan_create(sincfft_nfft_plan* plan, int64_t N, int64_t M, double sigma,
+                             int32_t m, const double* x, int32_t ptr_kind, int32_t device,
+                             void* stream) {
+  return guarded([&] {
+    if (!plan) sfb::fail(1, "plan pointer is NULL");
+    *plan = nullptr;
+    check_ptr_kind(ptr_kind);
+    if (!x) sfb::fail(1, "nfft_plan: NULL nodes");
+    if (N <= 0 || N % 2) sfb::fail(1, "nfft_plan: N must be a positive even integer");
+    if (M <= 0) sfb::fail(1, "nfft_plan: nodes must be a nonempty 1-d array");
+    set_device(device);
+    cudaStream_t s = as_stream(stream);
+    auto* h = new sincfft_nfft_plan_s();
+    try {
+      InBuf xb(x, sizeof(double) * M, ptr_kind, s);
+      sfb::build_nfft(h->impl, N, M, sigma, m, (const double*)xb.ptr, device, s);
+      SF_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      delete h;
+      throw;
     }
-  }
-  void finish(cudaStream_t s) {
-    if (kind == SINCFFT_PTR_DEVICE) return;
-    if (bytes) SF_CUDA(cudaMemcpyAsync(user, ptr, bytes, cudaMemcpyDeviceToHost, s));
-    if (kind == SINCFFT_PTR_HOST) SF_CUDA(cudaStreamSynchronize(s));
-  }
-};
-}  // namespace
+    *plan = h;
+  });
+}
+
+int sincfft_nfft_plan_destroy(sincfft_nfft_plan plan) {
+  return guarded([&] {
+    if (!plan) return;
+    set_device(plan->impl.device);
+    delete plan;
+  });
+}
+
+int sincfft_nfft_plan_geometry(sincfft_nfft_plan plan, int64_t* n_over, sincfft_geometry* trafo,
+                               sincfft_geometry* adjoint) {
+  return guarded([&] {
+    if (!plan) sfb::fail(1, "NULL plan");
+    if (n_over) *n_over = plan->impl.n_over;
+    if (trafo) fill_geometry(plan->impl.tr, trafo);
+    if (adjoint) fill_geometry(plan->impl.ad_fft, adjoint);
+  });
+}
+
+int sincfft_nfft_trafo(sincfft_nfft_plan plan, const double* c, double* out, int32_t ptr_kind,
+                       void* stream) {
+  return guarded([&] {
+    if (!plan || !c || !out) sfb::fail(1, "NULL argument");
+    check_ptr_kind(ptr_kind);
+    const sfb::NfftPlanImpl& p = plan->impl;
+    set_device(p.device);
+    cudaStream_t s = as_stream(stream);
+    InBuf cb(c, sizeof(double2) * (size_t)p.N, ptr_kind, s);
+    OutBuf ob(out, sizeof(double2) * (size_t)p.M, ptr_kind, s);
+    sfb::run_nfft_trafo(p, (const double2*)cb.ptr, (double2*)ob.ptr, s);
+    ob.finish(s);
+  });
+}
+
+int sincfft_nfft_adjoint(sincfft_nfft_plan plan, const double* y, double* out, int32_t ptr_kind,
+                         void* stream) {
+  return guarded([&] {
+    if (!plan || !y || !out) sfb::fail(1, "NULL argument");
+    check_ptr_kind(ptr_kind);
+    const sfb::NfftPlanImpl& p = plan->impl;
+    set_device(p.device);
+    cudaStream_t s = as_stream(stream);
+    InBuf yb(y, sizeof(double2) * (size_t)p.M, ptr_kind, s);
+    OutBuf ob(out, sizeof(double2) * (size_t)p.N, ptr_kind, s);
+    sfb::run_nfft_adjoint(p, (const double2*)yb.ptr, (double2*)ob.ptr, s);
+    ob.finish(s);
+  });
+}
+
+int sincfft_nfft_export_tables(sincfft_nfft_plan plan, int64_t* spread_idx, double* spread_val,
+                               double* hat) {
+  return guarded([&] {
+    if (!plan) sfb::fail(1, "NULL plan");
+    const sfb::NfftPlanImpl& p = plan->impl;
+    set_device(p.device);
+    cudaStream_t s = 0;
+    const int64_t n = p.M * 2 * p.m;
+    sfb::Scratch di(sizeof(int64_t) * n, s), dv(sizeof(double) * n, s), dh(sizeof(double) * p.N, s);
+    sfb::export_nfft(p, di.as<int64_t>(), dv.as<double>(), dh.as<double>(), s);
+    if (spread_idx)
+      SF_CUDA(cudaMemcpyAsync(spread_idx, di.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+    if (spread_val)
+      SF_CUDA(cudaMemcpyAsync(spread_val, dv.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    if (hat) SF_CUDA(cudaMemcpyAsync(hat, dh.p, sizeof(double) * p.N, cudaMemcpyDeviceToHost, s));
+    SF_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// ---------------------------------------------------------------- direct sums
 
 int sincfft_nndft_direct(const double* f, const double* v, int64_t M1, const double* x,
                          int64_t M2, int64_t N, double* out, int32_t ptr_kind, int32_t device,

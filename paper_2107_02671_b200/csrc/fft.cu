@@ -74,7 +74,7 @@ __global__ void k_prechirp(double2* P, const double* hat2, int64_t K, int64_t N2
   if (l >= K) return;
   // exponent 2e = 2 l s_lo + l^2, reduced exactly (|.| < 2^62 for K, N2 < 2^30)
   const int64_t e2 = (2 * l * (s_lo % (2 * N2))) % (2 * N2) + (l * l) % (2 * N2);
-  const double d = inv_n1n2 / hat2[l];
+  const double d = hat2 ? inv_n1n2 / hat2[l] : inv_n1n2;  // no deconvolution: NFFT adjoint
   P[l] = cscale(wpow_half(e2, N2), d);
 }
 
@@ -116,6 +116,7 @@ struct FftArgs {
   const int* rev2;
   int64_t K, L, L1, L2, Kout;
   int C_log2;
+  int conj_in;         // conjugate the input (inverse DFT via conj(F(conj x)))
   FftStages st1, st2;
 };
 
@@ -138,7 +139,11 @@ __global__ void __launch_bounds__(512) k_single(FftArgs a, int spectrum) {
       const int i = i0 + u * T;
       v[u] = make_double2(0.0, 0.0);
       if (MODE == IN_GP) {
-        if (i < a.K) v[u] = cmul(__ldg(g + i), __ldg(a.P + i));
+        if (i < a.K) {
+          double2 gv = __ldg(g + i);
+          if (a.conj_in) gv.y = -gv.y;
+          v[u] = cmul(gv, __ldg(a.P + i));
+        }
       } else if (i < L) {
         v[u] = __ldg(g + i);
       }
@@ -201,7 +206,11 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd(FftArgs a) {
       v[u] = make_double2(0.0, 0.0);
       if (e < n_el && n1 < a.L1) {
         if (MODE == IN_GP) {
-          if (n < a.K) v[u] = cmul(__ldg(g + n), __ldg(a.P + n));
+          if (n < a.K) {
+            double2 gv = __ldg(g + n);
+            if (a.conj_in) gv.y = -gv.y;
+            v[u] = cmul(gv, __ldg(a.P + n));
+          }
         } else {
           v[u] = __ldg(g + n);
         }
@@ -481,6 +490,7 @@ struct DirectArgs {
   int64_t K, N2, A, P, LP, Kout, s_lo;
   int C_log2, R_log2;
   int p_smooth;
+  int conj_in;
   FftStages stA, stP;
 };
 
@@ -506,7 +516,11 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_dstep1(DirectArgs a) {
         int64_t l = -1;
         if (n < a.K - halfK) l = n + halfK;                     // n in [0, K/2)
         else if (n >= a.N2 - halfK) l = n - a.N2 + halfK;       // n in [N2 - K/2, N2)
-        if (l >= 0) v[u] = cscale(__ldg(g + l), __ldg(a.D + l));
+        if (l >= 0) {
+          double2 gv = __ldg(g + l);
+          if (a.conj_in) gv.y = -gv.y;
+          v[u] = cscale(gv, __ldg(a.D + l));
+        }
       }
     }
 #pragma unroll
@@ -617,7 +631,7 @@ __global__ void k_chirp_p(double2* cp, int64_t P) {
 
 __global__ void k_deconv(double* D, const double* hat2, int64_t K, double inv_n1n2) {
   const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (l < K) D[l] = inv_n1n2 / hat2[l];
+  if (l < K) D[l] = hat2 ? inv_n1n2 / hat2[l] : inv_n1n2;
 }
 
 // ------------------------------------------------------------ host planning
@@ -756,6 +770,7 @@ FftArgs make_args(const NnfftPlanImpl& p) {
   a.L2 = f.L2;
   a.Kout = f.Kout;
   a.C_log2 = f.C_log2;
+  a.conj_in = f.conj_in ? 1 : 0;
   a.st1 = f.st1;
   a.st2 = f.st2;
   return a;
@@ -823,8 +838,7 @@ void build_direct(NnfftPlanImpl& p, cudaStream_t s) {
   upload(d.revA, digit_reverse(d.stA));
   if (d.p_smooth) upload(d.revP, digit_reverse(d.stP));
   d.D.alloc(g.K);
-  k_deconv<<<(unsigned)ceil_div(g.K, 256), 256, 0, s>>>(d.D.p, p.hat2.p, g.K,
-                                                       1.0 / ((double)g.N1 * (double)g.N2));
+  k_deconv<<<(unsigned)ceil_div(g.K, 256), 256, 0, s>>>(d.D.p, p.hat2.p, g.K, p.fft.in_scale);
   SF_LAUNCH_CHECK();
   if (!d.p_smooth) {
     d.cp.alloc(d.P);
@@ -868,6 +882,7 @@ DirectArgs make_direct_args(const NnfftPlanImpl& p) {
   a.C_log2 = d.C_log2;
   a.R_log2 = d.R_log2;
   a.p_smooth = d.p_smooth ? 1 : 0;
+  a.conj_in = p.fft.conj_in ? 1 : 0;
   a.stA = d.stA;
   a.stP = d.stP;
   return a;
@@ -966,7 +981,7 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   f.P.alloc(g.K);
   f.Q.alloc(f.Kout);
   k_prechirp<<<(unsigned)ceil_div(g.K, 256), 256, 0, s>>>(
-      f.P.p, p.hat2.p, g.K, g.N2, f.s_lo, 1.0 / ((double)g.N1 * (double)g.N2));
+      f.P.p, p.hat2.p, g.K, g.N2, f.s_lo, f.in_scale);
   SF_LAUNCH_CHECK();
   k_postchirp<<<(unsigned)ceil_div(f.Kout, 256), 256, 0, s>>>(f.Q.p, f.Kout, g.K, g.N2, f.s_lo);
   SF_LAUNCH_CHECK();

@@ -25,6 +25,7 @@ struct GatherArgs {
   double2* out;      // (M2, batch) row-major
   int64_t M2, Kout, N2, s_lo;
   int batch;
+  int conj_out;
 };
 
 
@@ -99,13 +100,13 @@ __global__ void __launch_bounds__(kGatherThreads) k_gather(GatherArgs a, WinCoef
   // scattered store, but inside this slice's window of `out` (the plan sorts
   // targets by (original-index slice, position)), which stays L2-resident, so
   // both 16-byte halves of each 32-byte sector merge in L2 before eviction
-  a.out[(int64_t)dst * a.batch + col] = make_double2(s.x * sc, s.y * sc);
+  a.out[(int64_t)dst * a.batch + col] = make_double2(s.x * sc, a.conj_out ? -(s.y * sc) : s.y * sc);
 }
 
 void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batch,
                 cudaStream_t s) {
   GatherArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, p.gp.span.p, h, out,
-               p.g.M2,     p.fft.Kout,  p.g.N2,        p.fft.s_lo,  batch};
+               p.g.M2,     p.fft.Kout,  p.g.N2,        p.fft.s_lo,  batch, p.gp.conj_out ? 1 : 0};
   const dim3 grid((unsigned)ceil_div(p.g.M2, kGatherThreads), batch);
   switch (p.g.m2) {
 #define SF_CASE(MM)                                          \

@@ -74,6 +74,7 @@ constexpr int kGatherThreads = 256;  // targets per gather CTA
 constexpr int kGatherSpan = 2048;    // h values staged per CTA (32 KiB)
 
 struct GatherPlan {
+  bool conj_out = false;  // store conj(out) (pairs with FftPlan::conj_in)
   DevArray<double> pos;
   DevArray<int> perm;
   DevArray<double> scale;
@@ -103,6 +104,8 @@ struct DirectFft {
 
 struct FftPlan {
   int64_t L = 0, L1 = 0, L2 = 0, Kout = 0, s_lo = 0;
+  double in_scale = 0.0;  // input factor: 1/(N1 N2) (NNFFT, with 1/phi_hat_2), 1/n_over (NFFT)
+  bool conj_in = false;   // inverse DFT as conj(F(conj x)) (NFFT trafo; gather conjugates)
   int C = 1, C_log2 = 0;  // columns per CTA in the column kernels
   bool single = true;     // L fits one CTA
   bool direct = false;    // DirectFft path instead of the Bluestein over L

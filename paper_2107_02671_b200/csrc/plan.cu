@@ -603,6 +603,7 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
   ts.N1 = g.N1;
   build_targets(p, p.x_clip.p, g.M2, (double)g.N / (double)g.N1, g.N2, g.m2, ts, s);
 
+  p.fft.in_scale = 1.0 / ((double)g.N1 * (double)g.N2);
   build_fft(p, s);
   SF_CUDA(cudaStreamSynchronize(s));
 }

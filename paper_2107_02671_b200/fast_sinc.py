@@ -4,12 +4,13 @@ drop-in for ``sincfft.fast_sinc`` (reference: ``pkg/src/sincfft/fast_sinc.py``).
     h(b_l) = sum_k c_k sinc(N pi (b_l - a_k))
            ~ sum_j w_j e^{+pi i N z_j b_l} sum_k c_k e^{-pi i N z_j a_k}
 
-computed as NNFFT (sources -> Chebyshev nodes z/2) -> times w -> NNFFT
-(Chebyshev nodes -> targets), both NNFFTs on the GPU with the weight multiply
-fused into the first stage's gather.  Mode detection and validation follow the
-reference exactly; every layout is computed through the GENERAL route (the
-equispaced NFFT routes are the next scope row; the
-reference pins GENERAL vs EQUISPACED_TARGETS to 1e-11, test_acceptance.py:161).
+computed as stage 1 (sources -> Chebyshev nodes z/2) -> times w -> stage 3
+(Chebyshev nodes -> targets) on the GPU, with the weight multiply fused into
+stage 1's gather.  Mode detection, forcing and validation follow the
+reference exactly, and so does the route (fast_sinc.py:198-220): a stage runs
+as an NNFFT, or -- when its node set is the even grid -- as the classical
+NFFT trafo (equispaced sources) / NFFT adjoint (equispaced targets), which
+skips one window stage (``paper_2107_02671_b200.nfft``).
 """
 
 from __future__ import annotations
@@ -36,6 +37,10 @@ class SincMode(enum.Enum):
     EQUISPACED_SOURCES = "equispaced-sources"
     EQUISPACED_TARGETS = "equispaced-targets"
     EQUISPACED_BOTH = "equispaced-both"
+
+
+_MODE_CODE = {SincMode.GENERAL: 0, SincMode.EQUISPACED_SOURCES: 1,
+              SincMode.EQUISPACED_TARGETS: 2, SincMode.EQUISPACED_BOTH: 3}
 
 
 def _even_bandwidth(N, sigma1, m1):
@@ -72,7 +77,10 @@ class SincPlan:
         (self.m1, self.m2, self.sigma1, self.sigma2, self.window1, self.window2) = params
         self.n_star = n_star
         self.inner_geometry = inner_geometry
-        self.route = "general"
+        self.route = {SincMode.GENERAL: "nnfft/nnfft",
+                      SincMode.EQUISPACED_SOURCES: "nfft/nnfft",
+                      SincMode.EQUISPACED_TARGETS: "nnfft/adjoint",
+                      SincMode.EQUISPACED_BOTH: "nfft/adjoint"}[mode]
         self.device = device
 
     def __del__(self):
@@ -162,7 +170,8 @@ def sinc_plan(N, a, b, *, n=None, epsilon=None, m1=6, m2=6, sigma1=2.0, sigma2=2
         C.byref(h), int(N), n_star, a.size, b.size, int(n),
         C.c_void_p(z.ctypes.data), C.c_void_p(w.ctypes.data),
         C.c_void_p(a.ctypes.data), C.c_void_p(b.ctypes.data),
-        float(sigma1), float(sigma2), int(m1), int(m2), _lib.PTR_HOST, dev, None))
+        float(sigma1), float(sigma2), int(m1), int(m2), _MODE_CODE[mode], _lib.PTR_HOST, dev,
+        None))
     return SincPlan(h, int(N), int(n), quad, a, b, mode, params, n_star, inner, dev)
 
 
