@@ -70,7 +70,12 @@ constexpr int kBatchedMin = 16;  // columns from which the column-vectorised pat
 constexpr int64_t kGatherSliceDefault = (int64_t)1 << 20;
 int64_t gather_slice();  // kGatherSliceDefault unless SFB_GATHER_SLICE_LOG2 is set (tuning)
 
-constexpr int kGatherThreads = 256;  // targets per gather CTA
+constexpr int kGatherThreads = 256;  // threads per gather CTA
+#ifndef SFB_GATHER_TPT
+#define SFB_GATHER_TPT 2
+#endif
+constexpr int kGatherTPT = SFB_GATHER_TPT;                 // targets per thread
+constexpr int kGatherGroup = kGatherThreads * kGatherTPT;  // targets per CTA
 constexpr int kGatherSpan = 2048;    // h values staged per CTA (32 KiB)
 
 struct GatherPlan {

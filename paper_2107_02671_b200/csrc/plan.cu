@@ -267,13 +267,13 @@ __global__ void k_tgt_tables(const double* x, const int* perm, int64_t n, double
   if (!(hat > 0.0)) atomicAdd(min_hat_bits, 1ull);
 }
 
-// h range [klo, khi] (k' = s - s_lo) read by each gather CTA of kGatherThreads
+// h range [klo, khi] (k' = s - s_lo) read by each gather CTA of kGatherGroup
 // sorted targets; {-1, -1} (never staged) if it does not fit in int
 __global__ void k_gather_spans(const double* pos, int64_t n, int64_t nblk, int m2, int64_t s_lo,
                                int2* span) {
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= nblk) return;
-  const int64_t j0 = b * kGatherThreads, jl = min(j0 + kGatherThreads, n) - 1;
+  const int64_t j0 = b * kGatherGroup, jl = min(j0 + kGatherGroup, n) - 1;
   const int64_t lo = (int64_t)floor(pos[j0]) + 1 - m2 - s_lo;
   const int64_t hi = (int64_t)floor(pos[jl]) + m2 - s_lo;
   span[b] = (lo >= 0 && hi < (1ll << 31) && lo <= hi) ? make_int2((int)lo, (int)hi)
@@ -547,7 +547,7 @@ void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, 
     const int64_t s_hi = (int64_t)std::floor(phi) + m2;
     p.fft.s_lo = s_lo;
     p.fft.Kout = std::min<int64_t>(s_hi - s_lo + 1, N2);
-    const int64_t nblk = ceil_div(M2, kGatherThreads);
+    const int64_t nblk = ceil_div(M2, kGatherGroup);
     p.gp.span.alloc(nblk);
     k_gather_spans<<<blocks(nblk), 256, 0, s>>>(p.gp.pos.p, M2, nblk, m2, s_lo, p.gp.span.p);
     SF_LAUNCH_CHECK();

@@ -193,6 +193,50 @@ __device__ __forceinline__ void window_accumulate2(const WinCoef& C, double d0, 
   }
 }
 
+// Gather form of window_accumulate2: two targets (d0 over h0[0..2M), d1 over
+// h1[0..2M)) interpolated together, every coefficient feeding both Horner
+// chains and each tap pair consumed as soon as it is formed (no tap arrays).
+template <int M>
+__device__ __forceinline__ void window_dot2(const WinCoef& C, double d0, double d1,
+                                            const double2* h0, const double2* h1, double2& s0,
+                                            double2& s1) {
+  constexpr int P = window_degree(M);
+  constexpr int NE = P / 2 + 1;
+  constexpr int NO = (P + 1) / 2;
+  const double u0 = 2.0 * d0 - 1.0, u1 = 2.0 * d1 - 1.0;
+  const double v0 = u0 * u0, v1 = u1 * u1;
+  const double sh0 = sqrt(d0), sl0 = sqrt(1.0 - d0), sh1 = sqrt(d1), sl1 = sqrt(1.0 - d1);
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    double E0 = C.e[q][NE - 1], E1 = E0;
+#pragma unroll
+    for (int k = NE - 2; k >= 0; --k) {
+      const double c = C.e[q][k];
+      E0 = fma(E0, v0, c);
+      E1 = fma(E1, v1, c);
+    }
+    double O0 = C.o[q][NO - 1], O1 = O0;
+#pragma unroll
+    for (int k = NO - 2; k >= 0; --k) {
+      const double c = C.o[q][k];
+      O0 = fma(O0, v0, c);
+      O1 = fma(O1, v1, c);
+    }
+    double hi0 = fma(u0, O0, E0), lo0 = fma(-u0, O0, E0);
+    double hi1 = fma(u1, O1, E1), lo1 = fma(-u1, O1, E1);
+    const int ih = (q < M - 1) ? M + q : 2 * M - 1;
+    const int il = (q < M - 1) ? M - 1 - q : 0;
+    if (q == M - 1) {
+      hi0 *= sh0, lo0 *= sl0, hi1 *= sh1, lo1 *= sl1;
+    }
+    const double2 a0 = h0[ih], b0 = h0[il], a1 = h1[ih], b1 = h1[il];
+    s0.x = fma(a0.x, hi0, fma(b0.x, lo0, s0.x));
+    s0.y = fma(a0.y, hi0, fma(b0.y, lo0, s0.y));
+    s1.x = fma(a1.x, hi1, fma(b1.x, lo1, s1.x));
+    s1.y = fma(a1.y, hi1, fma(b1.y, lo1, s1.y));
+  }
+}
+
 // Fourier transform of the sinh shape function, omega_hat(v)
 // (windows.py:143-160), all three branches; on the NNFFT path only the
 // w > 1e-3 branch is reachable.
