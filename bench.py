@@ -421,7 +421,9 @@ def run_b200(args, cfg):
                                                   h_out[k % nbuf].data_ptr(), B,
                                                   _lib.PTR_HOST_ASYNC, st))
 
-    for k in range(max(2, args.warmup)):
+    # warm every stream's buffers and the stream-ordered pool (its first
+    # growth costs a few ms of host time per allocation)
+    for k in range(max(3 * nbuf, args.warmup)):
         e2e_step(k)
     barrier()
     ev0.record(stream)

@@ -85,7 +85,7 @@ class SincPlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None and getattr(_lib, "lib", None) is not None:
             _lib.lib.sincfft_sinc_plan_destroy(h)
             self._h = None
 

@@ -45,7 +45,7 @@ class NfftPlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None and getattr(_lib, "lib", None) is not None:
             _lib.lib.sincfft_nfft_plan_destroy(h)
             self._h = None
 

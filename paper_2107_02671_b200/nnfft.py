@@ -170,7 +170,7 @@ class NnfftPlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None and getattr(_lib, "lib", None) is not None:
             _lib.lib.sincfft_nnfft_plan_destroy(h)
             self._h = None
 
