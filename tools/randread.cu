@@ -22,6 +22,29 @@ __global__ void k_read(const double2* __restrict__ f, const int* __restrict__ id
   if (acc.x == 12345.0) out[0] = acc;
 }
 
+// variants of the same random 16-byte read: 0 ld.global.nc, 1 ld.global.cg
+// (L2 only), 2 ld.global.nc.L2::64B, 3 ld.global.nc.L2::128B,
+// 4 ld.global.nc.L1::no_allocate, 5 8-byte reads of .x only
+template <int V>
+__global__ void k_read_v(const double2* __restrict__ f, const int* __restrict__ idx, int n,
+                         double2* out) {
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double2* p = f + idx[i];
+    double a = 0.0, b = 0.0;
+    if (V == 0) asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+    if (V == 1) asm volatile("ld.global.cg.v2.f64 {%0,%1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+    if (V == 2) asm volatile("ld.global.nc.L2::64B.v2.f64 {%0,%1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+    if (V == 3) asm volatile("ld.global.nc.L2::128B.v2.f64 {%0,%1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+    if (V == 4)
+      asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                   : "=d"(a), "=d"(b) : "l"(p));
+    if (V == 5) asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(a) : "l"(p));
+    acc += a + b;
+  }
+  if (acc == 12345.0) out[0] = make_double2(acc, 0);
+}
+
 __global__ void k_red(double* g, const int* __restrict__ idx, int n, int K) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int p = idx[i] % K;
@@ -65,6 +88,30 @@ int main() {
       best = std::min(best, ms);
     }
     printf("read window=%ld ms=%.4f  (%.1f GB/s useful)\n", W, best, 16.0 * n / best / 1e6);
+  }
+  {
+    std::iota(h.begin(), h.end(), 0);
+    std::shuffle(h.begin(), h.end(), rng);
+    cudaMemcpy(idx, h.data(), sizeof(int) * n, cudaMemcpyHostToDevice);
+    auto run = [&](auto kern, const char* name) {
+      float best = 1e9;
+      for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(a);
+        kern<<<148 * 8, 256>>>(f, idx, n, out);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        best = std::min(best, ms);
+      }
+      printf("variant %-28s random 16B reads: ms=%.4f\n", name, best);
+    };
+    run(k_read_v<0>, "ld.global.nc");
+    run(k_read_v<1>, "ld.global.cg");
+    run(k_read_v<2>, "ld.global.nc.L2::64B");
+    run(k_read_v<3>, "ld.global.nc.L2::128B");
+    run(k_read_v<4>, "nc.L1::no_allocate");
+    run(k_read_v<5>, "8-byte .x only");
   }
   // RED: coalesced-ish (index i) vs random over the grid
   for (int mode = 0; mode < 2; ++mode) {
