@@ -482,7 +482,8 @@ int sincfft_nnfft_execute_profiled(sincfft_nnfft_plan plan, const double* f, dou
 
 int sincfft_nnfft_launches_per_execute(sincfft_nnfft_plan plan, int64_t batch) {
   if (!plan) return -1;
-  const int fft = plan->impl.fft.single ? 1 : plan->impl.fft.direct ? 2 : 3;
+  const int fft = plan->impl.fft.single ? 1 : plan->impl.fft.direct ? 2
+                                            : 3 + (plan->impl.fft.fixD > 0 ? 1 : 0);
   // column-vectorised batch: halo zeroing + spread + [2 transposes] + FFT + gather
   if (batch >= sfb::kBatchedMin)
     return 1 + 1 + (sfb::fft_supports_point_major(plan->impl) ? 0 : 2) + fft + 1;

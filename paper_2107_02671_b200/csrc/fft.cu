@@ -36,8 +36,12 @@ namespace sfb {
 
 constexpr int kSingleMax = 8192;      // largest L done by one CTA
 constexpr int kRowMax = 8192;         // largest row length L1
-constexpr int kColElems = 4096;       // C * L2 per column-kernel CTA
+#ifndef SFB_FFT_COLELEMS
+#define SFB_FFT_COLELEMS 4096
+#endif
+constexpr int kColElems = SFB_FFT_COLELEMS;  // C * L2 per column-kernel CTA
 constexpr int kTwSplit = 4096;        // two-level W_L table split
+constexpr int64_t kFixMax = 2048;     // largest shortfall D of a short Bluestein length
 
 enum { IN_GP = 0, IN_PLAIN = 1 };     // input mode: g*P (execute) or plain array (plan)
 
@@ -99,6 +103,56 @@ __global__ void k_chirp_kernel(double2* b, int64_t L, int64_t K, int64_t Kout, i
   }
   const int64_t m = 2 * N2;
   b[i] = wpow_half(-((j * j) % m), N2);
+}
+
+// Short cyclic length (L = K + Kout - 1 - D, 0 < D <= kFixMax): the chirp
+// slots i in [L - K + 1, Kout - 1] are claimed by both j = i and j = i - L;
+// k_chirp_kernel keeps j = i, so for k' < D the terms l >= K - D + k' used
+// b_{k'-l+L} instead of b_{k'-l}.  The fix adds, after the inverse pass,
+//   Q_k' * sum_{t=k'}^{D-1} a_{K-D+t} c_{t-k'},  a_l = g_l P_l,
+//   c_u = b_{-(K-D)-u} - b_{-(K-D)-u+L}   (a D-point correlation, D^2/2 MACs)
+// which lets the planner take a much smoother L (config 3: 2^22 instead of
+// 4096 * 1029 at D = 79).
+__global__ void k_fix_table(double2* c, int64_t D, int64_t K, int64_t L, int64_t N2) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= D) return;
+  const int64_t m = 2 * N2;
+  const int64_t j1 = -(K - D) - u, j2 = j1 + L;
+  const double2 b1 = wpow_half(-((j1 % m) * (j1 % m) % m), N2);
+  const double2 b2 = wpow_half(-((j2 % m) * (j2 % m) % m), N2);
+  c[u] = make_double2(b1.x - b2.x, b1.y - b2.y);
+}
+
+// one warp per (k' < D, column); grid/h column-major ([B][K], [B][Kout]) or
+// point-major ([K][B], [Kout][B])
+__global__ void k_bluestein_fix(const double2* __restrict__ g, const double2* __restrict__ P,
+                                const double2* __restrict__ c, const double2* __restrict__ Q,
+                                double2* h, int64_t K, int64_t D, int64_t Kout, int conj_in,
+                                int B, int point_major) {
+  const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int col = blockIdx.y;
+  if (k >= D) return;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int64_t t = k + lane; t < D; t += 32) {
+    const int64_t l = K - D + t;
+    double2 gv = point_major ? g[l * B + col] : g[(int64_t)col * K + l];
+    if (conj_in) gv.y = -gv.y;
+    const double2 av = cmul(gv, P[l]);
+    const double2 cv = c[t - k];
+    acc.x += av.x * cv.x - av.y * cv.y;
+    acc.y += av.x * cv.y + av.y * cv.x;
+  }
+  for (int o = 16; o; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+  }
+  if (lane == 0) {
+    const double2 d = cmul(Q[k], acc);
+    double2* hp = point_major ? h + k * B + col : h + (int64_t)col * Kout + k;
+    hp->x += d.x;
+    hp->y += d.y;
+  }
 }
 
 // ------------------------------------------------------------ FFT kernels
@@ -714,14 +768,17 @@ double stage_cost(int64_t n) {
   return c;
 }
 
+// Model cost of the four-step L1 x L2 (smem stage costs per point), with
+// factors calibrated on B200 (config 3: 4096 x 1024 best, 8192-point rows
+// 16 % slower; config 4 point-major: 512 x 512 best, 4096 x 64 1.8x slower).
 double cost(int64_t L1, int64_t L2) {
   double c = (double)(L1 * L2) * (2.0 * stage_cost(L1) + 2.0 * stage_cost(L2) + 12.0);
-  if (L1 > 4096) c *= 1.05;  // one CTA per SM for the longest rows
-  // column kernels move C contiguous elements (16*C bytes) per row: fewer than
-  // 8 columns per CTA wastes DRAM bursts
+  if (L1 > 4096) c *= 1.25;       // rows above 64 KiB: one CTA per SM
+  if (L1 > 16 * L2) c *= 1.3;     // very short columns starve the column kernels
+  // column kernels move C contiguous elements (16*C bytes) per row
   int C = 8;
   while (C > 1 && C * L2 > kColElems) C >>= 1;
-  if (C < 8) c *= 1.0 + 0.12 * (C == 4 ? 1 : C == 2 ? 2 : 3);
+  if (C < 8) c *= 1.0 + 0.04 * (C == 4 ? 1 : C == 2 ? 2 : 3);
   return c;
 }
 
@@ -942,22 +999,29 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   } else {
     f.single = false;
     double best = 1e300;
+    // L may fall short of K + Kout - 1 by D <= Dmax slots (fixed afterwards
+    // by k_bluestein_fix at ~D^2 cost), which admits much smoother lengths
+    const int64_t Dmax = getenv("SFB_FFT_NO_SHORT_L") ? 0 : std::min<int64_t>(kFixMax, Lmin / 8);
     for (int64_t L2 = 2; L2 <= 2048; ++L2) {
       if (!smooth7(L2)) continue;
-      const int64_t L1 = next_smooth(ceil_div(Lmin, L2));
-      if (L1 > kRowMax || L1 < 2) continue;
-      const double c = cost(L1, L2);
-      if (c < best) best = c, f.L1 = L1, f.L2 = L2;
+      for (int pass = 0; pass < 2; ++pass) {
+        const int64_t L1 = next_smooth(ceil_div(pass ? Lmin - Dmax : Lmin, L2));
+        if (L1 > kRowMax || L1 < 2) continue;
+        const int64_t D = std::max<int64_t>(0, Lmin - L1 * L2);
+        const double c = cost(L1, L2) + (double)D * (double)D;
+        if (c < best) best = c, f.L1 = L1, f.L2 = L2;
+      }
     }
     if (const char* e = getenv("SFB_FFT_L1L2")) {  // tuning override "L1xL2"
       long long a1 = 0, a2 = 0;
-      if (sscanf(e, "%lldx%lld", &a1, &a2) == 2 && a1 * a2 >= Lmin && smooth7(a1) &&
+      if (sscanf(e, "%lldx%lld", &a1, &a2) == 2 && a1 * a2 >= Lmin - Dmax && smooth7(a1) &&
           smooth7(a2) && a1 <= kRowMax && a2 <= 2048)
         f.L1 = a1, f.L2 = a2, best = 0;
     }
     if (best >= 1e300)
       fail(5, "FFT length " + std::to_string(Lmin) + " exceeds the supported four-step range");
     f.L = f.L1 * f.L2;
+    f.fixD = std::max<int64_t>(0, Lmin - f.L);
     int C = 8;
     while (C > 1 && C * f.L2 > kColElems) C >>= 1;
     f.C = C;
@@ -990,6 +1054,11 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   DevArray<double2> b(f.L);
   k_chirp_kernel<<<(unsigned)ceil_div(f.L, 256), 256, 0, s>>>(b.p, f.L, g.K, f.Kout, g.N2);
   SF_LAUNCH_CHECK();
+  if (f.fixD > 0) {
+    f.fixc.alloc(f.fixD);
+    k_fix_table<<<(unsigned)ceil_div(f.fixD, 256), 256, 0, s>>>(f.fixc.p, f.fixD, g.K, f.L, g.N2);
+    SF_LAUNCH_CHECK();
+  }
   FftArgs a = make_args(p);
   a.g = b.p;
   if (f.single) {
@@ -1006,6 +1075,16 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
     SF_LAUNCH_CHECK();
   }
   SF_CUDA(cudaStreamSynchronize(s));  // b is released at scope exit
+}
+
+static void launch_fix(const NnfftPlanImpl& p, const double2* grid, double2* h, int batch,
+                       int point_major, cudaStream_t s) {
+  const FftPlan& f = p.fft;
+  if (f.fixD <= 0) return;
+  k_bluestein_fix<<<dim3((unsigned)ceil_div(f.fixD * 32, 256), batch), 256, 0, s>>>(
+      grid, f.P.p, f.fixc.p, f.Q.p, h, p.g.K, f.fixD, f.Kout, f.conj_in ? 1 : 0, batch,
+      point_major);
+  SF_LAUNCH_CHECK();
 }
 
 bool fft_supports_point_major(const NnfftPlanImpl& p) {
@@ -1034,6 +1113,7 @@ void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h
   SF_LAUNCH_CHECK();
   k_colinv_b<<<gc, 256, smc, s>>>(x);
   SF_LAUNCH_CHECK();
+  launch_fix(p, grid, h, batch, 1, s);
 }
 
 void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work, int batch,
@@ -1070,6 +1150,7 @@ void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* w
   SF_LAUNCH_CHECK();
   k_colinv<<<gc, 256, smc, s>>>(a);
   SF_LAUNCH_CHECK();
+  launch_fix(p, grid, h, batch, 0, s);
 }
 
 }  // namespace sfb

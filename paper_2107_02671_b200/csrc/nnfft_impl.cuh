@@ -110,6 +110,8 @@ struct DirectFft {
 struct FftPlan {
   int64_t L = 0, L1 = 0, L2 = 0, Kout = 0, s_lo = 0;
   double in_scale = 0.0;  // input factor: 1/(N1 N2) (NNFFT, with 1/phi_hat_2), 1/n_over (NFFT)
+  int64_t fixD = 0;       // L = K + Kout - 1 - fixD: outputs k' < fixD corrected (fft.cu)
+  DevArray<double2> fixc; // the correction's correlation kernel [fixD]
   bool conj_in = false;   // inverse DFT as conj(F(conj x)) (NFFT trafo; gather conjugates)
   int C = 1, C_log2 = 0;  // columns per CTA in the column kernels
   bool single = true;     // L fits one CTA

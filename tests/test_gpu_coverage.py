@@ -230,3 +230,36 @@ def test_config4_full_size_columns_vs_oracle():
     tab = O.plan(N, vs, x, m1=6, m2=6)
     for b in (0, 7, 19, 31):
         assert relerr(out[:, b], O.trafo(tab, f[:, b]), f[:, b]) <= TOL, b
+
+
+@pytest.mark.parametrize("N,M,m,B", [(1 << 16, 1 << 18, 4, 0), (65536, 200000, 6, 20),
+                                     (1 << 17, 300000, 8, 0)])
+def test_short_bluestein_length_fix(N, M, m, B):
+    """Plans whose Bluestein length L falls short of K + Kout - 1 (the first
+    D outputs are corrected by k_bluestein_fix, fft.cu): single column and
+    the point-major batched path, against the oracle column by column."""
+    v, x, f = nodes_and_coeffs(N + M, M, M, clustered=(m == 8), batch=B)
+    n, vs = sf.rescale_frequencies(N, v, 2.0, m)
+    plan = sf.nnfft_plan(n, vs, x, m1=m, m2=m)
+    g = plan.backend_geometry
+    assert g["L"] < g["K"] + g["Kout"] - 1, g  # the short-length path is exercised
+    out = sf.nnfft_trafo(plan, f)
+    tab = O.plan(n, vs, x, m1=m, m2=m)
+    cols = [None] if not B else [0, B - 1]
+    for b in cols:
+        fb = f if b is None else f[:, b]
+        ob = out if b is None else out[:, b]
+        assert relerr(ob, O.trafo(tab, fb), fb) <= TOL, b
+
+
+def test_short_bluestein_length_nfft():
+    """The same fix under the NFFT trafo's conjugated input (nfft.cu)."""
+    rng = np.random.default_rng(77)
+    N, M = 1 << 16, 1 << 17
+    x = rng.uniform(-0.5, 0.5, M)
+    c = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    y = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+    plan = sf.nfft_plan(N, x, m=6)
+    t = O.nfft_plan(N, x, 2.0, 6)
+    assert relerr(sf.nfft_trafo(plan, c), O.nfft_trafo(t, c), c) <= TOL
+    assert relerr(sf.nfft_adjoint(plan, y), O.nfft_adjoint(t, y), y) <= TOL
