@@ -136,6 +136,14 @@ SINCFFT_API int sincfft_nnfft_export_tables(sincfft_nnfft_plan plan, int64_t *sp
                                 int64_t *gather_idx, double *gather_val, double *hat1,
                                 double *hat2);
 
+/* Adjoint NNFFT (BASELINE north star "adjoint-NNFFT entry point"; SURVEY.md
+ * 8f row f4; not in the reference): the exact conjugate transpose of
+ * sincfft_nnfft_execute on the same plan, out_k ~ sum_j y_j e^{+2 pi i N v_k x_j}.
+ * y: (M2, batch) row-major complex, out: (M1, batch).  The adjoint's
+ * sub-plans are built on the first call (thread-safe) and kept with the plan. */
+SINCFFT_API int sincfft_nnfft_adjoint(sincfft_nnfft_plan plan, const double *y, double *out,
+                                      int64_t batch, int32_t ptr_kind, void *stream);
+
 /* --- fast sinc transform (Algorithm 6.3, all four layouts) ---------------
  * Replaces sincfft.fast_sinc.sinc_plan (fast_sinc.py:123-223).  The caller
  * supplies the Clenshaw-Curtis points z[n+1] and weights w[n+1] (host

@@ -13,15 +13,15 @@ from .direct import ndft_direct, nndft_direct, sinc_transform_direct
 from .nfft import NfftPlan, nfft_adjoint, nfft_plan, nfft_trafo
 from .errors import ParameterError, PositivityError
 from .fast_sinc import SincMode, SincPlan, fast_sinc_transform, sinc_plan
-from .nnfft import (NnfftGeometry, NnfftPlan, WindowSpec, nnfft_plan, nnfft_trafo,
-                    nnfft_trafo_into, rescale_frequencies)
+from .nnfft import (NnfftGeometry, NnfftPlan, WindowSpec, nnfft_adjoint, nnfft_plan,
+                    nnfft_trafo, nnfft_trafo_into, rescale_frequencies)
 from .quadrature import CcQuadrature, cc_quadrature, cc_weights_direct, cc_weights_fast
 
 __version__ = "0.1.0"
 
 __all__ = [
     "ParameterError", "PositivityError",
-    "WindowSpec", "NnfftGeometry", "NnfftPlan", "nnfft_plan", "nnfft_trafo", "nnfft_trafo_into",
+    "WindowSpec", "NnfftGeometry", "NnfftPlan", "nnfft_plan", "nnfft_trafo", "nnfft_trafo_into", "nnfft_adjoint",
     "rescale_frequencies",
     "CcQuadrature", "cc_quadrature", "cc_weights_direct", "cc_weights_fast",
     "SincMode", "SincPlan", "sinc_plan", "fast_sinc_transform",

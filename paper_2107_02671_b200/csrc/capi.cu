@@ -36,6 +36,8 @@ struct GraphCache {
 struct sincfft_nnfft_plan_s {
   sfb::NnfftPlanImpl impl;
   GraphCache graphs;
+  std::mutex adj_mu;                       // adjoint sub-plans, built on first use
+  std::unique_ptr<sfb::NnfftAdjoint> adj;
 };
 
 struct sincfft_sinc_plan_s {
@@ -527,6 +529,39 @@ int sincfft_nnfft_export_tables(sincfft_nnfft_plan plan, int64_t* spread_idx, do
     }
     if (hat2)
       SF_CUDA(cudaMemcpy(hat2, p.hat2.p, sizeof(double) * p.g.K, cudaMemcpyDeviceToHost));
+  });
+}
+
+// ------------------------------------------------------------- adjoint NNFFT
+int sincfft_nnfft_adjoint(sincfft_nnfft_plan plan, const double* y, double* out, int64_t batch,
+                          int32_t ptr_kind, void* stream) {
+  return guarded([&] {
+    if (!plan || !y || !out) sfb::fail(1, "NULL argument");
+    if (batch < 1) sfb::fail(1, "batch must be >= 1");
+    check_ptr_kind(ptr_kind);
+    const sfb::NnfftPlanImpl& p = plan->impl;
+    set_device(p.device);
+    cudaStream_t s = as_stream(stream);
+    {
+      std::lock_guard<std::mutex> lk(plan->adj_mu);
+      if (!plan->adj) {
+        std::unique_ptr<sfb::NnfftAdjoint> a(new sfb::NnfftAdjoint());
+        cudaStream_t bs;
+        SF_CUDA(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking));
+        try {
+          sfb::build_adjoint(p, *a, bs);
+        } catch (...) {
+          cudaStreamDestroy(bs);
+          throw;
+        }
+        SF_CUDA(cudaStreamDestroy(bs));
+        plan->adj = std::move(a);
+      }
+    }
+    InBuf yb(y, sizeof(double2) * (size_t)p.g.M2 * batch, ptr_kind, s);
+    OutBuf ob(out, sizeof(double2) * (size_t)p.g.M1 * batch, ptr_kind, s);
+    sfb::run_adjoint(p, *plan->adj, (const double2*)yb.ptr, (double2*)ob.ptr, (int)batch, s);
+    ob.finish(s);
   });
 }
 

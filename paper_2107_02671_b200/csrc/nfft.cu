@@ -171,7 +171,7 @@ void build_nfft(NfftPlanImpl& p, int64_t N, int64_t M, double sigma, int m, cons
   SF_CUDA(cudaMemcpyAsync(t.hat2.p, p.hat.p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
   t.sp.n_sms = 148;
   SF_CUDA(cudaDeviceGetAttribute(&t.sp.n_sms, cudaDevAttrMultiProcessorCount, device));
-  build_targets(t, p.x_clip.p, M, 1.0, n_over, m, TargetScale{}, s);
+  build_targets(t, p.x_clip.p, M, 1.0, (double)n_over, n_over, m, TargetScale{}, s);
   t.gp.conj_out = true;
   t.fft.conj_in = true;
   t.fft.in_scale = 1.0 / (double)n_over;

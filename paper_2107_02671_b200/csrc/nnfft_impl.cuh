@@ -136,6 +136,19 @@ struct NnfftPlanImpl {
   DevArray<double> hat2;            // phi_hat_2 at l - K/2          [K]
 };
 
+// Adjoint NNFFT sub-plans (adjoint.cu), built lazily from a forward plan
+struct NnfftAdjoint {
+  int64_t halo = 0;
+  DevArray<double> s1;      // 1/phi_hat_1(N x_j), original order
+  NnfftPlanImpl spread_x;   // spread at N2 xs onto N2 + 2 halo points (window 2)
+  NnfftPlanImpl fft;        // N2 folded inputs -> K outputs at l - K/2 (conjugated)
+  NnfftPlanImpl gather_v;   // gather over the K-grid at N1 v (window 1)
+};
+void build_adjoint(const NnfftPlanImpl& p, NnfftAdjoint& a, cudaStream_t stream);
+// y: (M2, batch) row-major -> out: (M1, batch) row-major, device pointers
+void run_adjoint(const NnfftPlanImpl& p, const NnfftAdjoint& a, const double2* y, double2* out,
+                 int batch, cudaStream_t stream);
+
 // ----- plan.cu
 Geometry make_geometry(int64_t N, int64_t M1, int64_t M2, double sigma1, double sigma2, int m1,
                        int m2);
@@ -150,8 +163,11 @@ struct TargetScale {
 };
 void build_sources(NnfftPlanImpl& p, const double* v, int64_t M1, double N1, int64_t K,
                    cudaStream_t stream);
-void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, int64_t N2,
-                   int m2, const TargetScale& ts, cudaStream_t stream);
+// positions pos_scale * (ratio * x); N2 = the periodic length the gather
+// wraps at (and the clamp of Kout)
+void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, double pos_scale,
+                   int64_t N2, int m2, const TargetScale& ts, cudaStream_t stream,
+                   int64_t force_s_lo = 0, int64_t force_kout = 0);
 // multiply the gather scale by per-target weights (device, original order)
 void fuse_target_weights(NnfftPlanImpl& p, const double* w_dev, cudaStream_t stream);
 

@@ -510,14 +510,15 @@ void build_sources(NnfftPlanImpl& p, const double* v, int64_t M1, double N1, int
 // (original-index slice, cell), the per-target scale (1/phi_hat_1(N x) for
 // the NNFFT, 1 for the NFFT), the per-CTA h spans and the output window
 // [s_lo, s_lo + Kout) the gather reads (Kout <= N2; wider windows wrap).
-void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, int64_t N2,
-                   int m2, const TargetScale& ts, cudaStream_t s) {
+void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, double pos_scale,
+                   int64_t N2, int m2, const TargetScale& ts, cudaStream_t s,
+                   int64_t force_s_lo, int64_t force_kout) {
     Scratch kin(sizeof(unsigned long long) * M2, s), kout(sizeof(unsigned long long) * M2, s);
     Scratch iin(sizeof(int) * M2, s);
     p.gp.perm.alloc(M2);
     const int cbits = key_bits((uint64_t)(2 * N2 + 2));
     const int64_t slice = gather_slice();
-    k_tgt_keys<<<blocks(M2), 256, 0, s>>>(x, M2, ratio, (double)N2, N2, cbits, slice,
+    k_tgt_keys<<<blocks(M2), 256, 0, s>>>(x, M2, ratio, pos_scale, N2, cbits, slice,
                                           kin.as<unsigned long long>(), iin.as<int>());
     SF_LAUNCH_CHECK();
     size_t tb = 0;
@@ -535,7 +536,7 @@ void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, 
     p.gp.scale.alloc(M2);
     Scratch bad(sizeof(unsigned long long), s);
     SF_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
-    k_tgt_tables<<<blocks(M2), 256, 0, s>>>(x, p.gp.perm.p, M2, ratio, (double)N2, ts.hat1 ? 1 : 0,
+    k_tgt_tables<<<blocks(M2), 256, 0, s>>>(x, p.gp.perm.p, M2, ratio, pos_scale, ts.hat1 ? 1 : 0,
                                             ts.N, ts.beta1, ts.m1, ts.N1, p.gp.pos.p,
                                             p.gp.scale.p, bad.as<unsigned long long>());
     SF_LAUNCH_CHECK();
@@ -543,10 +544,16 @@ void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, 
       fail(2, "nnfft_plan: phi_hat_1(N x_j) must be strictly positive at every node");
     double plo, phi;
     device_minmax(p.gp.pos.p, M2, s, &plo, &phi);
-    const int64_t s_lo = (int64_t)std::floor(plo) + 1 - m2;
+    int64_t s_lo = (int64_t)std::floor(plo) + 1 - m2;
     const int64_t s_hi = (int64_t)std::floor(phi) + m2;
-    p.fft.s_lo = s_lo;
     p.fft.Kout = std::min<int64_t>(s_hi - s_lo + 1, N2);
+    if (force_kout > 0) {  // the caller's h window (adjoint gather over a whole K-grid)
+      if (s_lo < force_s_lo || s_hi >= force_s_lo + force_kout)
+        fail(1, "internal: target window outside the forced h range");
+      s_lo = force_s_lo;
+      p.fft.Kout = force_kout;
+    }
+    p.fft.s_lo = s_lo;
     const int64_t nblk = ceil_div(M2, kGatherGroup);
     p.gp.span.alloc(nblk);
     k_gather_spans<<<blocks(nblk), 256, 0, s>>>(p.gp.pos.p, M2, nblk, m2, s_lo, p.gp.span.p);
@@ -601,7 +608,7 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
   ts.beta1 = g.beta1;
   ts.m1 = g.m1;
   ts.N1 = g.N1;
-  build_targets(p, p.x_clip.p, g.M2, (double)g.N / (double)g.N1, g.N2, g.m2, ts, s);
+  build_targets(p, p.x_clip.p, g.M2, (double)g.N / (double)g.N1, (double)g.N2, g.N2, g.m2, ts, s);
 
   p.fft.in_scale = 1.0 / ((double)g.N1 * (double)g.N2);
   build_fft(p, s);

@@ -316,6 +316,43 @@ def _trafo_torch(plan, f):
     return out
 
 
+def nnfft_adjoint(plan, y):
+    """Adjoint NNFFT: ``sum_j y_j e^{+2 pi i N v_k x_j}`` at every frequency
+    node, the exact conjugate transpose of :func:`nnfft_trafo` on the same
+    plan (BASELINE north star's adjoint-NNFFT entry point; not in the
+    reference).  ``y``: shape (M2,) or (M2, B), numpy or
+    CUDA tensor; returns shape (M1,) or (M1, B)."""
+    geo = plan.geometry
+    if _is_torch(y):
+        import torch
+        if y.device.type != "cuda" or y.device.index != plan.device:
+            raise ParameterError("nnfft_adjoint: tensor must live on the plan's CUDA device")
+        y = y.to(torch.complex128).contiguous()
+        if tuple(y.shape) == (geo.M2,):
+            batch, oshape = 1, (geo.M1,)
+        elif y.ndim == 2 and y.shape[0] == geo.M2:
+            batch, oshape = y.shape[1], (geo.M1, y.shape[1])
+        else:
+            raise ParameterError(f"nnfft_adjoint: expected {geo.M2} values, got {tuple(y.shape)}")
+        out = torch.empty(oshape, dtype=torch.complex128, device=y.device)
+        _lib.check(_lib.lib.sincfft_nnfft_adjoint(plan.handle, C.c_void_p(y.data_ptr()),
+                                                  C.c_void_p(out.data_ptr()), batch,
+                                                  _lib.PTR_DEVICE, _stream_handle(y)))
+        return out
+    y = np.ascontiguousarray(y, dtype=complex)
+    if y.shape == (geo.M2,):
+        batch = 1
+        out = np.empty(geo.M1, dtype=complex)
+    elif y.ndim == 2 and y.shape[0] == geo.M2 and y.shape[1] >= 1:
+        batch = y.shape[1]
+        out = np.empty((geo.M1, batch), dtype=complex)
+    else:
+        raise ParameterError(f"nnfft_adjoint: expected {geo.M2} values, got {y.shape}")
+    _lib.check(_lib.lib.sincfft_nnfft_adjoint(plan.handle, _vp(y), _vp(out), batch,
+                                              _lib.PTR_HOST, None))
+    return out
+
+
 def nnfft_trafo_into(plan, f, out, stream=None, blocking=True):
     """Extension for pipelined host-side use: write the transform of ``f`` into
     ``out`` (CPU torch tensors, ideally page-locked, or numpy arrays).  With

@@ -126,3 +126,14 @@ def test_sinc_modes(golden):
         assert rel(out, s("out"), s("c")) <= 1e-15, k
         err = np.max(np.abs(out - s("direct"))) / np.sum(np.abs(s("c")))
         assert err <= float(s("bound_full")), k
+
+
+def test_oracle_adjoint_is_the_conjugate_transpose(golden):
+    """The oracle's adjoint NNFFT (no reference counterpart) is pinned through
+    the pinned trafo: <A f, y> = <f, A^H y> to rounding on config 1's plan."""
+    g = golden("nnfft_config1.npz")
+    t = O.plan(int(g["n_star"]), g["v_star"], g["x"], m1=int(g["m"]), m2=int(g["m"]))
+    y = np.random.default_rng(3).standard_normal(g["x"].size) * (1 + 2j)
+    lhs = np.vdot(y, O.trafo(t, g["f"]))
+    rhs = np.vdot(O.adjoint(t, y), g["f"])
+    assert abs(lhs - rhs) <= 1e-14 * np.linalg.norm(g["f"]) * np.linalg.norm(y) * 64
