@@ -425,6 +425,9 @@ def run_b200(args, cfg):
     # growth costs a few ms of host time per allocation)
     for k in range(max(3 * nbuf, args.warmup)):
         e2e_step(k)
+    # drain the warm-up backlog (the host enqueues far ahead of the copies)
+    # so the timed region holds exactly the timed steps
+    torch.cuda.synchronize()
     barrier()
     ev0.record(stream)
     for st in streams:

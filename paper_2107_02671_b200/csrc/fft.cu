@@ -177,7 +177,10 @@ struct FftArgs {
 // Global <-> shared copies are issued kU elements per thread at a time so
 // that kU independent loads are in flight before the first dependent store
 // (a plain strided loop serialises one DRAM latency per element).
-constexpr int kU = 8;
+#ifndef SFB_FFT_KU
+#define SFB_FFT_KU 8
+#endif
+constexpr int kU = SFB_FFT_KU;
 
 template <int MODE>
 __global__ void __launch_bounds__(512) k_single(FftArgs a, int spectrum) {

@@ -21,7 +21,7 @@ hf = [torch.from_numpy(f).pin_memory() for _ in range(nb)]
 ho = [torch.empty(M, dtype=torch.complex128).pin_memory() for _ in range(nb)]
 st = [torch.cuda.Stream() for _ in range(nb)]
 L = _lib.lib
-for rep in range(3):
+for rep in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     lat = []
