@@ -128,7 +128,7 @@ __device__ __forceinline__ double2 gather_one(const GatherArgs& a, const double2
 }
 
 #ifndef SFB_GATHER2_MINB
-#define SFB_GATHER2_MINB 4  // 64 registers: 4 CTAs/SM (0.381 -> 0.313 ms at config 3)
+#define SFB_GATHER2_MINB (8 * 128 / SFB_GATHER_THREADS)  // 64 registers (0.381 -> 0.299 ms at config 3)
 #endif
 template <int M>
 __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(GatherArgs a,

@@ -70,13 +70,19 @@ constexpr int kBatchedMin = 16;  // columns from which the column-vectorised pat
 constexpr int64_t kGatherSliceDefault = (int64_t)1 << 20;
 int64_t gather_slice();  // kGatherSliceDefault unless SFB_GATHER_SLICE_LOG2 is set (tuning)
 
-constexpr int kGatherThreads = 256;  // threads per gather CTA
+#ifndef SFB_GATHER_THREADS
+#define SFB_GATHER_THREADS 128  // 128 x 8 CTAs/SM measured 3 % faster than 256 x 4
+#endif
+#ifndef SFB_GATHER_SPAN
+#define SFB_GATHER_SPAN 1024
+#endif
+constexpr int kGatherThreads = SFB_GATHER_THREADS;  // threads per gather CTA
 #ifndef SFB_GATHER_TPT
 #define SFB_GATHER_TPT 2
 #endif
 constexpr int kGatherTPT = SFB_GATHER_TPT;                 // targets per thread
 constexpr int kGatherGroup = kGatherThreads * kGatherTPT;  // targets per CTA
-constexpr int kGatherSpan = 2048;    // h values staged per CTA (32 KiB)
+constexpr int kGatherSpan = SFB_GATHER_SPAN;  // h values staged per CTA (16 KiB)
 
 struct GatherPlan {
   bool conj_out = false;  // store conj(out) (pairs with FftPlan::conj_in)
