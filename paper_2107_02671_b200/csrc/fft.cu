@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(512) k_single(FftArgs a, int spectrum) {
   }
 }
 
-template <int MODE>
+template <int MODE, int NCT = 0, int NBL = 0>
 __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd(FftArgs a) {
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
@@ -278,7 +278,8 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd(FftArgs a) {
       if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = v[u];
   }
   __syncthreads();
-  fft_dif(sm, a.C_log2, a.st2, a.tw2);
+  if constexpr (NCT > 0) fft_dif_ct<NCT, NBL, 256>(sm, a.st2, a.tw2);
+  else fft_dif(sm, a.C_log2, a.st2, a.tw2);
   double2* Y = a.Y + (int64_t)col * a.L;
   for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
     double2 w[kU];
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd(FftArgs a) {
   }
 }
 
+template <int NCT = 0>
 __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_rowmul(FftArgs a, int spectrum) {
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
@@ -315,7 +317,8 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_rowmul(FftArgs a, int spe
       if (i0 + u * T < L1) sm[spad(i0 + u * T)] = v[u];
   }
   __syncthreads();
-  fft_dif(sm, 0, a.st1, a.tw1);
+  if constexpr (NCT > 0) fft_dif_ct<NCT, 0, 256>(sm, a.st1, a.tw1);
+  else fft_dif(sm, 0, a.st1, a.tw1);
   const double2* B = a.Bhat + p * a.L1;
   if (spectrum) {
     const double inv = 1.0 / (double)a.L;
@@ -334,10 +337,12 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_rowmul(FftArgs a, int spe
     }
   }
   __syncthreads();
-  fft_dit(sm, 0, a.st1, a.tw1);
+  if constexpr (NCT > 0) fft_dit_ct<NCT, 0, 256>(sm, a.st1, a.tw1);
+  else fft_dit(sm, 0, a.st1, a.tw1);
   for (int i = threadIdx.x; i < L1; i += T) row[i] = cconj(sm[spad(i)]);
 }
 
+template <int NCT = 0, int NBL = 0>
 __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv(FftArgs a) {
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
@@ -366,7 +371,8 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv(FftArgs a) {
       if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = cmul(cconj(v[u]), w[u]);
   }
   __syncthreads();
-  fft_dit(sm, a.C_log2, a.st2, a.tw2);
+  if constexpr (NCT > 0) fft_dit_ct<NCT, NBL, 256>(sm, a.st2, a.tw2);
+  else fft_dit(sm, a.C_log2, a.st2, a.tw2);
   double2* h = a.h + (int64_t)col * a.Kout;
   for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
     double2 qv[kU];
@@ -958,8 +964,11 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_single<IN_PLAIN>, smem_bytes(kSingleMax));
   set_smem(k_colfwd<IN_GP>, smem_bytes(kColElems));
   set_smem(k_colfwd<IN_PLAIN>, smem_bytes(kColElems));
-  set_smem(k_rowmul, smem_bytes(kRowMax));
-  set_smem(k_colinv, smem_bytes(kColElems));
+  set_smem(k_rowmul<0>, smem_bytes(kRowMax));
+  set_smem(k_colinv<0, 0>, smem_bytes(kColElems));
+  set_smem(k_colfwd<IN_GP, 1024, 2>, smem_bytes(kColElems));
+  set_smem(k_colinv<1024, 2>, smem_bytes(kColElems));
+  set_smem(k_rowmul<4096>, smem_bytes(kRowMax));
   set_smem(k_colfwd_b, smem_bytes(kColElems));
   set_smem(k_rowmul_b, smem_bytes(kColElems));
   set_smem(k_colinv_b, smem_bytes(kColElems));
@@ -1074,7 +1083,7 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
     a.Y = f.Bhat.p;
     k_colfwd<IN_PLAIN><<<dim3((unsigned)ceil_div(f.L1, f.C), 1), 256, smc, s>>>(a);
     SF_LAUNCH_CHECK();
-    k_rowmul<<<dim3((unsigned)f.L2, 1), 256, smr, s>>>(a, 1);
+    k_rowmul<0><<<dim3((unsigned)f.L2, 1), 256, smr, s>>>(a, 1);
     SF_LAUNCH_CHECK();
   }
   SF_CUDA(cudaStreamSynchronize(s));  // b is released at scope exit
@@ -1147,11 +1156,17 @@ void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* w
   }
   const size_t smc = smem_bytes(f.L2 * f.C), smr = smem_bytes(f.L1);
   const dim3 gc((unsigned)ceil_div(f.L1, f.C), batch);
-  k_colfwd<IN_GP><<<gc, 256, smc, s>>>(a);
+  // compile-time specialisations of the shapes in use (config 3: 4096 x 1024)
+  const bool ct_col = f.L2 == 1024 && f.C_log2 == 2 && f.st2.n == 1024;
+  const bool ct_row = f.L1 == 4096 && f.st1.n == 4096;
+  if (ct_col) k_colfwd<IN_GP, 1024, 2><<<gc, 256, smc, s>>>(a);
+  else k_colfwd<IN_GP><<<gc, 256, smc, s>>>(a);
   SF_LAUNCH_CHECK();
-  k_rowmul<<<dim3((unsigned)f.L2, batch), 256, smr, s>>>(a, 0);
+  if (ct_row) k_rowmul<4096><<<dim3((unsigned)f.L2, batch), 256, smr, s>>>(a, 0);
+  else k_rowmul<0><<<dim3((unsigned)f.L2, batch), 256, smr, s>>>(a, 0);
   SF_LAUNCH_CHECK();
-  k_colinv<<<gc, 256, smc, s>>>(a);
+  if (ct_col) k_colinv<1024, 2><<<gc, 256, smc, s>>>(a);
+  else k_colinv<0, 0><<<gc, 256, smc, s>>>(a);
   SF_LAUNCH_CHECK();
   launch_fix(p, grid, h, batch, 0, s);
 }

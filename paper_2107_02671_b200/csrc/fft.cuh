@@ -303,4 +303,104 @@ __device__ __forceinline__ void fft_dit(double2* s, int nb_log2, const FftStages
   }
 }
 
+// ------------------------------------------- compile-time specialisations
+// The same stages with n, the batch width NB = 2^NBL and the thread count
+// known at compile time (power-of-two n, radix 8 then 4 or 2, exactly the
+// decomposition make_stages() produces): every index, the butterfly loop and
+// -- for strides that are multiples of 512 slots, where the XOR swizzle
+// reduces to an offset -- the swizzled addresses fold into constants.
+__host__ __device__ constexpr int ct_nst(int n) {
+  int k = 0;
+  while (n % 8 == 0) n /= 8, ++k;
+  if (n % 4 == 0) n /= 4, ++k;
+  if (n % 2 == 0) n /= 2, ++k;
+  return n == 1 ? k : -1;
+}
+__host__ __device__ constexpr int ct_rad(int n, int q) {
+  int k = 0;
+  while (n % 8 == 0) {
+    if (k == q) return 8;
+    n /= 8, ++k;
+  }
+  if (n % 4 == 0) {
+    if (k == q) return 4;
+    n /= 4, ++k;
+  }
+  if (n % 2 == 0 && k == q) return 2;
+  return 0;
+}
+__host__ __device__ constexpr int ct_prod(int n, int a, int b) {  // rad[a..b)
+  int p = 1;
+  for (int q = a; q < b; ++q) p *= ct_rad(n, q);
+  return p;
+}
+
+template <int R, bool DIT, int S, int G, int NBL, int NTHR>
+__device__ __forceinline__ void fft_stage_ct(double2* s, const double2* __restrict__ tw,
+                                             int tid) {
+  constexpr int NB = 1 << NBL;
+  constexpr int NQ = G * S;        // butterflies per vector
+  constexpr int DQ = NTHR >> NBL;  // butterflies a thread advances by
+  constexpr int STRIDE = S << NBL; // slot distance between legs
+  const int b = tid & (NB - 1);
+  const int q0 = tid >> NBL;
+#pragma unroll
+  for (int it = 0; it < (NQ + DQ - 1) / DQ; ++it) {
+    const int q = q0 + it * DQ;
+    if ((NQ % DQ) != 0 && q >= NQ) break;
+    const int g = q / S, j = q % S;
+    const int e0 = (((g * R * S) + j) << NBL) + b;
+    double2 x[R];
+    if constexpr (STRIDE % 512 == 0) {
+      const int p0 = spad(e0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r] = s[p0 + r * STRIDE];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r] = s[spad(e0 + r * STRIDE)];
+    }
+    const bool twid = j != 0;
+    double2 w1 = make_double2(1.0, 0.0);
+    if (twid) w1 = __ldg(tw + j);
+    if (DIT && twid) apply_twiddles<R>(x, w1);
+    Dft<R>::run(x);
+    if (!DIT && twid) apply_twiddles<R>(x, w1);
+    if constexpr (STRIDE % 512 == 0) {
+      const int p0 = spad(e0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[p0 + r * STRIDE] = x[r];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[spad(e0 + r * STRIDE)] = x[r];
+    }
+  }
+}
+
+template <int N, int NBL, int NTHR, bool DIT, int Q>
+__device__ __forceinline__ void fft_ct_from(double2* s, const FftStages& st,
+                                            const double2* __restrict__ tw) {
+  constexpr int NST = ct_nst(N);
+  static_assert(NST > 0, "compile-time FFT needs a power-of-two length");
+  if constexpr (Q >= 0 && Q < NST) {
+    constexpr int R = ct_rad(N, Q);
+    constexpr int S = ct_prod(N, Q + 1, NST);
+    constexpr int G = ct_prod(N, 0, Q);
+    fft_stage_ct<R, DIT, S, G, NBL, NTHR>(s, tw + st.toff[Q], threadIdx.x);
+    __syncthreads();
+    fft_ct_from<N, NBL, NTHR, DIT, DIT ? Q - 1 : Q + 1>(s, st, tw);
+  }
+}
+
+template <int N, int NBL, int NTHR>
+__device__ __forceinline__ void fft_dif_ct(double2* s, const FftStages& st,
+                                           const double2* __restrict__ tw) {
+  fft_ct_from<N, NBL, NTHR, false, 0>(s, st, tw);
+}
+
+template <int N, int NBL, int NTHR>
+__device__ __forceinline__ void fft_dit_ct(double2* s, const FftStages& st,
+                                           const double2* __restrict__ tw) {
+  fft_ct_from<N, NBL, NTHR, true, ct_nst(N) - 1>(s, st, tw);
+}
+
 }  // namespace sfb
