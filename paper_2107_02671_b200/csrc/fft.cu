@@ -37,9 +37,10 @@ namespace sfb {
 constexpr int kSingleMax = 8192;      // largest L done by one CTA
 constexpr int kRowMax = 8192;         // largest row length L1
 #ifndef SFB_FFT_COLELEMS
-#define SFB_FFT_COLELEMS 4096
+#define SFB_FFT_COLELEMS 2048
 #endif
-constexpr int kColElems = SFB_FFT_COLELEMS;  // C * L2 per column-kernel CTA
+constexpr int kColElems = SFB_FFT_COLELEMS;  // C * L2 per single-column column-kernel CTA
+constexpr int kColElemsB = 4096;             // per point-major (batched) CTA
 constexpr int kTwSplit = 4096;        // two-level W_L table split
 constexpr int64_t kFixMax = 2048;     // largest shortfall D of a short Bluestein length
 
@@ -181,6 +182,12 @@ struct FftArgs {
 #define SFB_FFT_KU 8
 #endif
 constexpr int kU = SFB_FFT_KU;
+// the single-column column kernels (k_colfwd / k_colinv) run 4 CTAs per SM
+// with C = 2 columns; fewer loads in flight keep them under 64 registers
+#ifndef SFB_FFT_KU_COL
+#define SFB_FFT_KU_COL 4
+#endif
+constexpr int kUc = SFB_FFT_KU_COL;
 
 template <int MODE>
 __global__ void __launch_bounds__(512) k_single(FftArgs a, int spectrum) {
@@ -243,8 +250,11 @@ __global__ void __launch_bounds__(512) k_single(FftArgs a, int spectrum) {
   }
 }
 
+#ifndef SFB_FFT_COL_MINB
+#define SFB_FFT_COL_MINB 4  // 32 KiB + <= 64 registers: 4 CTAs per SM
+#endif
 template <int MODE, int NCT = 0, int NBL = 0>
-__global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd(FftArgs a) {
+__global__ void __launch_bounds__(256, SFB_FFT_COL_MINB) k_colfwd(FftArgs a) {
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int C = 1 << a.C_log2;
@@ -253,10 +263,10 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd(FftArgs a) {
   const int n_el = L2 << a.C_log2;
   const int T = blockDim.x;
   const double2* g = a.g + (int64_t)col * (MODE == IN_GP ? a.K : 0);
-  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
-    double2 v[kU];
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kUc * T) {
+    double2 v[kUc];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kUc; ++u) {
       const int e = e0 + u * T;
       const int64_t n1 = c0 + (e & (C - 1));
       const int64_t n = n1 + a.L1 * (e >> a.C_log2);
@@ -274,24 +284,24 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd(FftArgs a) {
       }
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u)
+    for (int u = 0; u < kUc; ++u)
       if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = v[u];
   }
   __syncthreads();
   if constexpr (NCT > 0) fft_dif_ct<NCT, NBL, 256>(sm, a.st2, a.tw2);
   else fft_dif(sm, a.C_log2, a.st2, a.tw2);
   double2* Y = a.Y + (int64_t)col * a.L;
-  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
-    double2 w[kU];
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kUc * T) {
+    double2 w[kUc];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kUc; ++u) {
       const int e = e0 + u * T;
       const int64_t n1 = c0 + (e & (C - 1));
       w[u] = make_double2(1.0, 0.0);
       if (e < n_el && n1 < a.L1) w[u] = wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)__ldg(a.rev2 + (e >> a.C_log2)));
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kUc; ++u) {
       const int e = e0 + u * T;
       const int64_t n1 = c0 + (e & (C - 1));
       if (e < n_el && n1 < a.L1) Y[n1 + a.L1 * (e >> a.C_log2)] = cmul(sm[spad(e)], w[u]);
@@ -343,7 +353,7 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_rowmul(FftArgs a, int spe
 }
 
 template <int NCT = 0, int NBL = 0>
-__global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv(FftArgs a) {
+__global__ void __launch_bounds__(256, SFB_FFT_COL_MINB) k_colinv(FftArgs a) {
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int C = 1 << a.C_log2;
@@ -352,10 +362,10 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv(FftArgs a) {
   const int n_el = L2 << a.C_log2;
   const int T = blockDim.x;
   const double2* Y = a.Y + (int64_t)col * a.L;
-  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
-    double2 v[kU], w[kU];
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kUc * T) {
+    double2 v[kUc], w[kUc];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kUc; ++u) {
       const int e = e0 + u * T;
       const int64_t n1 = c0 + (e & (C - 1));
       const int p = e >> a.C_log2;
@@ -367,24 +377,24 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv(FftArgs a) {
       }
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u)
+    for (int u = 0; u < kUc; ++u)
       if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = cmul(cconj(v[u]), w[u]);
   }
   __syncthreads();
   if constexpr (NCT > 0) fft_dit_ct<NCT, NBL, 256>(sm, a.st2, a.tw2);
   else fft_dit(sm, a.C_log2, a.st2, a.tw2);
   double2* h = a.h + (int64_t)col * a.Kout;
-  for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
-    double2 qv[kU];
+  for (int e0 = threadIdx.x; e0 < n_el; e0 += kUc * T) {
+    double2 qv[kUc];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kUc; ++u) {
       const int e = e0 + u * T;
       const int64_t k = c0 + (e & (C - 1)) + a.L1 * (e >> a.C_log2);
       qv[u] = make_double2(0.0, 0.0);
       if (e < n_el && c0 + (e & (C - 1)) < a.L1 && k < a.Kout) qv[u] = __ldg(a.Q + k);
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kUc; ++u) {
       const int e = e0 + u * T;
       const int64_t n1 = c0 + (e & (C - 1));
       const int64_t k = n1 + a.L1 * (e >> a.C_log2);
@@ -968,10 +978,12 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_colinv<0, 0>, smem_bytes(kColElems));
   set_smem(k_colfwd<IN_GP, 1024, 2>, smem_bytes(kColElems));
   set_smem(k_colinv<1024, 2>, smem_bytes(kColElems));
+  set_smem(k_colfwd<IN_GP, 1024, 1>, smem_bytes(kColElems));
+  set_smem(k_colinv<1024, 1>, smem_bytes(kColElems));
   set_smem(k_rowmul<4096>, smem_bytes(kRowMax));
-  set_smem(k_colfwd_b, smem_bytes(kColElems));
-  set_smem(k_rowmul_b, smem_bytes(kColElems));
-  set_smem(k_colinv_b, smem_bytes(kColElems));
+  set_smem(k_colfwd_b, smem_bytes(kColElemsB));
+  set_smem(k_rowmul_b, smem_bytes(kColElemsB));
+  set_smem(k_colinv_b, smem_bytes(kColElemsB));
   FftPlan& f = p.fft;
   const Geometry& g = p.g;
   const int64_t Lmin = g.K + f.Kout - 1;
@@ -1113,8 +1125,8 @@ void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h
   x.a.Y = work;
   x.B = batch;
   int cc = 8, cr = 8;
-  while (cc > 1 && cc * f.L2 > kColElems) cc >>= 1;
-  while (cr > 1 && cr * f.L1 > kColElems) cr >>= 1;
+  while (cc > 1 && cc * f.L2 > kColElemsB) cc >>= 1;
+  while (cr > 1 && cr * f.L1 > kColElemsB) cr >>= 1;
   x.cb_log2_col = log2i(cc);
   x.cb_log2_row = log2i(cr);
   const size_t smc = smem_bytes(f.L2 * cc), smr = smem_bytes(f.L1 * cr);
@@ -1158,14 +1170,17 @@ void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* w
   const dim3 gc((unsigned)ceil_div(f.L1, f.C), batch);
   // compile-time specialisations of the shapes in use (config 3: 4096 x 1024)
   const bool ct_col = f.L2 == 1024 && f.C_log2 == 2 && f.st2.n == 1024;
+  const bool ct_col1 = f.L2 == 1024 && f.C_log2 == 1 && f.st2.n == 1024;
   const bool ct_row = f.L1 == 4096 && f.st1.n == 4096;
   if (ct_col) k_colfwd<IN_GP, 1024, 2><<<gc, 256, smc, s>>>(a);
+  else if (ct_col1) k_colfwd<IN_GP, 1024, 1><<<gc, 256, smc, s>>>(a);
   else k_colfwd<IN_GP><<<gc, 256, smc, s>>>(a);
   SF_LAUNCH_CHECK();
   if (ct_row) k_rowmul<4096><<<dim3((unsigned)f.L2, batch), 256, smr, s>>>(a, 0);
   else k_rowmul<0><<<dim3((unsigned)f.L2, batch), 256, smr, s>>>(a, 0);
   SF_LAUNCH_CHECK();
   if (ct_col) k_colinv<1024, 2><<<gc, 256, smc, s>>>(a);
+  else if (ct_col1) k_colinv<1024, 1><<<gc, 256, smc, s>>>(a);
   else k_colinv<0, 0><<<gc, 256, smc, s>>>(a);
   SF_LAUNCH_CHECK();
   launch_fix(p, grid, h, batch, 0, s);
