@@ -415,6 +415,7 @@ struct FftBArgs {
   int cb_log2_col, cb_log2_row;
 };
 
+template <int NCT = 0, int NBL = 0>
 __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd_b(FftBArgs x) {
   extern __shared__ double2 sm[];
   const FftArgs& a = x.a;
@@ -439,7 +440,8 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd_b(FftBArgs x) {
       if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = v[u];
   }
   __syncthreads();
-  fft_dif(sm, x.cb_log2_col, a.st2, a.tw2);
+  if constexpr (NCT > 0) fft_dif_ct<NCT, NBL, 256>(sm, a.st2, a.tw2);
+  else fft_dif(sm, x.cb_log2_col, a.st2, a.tw2);
   for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
     double2 w[kU];
 #pragma unroll
@@ -458,6 +460,7 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd_b(FftBArgs x) {
   }
 }
 
+template <int NCT = 0, int NBL = 0>
 __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_rowmul_b(FftBArgs x) {
   extern __shared__ double2 sm[];
   const FftArgs& a = x.a;
@@ -482,18 +485,21 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_rowmul_b(FftBArgs x) {
       if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = v[u];
   }
   __syncthreads();
-  fft_dif(sm, x.cb_log2_row, a.st1, a.tw1);
+  if constexpr (NCT > 0) fft_dif_ct<NCT, NBL, 256>(sm, a.st1, a.tw1);
+  else fft_dif(sm, x.cb_log2_row, a.st1, a.tw1);
   const double2* Bh = a.Bhat + p * a.L1;
   for (int e = threadIdx.x; e < n_el; e += T)
     sm[spad(e)] = cconj(cmul(sm[spad(e)], __ldg(Bh + (e >> x.cb_log2_row))));
   __syncthreads();
-  fft_dit(sm, x.cb_log2_row, a.st1, a.tw1);
+  if constexpr (NCT > 0) fft_dit_ct<NCT, NBL, 256>(sm, a.st1, a.tw1);
+  else fft_dit(sm, x.cb_log2_row, a.st1, a.tw1);
   for (int e = threadIdx.x; e < n_el; e += T) {
     const int b = b0 + (e & (CB - 1));
     if (b < x.B) Y[(int64_t)(e >> x.cb_log2_row) * x.B + b] = cconj(sm[spad(e)]);
   }
 }
 
+template <int NCT = 0, int NBL = 0>
 __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv_b(FftBArgs x) {
   extern __shared__ double2 sm[];
   const FftArgs& a = x.a;
@@ -522,7 +528,8 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv_b(FftBArgs x) {
       if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = cmul(cconj(v[u]), w[u]);
   }
   __syncthreads();
-  fft_dit(sm, x.cb_log2_col, a.st2, a.tw2);
+  if constexpr (NCT > 0) fft_dit_ct<NCT, NBL, 256>(sm, a.st2, a.tw2);
+  else fft_dit(sm, x.cb_log2_col, a.st2, a.tw2);
   for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
     double2 qv[kU];
 #pragma unroll
@@ -981,9 +988,12 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_colfwd<IN_GP, 1024, 1>, smem_bytes(kColElems));
   set_smem(k_colinv<1024, 1>, smem_bytes(kColElems));
   set_smem(k_rowmul<4096>, smem_bytes(kRowMax));
-  set_smem(k_colfwd_b, smem_bytes(kColElemsB));
-  set_smem(k_rowmul_b, smem_bytes(kColElemsB));
-  set_smem(k_colinv_b, smem_bytes(kColElemsB));
+  set_smem(k_colfwd_b<0, 0>, smem_bytes(kColElemsB));
+  set_smem(k_rowmul_b<0, 0>, smem_bytes(kColElemsB));
+  set_smem(k_colinv_b<0, 0>, smem_bytes(kColElemsB));
+  set_smem(k_colfwd_b<512, 3>, smem_bytes(kColElemsB));
+  set_smem(k_rowmul_b<512, 3>, smem_bytes(kColElemsB));
+  set_smem(k_colinv_b<512, 3>, smem_bytes(kColElemsB));
   FftPlan& f = p.fft;
   const Geometry& g = p.g;
   const int64_t Lmin = g.K + f.Kout - 1;
@@ -1131,11 +1141,17 @@ void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h
   x.cb_log2_row = log2i(cr);
   const size_t smc = smem_bytes(f.L2 * cc), smr = smem_bytes(f.L1 * cr);
   const dim3 gc((unsigned)f.L1, (unsigned)ceil_div(batch, cc));
-  k_colfwd_b<<<gc, 256, smc, s>>>(x);
+  // compile-time specialisation of the config-4 shape (512 x 512, 8 columns)
+  const bool ctc = f.L2 == 512 && x.cb_log2_col == 3 && f.st2.n == 512;
+  const bool ctr = f.L1 == 512 && x.cb_log2_row == 3 && f.st1.n == 512;
+  if (ctc) k_colfwd_b<512, 3><<<gc, 256, smc, s>>>(x);
+  else k_colfwd_b<0, 0><<<gc, 256, smc, s>>>(x);
   SF_LAUNCH_CHECK();
-  k_rowmul_b<<<dim3((unsigned)f.L2, (unsigned)ceil_div(batch, cr)), 256, smr, s>>>(x);
+  if (ctr) k_rowmul_b<512, 3><<<dim3((unsigned)f.L2, (unsigned)ceil_div(batch, cr)), 256, smr, s>>>(x);
+  else k_rowmul_b<0, 0><<<dim3((unsigned)f.L2, (unsigned)ceil_div(batch, cr)), 256, smr, s>>>(x);
   SF_LAUNCH_CHECK();
-  k_colinv_b<<<gc, 256, smc, s>>>(x);
+  if (ctc) k_colinv_b<512, 3><<<gc, 256, smc, s>>>(x);
+  else k_colinv_b<0, 0><<<gc, 256, smc, s>>>(x);
   SF_LAUNCH_CHECK();
   launch_fix(p, grid, h, batch, 1, s);
 }
