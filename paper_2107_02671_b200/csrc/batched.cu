@@ -56,8 +56,11 @@ __device__ __forceinline__ void spread_flush(const SpreadBArgs& a, double2* r, i
   ++ccur;
 }
 
+#ifndef SFB_SPREADB_MINB
+#define SFB_SPREADB_MINB 3  // 154 registers, no spills: 1.70 -> 1.58 ms at config 4
+#endif
 template <int M>
-__global__ void __launch_bounds__(kThreadsB, 4) k_spread_b(SpreadBArgs a, WinCoef C) {
+__global__ void __launch_bounds__(kThreadsB, SFB_SPREADB_MINB) k_spread_b(SpreadBArgs a, WinCoef C) {
   extern __shared__ double wsm[];
   constexpr int WS = 2 * M + 1;  // padded row
   const int lane = threadIdx.x & 31;
