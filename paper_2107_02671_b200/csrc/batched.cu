@@ -315,7 +315,7 @@ void run_execute_batched(const NnfftPlanImpl& p, const double2* f, double2* out,
   Scratch gp(sizeof(double2) * (size_t)K * B, s);   // [K][B]
   const bool pm = fft_supports_point_major(p);
   Scratch gc(pm ? 0 : sizeof(double2) * (size_t)K * B, s);   // [B][K]
-  Scratch work(sizeof(double2) * (size_t)p.fft.work_elems() * B, s);
+  Scratch work(sizeof(double2) * (size_t)p.fft.work_elems() * (pm ? fft_point_major_group(B) : B), s);
   Scratch hc(pm ? 0 : sizeof(double2) * (size_t)Ko * B, s);  // [B][Kout]
   Scratch hp(sizeof(double2) * (size_t)Ko * B, s);  // [Kout][B]
   if (ev) SF_CUDA(cudaEventRecord(ev[0], s));

@@ -487,8 +487,11 @@ int sincfft_nnfft_launches_per_execute(sincfft_nnfft_plan plan, int64_t batch) {
   const int fft = plan->impl.fft.single ? 1 : plan->impl.fft.direct ? 2
                                             : 3 + (plan->impl.fft.fixD > 0 ? 1 : 0);
   // column-vectorised batch: halo zeroing + spread + [2 transposes] + FFT + gather
-  if (batch >= sfb::kBatchedMin)
-    return 1 + 1 + (sfb::fft_supports_point_major(plan->impl) ? 0 : 2) + fft + 1;
+  if (batch >= sfb::kBatchedMin) {
+    if (!sfb::fft_supports_point_major(plan->impl)) return 1 + 1 + 2 + fft + 1;
+    const int64_t G = sfb::fft_point_major_group((int)batch);
+    return 1 + 1 + 3 * ((batch + G - 1) / G) + (plan->impl.fft.fixD > 0 ? 1 : 0) + 1;
+  }
   // grid memset (a launch on the stream) + spread + FFT + gather
   return 1 + 1 + fft + 1;
 }

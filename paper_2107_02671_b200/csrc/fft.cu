@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "nnfft_impl.cuh"
+#include "fft_reg.cuh"
 
 namespace sfb {
 
@@ -411,7 +412,9 @@ __global__ void __launch_bounds__(256, SFB_FFT_COL_MINB) k_colinv(FftArgs a) {
 // contiguous bytes and no transposes are needed around the FFT.
 struct FftBArgs {
   FftArgs a;
-  int B;
+  int B;      // columns in this launch (a column group)
+  int ldg;    // row stride of grid / h (the full batch)
+  int ldy;    // row stride of the work array Y (the group)
   int cb_log2_col, cb_log2_row;
 };
 
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd_b(FftBArgs x) {
       const int b = b0 + (e & (CB - 1));
       const int64_t n = n1 + a.L1 * (int64_t)(e >> x.cb_log2_col);
       v[u] = make_double2(0.0, 0.0);
-      if (e < n_el && b < x.B && n < a.K) v[u] = cmul(__ldg(a.g + n * x.B + b), __ldg(a.P + n));
+      if (e < n_el && b < x.B && n < a.K) v[u] = cmul(__ldg(a.g + n * x.ldg + b), __ldg(a.P + n));
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colfwd_b(FftBArgs x) {
       const int e = e0 + u * T;
       const int b = b0 + (e & (CB - 1));
       if (e < n_el && b < x.B)
-        a.Y[(n1 + a.L1 * (int64_t)(e >> x.cb_log2_col)) * x.B + b] = cmul(sm[spad(e)], w[u]);
+        a.Y[(n1 + a.L1 * (int64_t)(e >> x.cb_log2_col)) * x.ldy + b] = cmul(sm[spad(e)], w[u]);
     }
   }
 }
@@ -470,7 +473,7 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_rowmul_b(FftBArgs x) {
   const int L1 = (int)a.L1;
   const int n_el = L1 << x.cb_log2_row;
   const int T = blockDim.x;
-  double2* Y = a.Y + p * a.L1 * x.B;
+  double2* Y = a.Y + p * a.L1 * x.ldy;
   for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
     double2 v[kU];
 #pragma unroll
@@ -478,7 +481,7 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_rowmul_b(FftBArgs x) {
       const int e = e0 + u * T;
       const int b = b0 + (e & (CB - 1));
       v[u] = make_double2(0.0, 0.0);
-      if (e < n_el && b < x.B) v[u] = Y[(int64_t)(e >> x.cb_log2_row) * x.B + b];
+      if (e < n_el && b < x.B) v[u] = Y[(int64_t)(e >> x.cb_log2_row) * x.ldy + b];
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -495,7 +498,7 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_rowmul_b(FftBArgs x) {
   else fft_dit(sm, x.cb_log2_row, a.st1, a.tw1);
   for (int e = threadIdx.x; e < n_el; e += T) {
     const int b = b0 + (e & (CB - 1));
-    if (b < x.B) Y[(int64_t)(e >> x.cb_log2_row) * x.B + b] = cconj(sm[spad(e)]);
+    if (b < x.B) Y[(int64_t)(e >> x.cb_log2_row) * x.ldy + b] = cconj(sm[spad(e)]);
   }
 }
 
@@ -519,7 +522,7 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv_b(FftBArgs x) {
       v[u] = make_double2(0.0, 0.0);
       w[u] = make_double2(1.0, 0.0);
       if (e < n_el && b < x.B) {
-        v[u] = a.Y[(n1 + a.L1 * (int64_t)pp) * x.B + b];
+        v[u] = a.Y[(n1 + a.L1 * (int64_t)pp) * x.ldy + b];
         w[u] = wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)__ldg(a.rev2 + pp));
       }
     }
@@ -544,7 +547,118 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_colinv_b(FftBArgs x) {
       const int e = e0 + u * T;
       const int b = b0 + (e & (CB - 1));
       const int64_t k = n1 + a.L1 * (int64_t)(e >> x.cb_log2_col);
-      if (e < n_el && b < x.B && k < a.Kout) a.h[k * x.B + b] = cmul(cconj(sm[spad(e)]), qv[u]);
+      if (e < n_el && b < x.B && k < a.Kout) a.h[k * x.ldg + b] = cmul(cconj(sm[spad(e)]), qv[u]);
+    }
+  }
+}
+
+// ------------------------------ register-resident batched passes (fft_reg.cuh)
+// Same three passes and layouts as k_colfwd_b / k_rowmul_b / k_colinv_b, with
+// the butterflies held in registers: global loads feed the first stage, the
+// last stage stores to global, and only the exchanges between stages go
+// through shared memory.
+template <int N, int NBL, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_colfwd_rb(FftBArgs x) {
+  using F = RegFft<N, NBL, T>;
+  constexpr int S0 = N / 8;
+  extern __shared__ double2 sm[];
+  const FftArgs& a = x.a;
+  const int64_t n1 = blockIdx.x;
+  const int b0 = blockIdx.y * F::NB;
+  F f;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k), b = b0 + F::vec(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int64_t n = n1 + a.L1 * (int64_t)F::template pos<S0>(u, r);
+      f.x[k][r] = make_double2(0.0, 0.0);
+      if (b < x.B && n < a.K) f.x[k][r] = cmul(__ldg(a.g + n * x.ldg + b), __ldg(a.P + n));
+    }
+  }
+  f.template dif_from<S0>(sm, a.st2, a.tw2);
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k), b = b0 + F::vec(k);
+    if (b >= x.B) continue;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int p = 8 * u + r;  // position p holds frequency rev8(p)
+      const double2 w = wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)rev8<N>(p));
+      a.Y[(n1 + a.L1 * (int64_t)p) * x.ldy + b] = cmul(f.x[k][r], w);
+    }
+  }
+}
+
+template <int N, int NBL, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_rowmul_rb(FftBArgs x) {
+  using F = RegFft<N, NBL, T>;
+  constexpr int S0 = N / 8;
+  extern __shared__ double2 sm[];
+  const FftArgs& a = x.a;
+  const int64_t p = blockIdx.x;
+  const int b0 = blockIdx.y * F::NB;
+  double2* Y = a.Y + p * a.L1 * x.ldy;
+  F f;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k), b = b0 + F::vec(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      f.x[k][r] = make_double2(0.0, 0.0);
+      if (b < x.B) f.x[k][r] = Y[(int64_t)F::template pos<S0>(u, r) * x.ldy + b];
+    }
+  }
+  f.template dif_from<S0>(sm, a.st1, a.tw1);
+  const double2* Bh = a.Bhat + p * a.L1;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) f.x[k][r] = cconj(cmul(f.x[k][r], __ldg(Bh + 8 * u + r)));
+  }
+  f.template dit_from<1>(sm, a.st1, a.tw1);
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k), b = b0 + F::vec(k);
+    if (b >= x.B) continue;
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      Y[(int64_t)F::template pos<S0>(u, r) * x.ldy + b] = cconj(f.x[k][r]);
+  }
+}
+
+template <int N, int NBL, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_colinv_rb(FftBArgs x) {
+  using F = RegFft<N, NBL, T>;
+  constexpr int S0 = N / 8;
+  extern __shared__ double2 sm[];
+  const FftArgs& a = x.a;
+  const int64_t n1 = blockIdx.x;
+  const int b0 = blockIdx.y * F::NB;
+  F f;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k), b = b0 + F::vec(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int p = 8 * u + r;
+      f.x[k][r] = make_double2(0.0, 0.0);
+      if (b < x.B) {
+        const double2 v = a.Y[(n1 + a.L1 * (int64_t)p) * x.ldy + b];
+        f.x[k][r] = cmul(cconj(v), wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)rev8<N>(p)));
+      }
+    }
+  }
+  f.template dit_from<1>(sm, a.st2, a.tw2);
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k), b = b0 + F::vec(k);
+    if (b >= x.B) continue;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int64_t kk = n1 + a.L1 * (int64_t)F::template pos<S0>(u, r);
+      if (kk < a.Kout) a.h[kk * x.ldg + b] = cmul(cconj(f.x[k][r]), __ldg(a.Q + kk));
     }
   }
 }
@@ -973,6 +1087,14 @@ DirectArgs make_direct_args(const NnfftPlanImpl& p) {
 
 }  // namespace
 
+template <int NBL, int T, int MINB>
+void set_reg_smem() {
+  const size_t sm = sizeof(double2) * ((size_t)512 << NBL);
+  set_smem(k_colfwd_rb<512, NBL, T, MINB>, sm);
+  set_smem(k_rowmul_rb<512, NBL, T, MINB>, sm);
+  set_smem(k_colinv_rb<512, NBL, T, MINB>, sm);
+}
+
 void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_dstep1, smem_bytes(kDirectSmem));
   set_smem(k_dstep2, smem_bytes(kDirectSmem2));
@@ -994,6 +1116,10 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_colfwd_b<512, 3>, smem_bytes(kColElemsB));
   set_smem(k_rowmul_b<512, 3>, smem_bytes(kColElemsB));
   set_smem(k_colinv_b<512, 3>, smem_bytes(kColElemsB));
+  set_reg_smem<3, 256, 2>();
+  set_reg_smem<2, 256, 3>();
+  set_reg_smem<2, 256, 4>();
+  set_reg_smem<3, 512, 1>();
   FftPlan& f = p.fft;
   const Geometry& g = p.g;
   const int64_t Lmin = g.K + f.Kout - 1;
@@ -1125,34 +1251,88 @@ bool fft_supports_point_major(const NnfftPlanImpl& p) {
   return !p.fft.direct && !p.fft.single;
 }
 
+// Columns are transformed in groups of G: the group's work array Y (L x G
+// complex) stays L2-resident across the three passes, so only the grid reads
+// and the h writes go to DRAM (all 256 columns at once: 3 x 2 x 1.1 GB).
+// register-resident kernel variant for this plan's point-major shape: 0 = none
+// (smem kernels); 1 = 8 columns x 256 threads (2 butterflies per thread);
+// 2 = 4 columns x 256 threads, 3 CTAs/SM; 3 = 8 columns x 512 threads;
+// 4 = as 2 with 4 CTAs/SM (64 registers)
+static int reg_variant(const FftPlan& f) {
+  if (!(f.L1 == 512 && f.L2 == 512 && f.st1.n == 512 && f.st2.n == 512)) return 0;
+  int v = 2;  // measured best (config 4 FFT 2.20 -> 1.90 ms)
+  if (const char* e = getenv("SFB_FFT_REG")) v = atoi(e);
+  return (v >= 0 && v <= 4) ? v : 2;
+}
+
+template <int NBL, int T, int MINB>
+static void launch_reg(const FftBArgs& x, int64_t L1, int64_t L2, cudaStream_t s) {
+  const size_t sm = sizeof(double2) * ((size_t)512 << NBL);
+  const dim3 gc((unsigned)L1, (unsigned)ceil_div(x.B, 1 << NBL));
+  const dim3 gr((unsigned)L2, (unsigned)ceil_div(x.B, 1 << NBL));
+  k_colfwd_rb<512, NBL, T, MINB><<<gc, T, sm, s>>>(x);
+  SF_LAUNCH_CHECK();
+  k_rowmul_rb<512, NBL, T, MINB><<<gr, T, sm, s>>>(x);
+  SF_LAUNCH_CHECK();
+  k_colinv_rb<512, NBL, T, MINB><<<gc, T, sm, s>>>(x);
+  SF_LAUNCH_CHECK();
+}
+
+static void run_reg_point_major(const FftBArgs& x, int64_t L1, int64_t L2, int v, cudaStream_t s) {
+  switch (v) {
+    case 1: launch_reg<3, 256, 2>(x, L1, L2, s); break;
+    case 2: launch_reg<2, 256, 3>(x, L1, L2, s); break;
+    case 4: launch_reg<2, 256, 4>(x, L1, L2, s); break;
+    default: launch_reg<3, 512, 1>(x, L1, L2, s); break;
+  }
+}
+
+int fft_point_major_group(int batch) {
+  int G = 0;  // all columns at once (16-64 column groups measured 7-48 % slower)
+  if (const char* e = getenv("SFB_FFT_GROUP")) G = atoi(e);
+  if (G <= 0 || G > batch) G = batch;
+  return G;
+}
+
 void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work,
                          int batch, cudaStream_t s) {
   const FftPlan& f = p.fft;
-  FftBArgs x{};
-  x.a = make_args(p);
-  x.a.g = grid;
-  x.a.h = h;
-  x.a.Y = work;
-  x.B = batch;
+  const int G = fft_point_major_group(batch);
   int cc = 8, cr = 8;
   while (cc > 1 && cc * f.L2 > kColElemsB) cc >>= 1;
   while (cr > 1 && cr * f.L1 > kColElemsB) cr >>= 1;
-  x.cb_log2_col = log2i(cc);
-  x.cb_log2_row = log2i(cr);
   const size_t smc = smem_bytes(f.L2 * cc), smr = smem_bytes(f.L1 * cr);
-  const dim3 gc((unsigned)f.L1, (unsigned)ceil_div(batch, cc));
-  // compile-time specialisation of the config-4 shape (512 x 512, 8 columns)
-  const bool ctc = f.L2 == 512 && x.cb_log2_col == 3 && f.st2.n == 512;
-  const bool ctr = f.L1 == 512 && x.cb_log2_row == 3 && f.st1.n == 512;
-  if (ctc) k_colfwd_b<512, 3><<<gc, 256, smc, s>>>(x);
-  else k_colfwd_b<0, 0><<<gc, 256, smc, s>>>(x);
-  SF_LAUNCH_CHECK();
-  if (ctr) k_rowmul_b<512, 3><<<dim3((unsigned)f.L2, (unsigned)ceil_div(batch, cr)), 256, smr, s>>>(x);
-  else k_rowmul_b<0, 0><<<dim3((unsigned)f.L2, (unsigned)ceil_div(batch, cr)), 256, smr, s>>>(x);
-  SF_LAUNCH_CHECK();
-  if (ctc) k_colinv_b<512, 3><<<gc, 256, smc, s>>>(x);
-  else k_colinv_b<0, 0><<<gc, 256, smc, s>>>(x);
-  SF_LAUNCH_CHECK();
+  const int reg = reg_variant(f);
+  for (int b0 = 0; b0 < batch; b0 += G) {
+    FftBArgs x{};
+    x.a = make_args(p);
+    x.a.g = grid + b0;
+    x.a.h = h + b0;
+    x.a.Y = work;
+    x.B = std::min(G, batch - b0);
+    x.ldg = batch;
+    x.ldy = G;
+    x.cb_log2_col = log2i(cc);
+    x.cb_log2_row = log2i(cr);
+    const dim3 gc((unsigned)f.L1, (unsigned)ceil_div(x.B, cc));
+    const dim3 gr((unsigned)f.L2, (unsigned)ceil_div(x.B, cr));
+    if (reg) {  // register-resident passes (512 x 512, the config-4 shape)
+      run_reg_point_major(x, f.L1, f.L2, reg, s);
+      continue;
+    }
+    // compile-time specialisation of the config-4 shape (512 x 512, 8 columns)
+    const bool ctc = f.L2 == 512 && x.cb_log2_col == 3 && f.st2.n == 512;
+    const bool ctr = f.L1 == 512 && x.cb_log2_row == 3 && f.st1.n == 512;
+    if (ctc) k_colfwd_b<512, 3><<<gc, 256, smc, s>>>(x);
+    else k_colfwd_b<0, 0><<<gc, 256, smc, s>>>(x);
+    SF_LAUNCH_CHECK();
+    if (ctr) k_rowmul_b<512, 3><<<gr, 256, smr, s>>>(x);
+    else k_rowmul_b<0, 0><<<gr, 256, smr, s>>>(x);
+    SF_LAUNCH_CHECK();
+    if (ctc) k_colinv_b<512, 3><<<gc, 256, smc, s>>>(x);
+    else k_colinv_b<0, 0><<<gc, 256, smc, s>>>(x);
+    SF_LAUNCH_CHECK();
+  }
   launch_fix(p, grid, h, batch, 1, s);
 }
 

@@ -184,6 +184,8 @@ void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* w
              cudaStream_t stream);
 // point-major variant: grid[K][batch] -> h[Kout][batch] (Bluestein path only)
 bool fft_supports_point_major(const NnfftPlanImpl& p);
+// columns per group of the point-major FFT (its work array holds L x group)
+int fft_point_major_group(int batch);
 void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work,
                          int batch, cudaStream_t stream);
 
