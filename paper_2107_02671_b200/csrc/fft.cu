@@ -563,8 +563,8 @@ __global__ void __launch_bounds__(T, MINB) k_colfwd_rb(FftBArgs x) {
   constexpr int S0 = N / 8;
   extern __shared__ double2 sm[];
   const FftArgs& a = x.a;
-  const int64_t n1 = blockIdx.x;
-  const int b0 = blockIdx.y * F::NB;
+  const int64_t n1 = blockIdx.y;
+  const int b0 = blockIdx.x * F::NB;  // column groups fastest: whole point rows
   F f;
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(T, MINB) k_colfwd_rb(FftBArgs x) {
       if (b < x.B && n < a.K) f.x[k][r] = cmul(__ldg(a.g + n * x.ldg + b), __ldg(a.P + n));
     }
   }
-  f.template dif_from<S0>(sm, a.st2, a.tw2);
+  f.dif(sm, a.st2, a.tw2);
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k), b = b0 + F::vec(k);
@@ -596,8 +596,8 @@ __global__ void __launch_bounds__(T, MINB) k_rowmul_rb(FftBArgs x) {
   constexpr int S0 = N / 8;
   extern __shared__ double2 sm[];
   const FftArgs& a = x.a;
-  const int64_t p = blockIdx.x;
-  const int b0 = blockIdx.y * F::NB;
+  const int64_t p = blockIdx.y;
+  const int b0 = blockIdx.x * F::NB;
   double2* Y = a.Y + p * a.L1 * x.ldy;
   F f;
 #pragma unroll
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(T, MINB) k_rowmul_rb(FftBArgs x) {
       if (b < x.B) f.x[k][r] = Y[(int64_t)F::template pos<S0>(u, r) * x.ldy + b];
     }
   }
-  f.template dif_from<S0>(sm, a.st1, a.tw1);
+  f.dif(sm, a.st1, a.tw1);
   const double2* Bh = a.Bhat + p * a.L1;
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(T, MINB) k_rowmul_rb(FftBArgs x) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) f.x[k][r] = cconj(cmul(f.x[k][r], __ldg(Bh + 8 * u + r)));
   }
-  f.template dit_from<1>(sm, a.st1, a.tw1);
+  f.dit(sm, a.st1, a.tw1);
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k), b = b0 + F::vec(k);
@@ -634,8 +634,8 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_rb(FftBArgs x) {
   constexpr int S0 = N / 8;
   extern __shared__ double2 sm[];
   const FftArgs& a = x.a;
-  const int64_t n1 = blockIdx.x;
-  const int b0 = blockIdx.y * F::NB;
+  const int64_t n1 = blockIdx.y;
+  const int b0 = blockIdx.x * F::NB;  // column groups fastest: whole point rows
   F f;
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_rb(FftBArgs x) {
       }
     }
   }
-  f.template dit_from<1>(sm, a.st2, a.tw2);
+  f.dit(sm, a.st2, a.tw2);
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k), b = b0 + F::vec(k);
@@ -659,6 +659,117 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_rb(FftBArgs x) {
     for (int r = 0; r < 8; ++r) {
       const int64_t kk = n1 + a.L1 * (int64_t)F::template pos<S0>(u, r);
       if (kk < a.Kout) a.h[kk * x.ldg + b] = cmul(cconj(f.x[k][r]), __ldg(a.Q + kk));
+    }
+  }
+}
+
+// Single-column (column-major [batch][*]) register-resident passes: the NB
+// vectors of a column CTA are NB consecutive n1 (as k_colfwd's C columns);
+// the row CTA holds one row (NB = 1).
+template <int N, int NBL, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
+  using F = RegFft<N, NBL, T>;
+  constexpr int S0 = N / 8;
+  extern __shared__ double2 sm[];
+  const int col = blockIdx.y;
+  const int64_t c0 = (int64_t)blockIdx.x * F::NB;
+  const double2* g = a.g + (int64_t)col * a.K;
+  F f;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+    const int64_t n1 = c0 + F::vec(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int64_t n = n1 + a.L1 * (int64_t)F::template pos<S0>(u, r);
+      f.x[k][r] = make_double2(0.0, 0.0);
+      if (n1 < a.L1 && n < a.K) {
+        double2 gv = __ldg(g + n);
+        if (a.conj_in) gv.y = -gv.y;
+        f.x[k][r] = cmul(gv, __ldg(a.P + n));
+      }
+    }
+  }
+  f.dif(sm, a.st2, a.tw2);
+  double2* Y = a.Y + (int64_t)col * a.L;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+    const int64_t n1 = c0 + F::vec(k);
+    if (n1 >= a.L1) continue;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int p = 8 * u + r;
+      Y[n1 + a.L1 * (int64_t)p] = cmul(f.x[k][r], wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)rev8<N>(p)));
+    }
+  }
+}
+
+template <int N, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_rowmul_r1(FftArgs a) {
+  using F = RegFft<N, 0, T>;
+  constexpr int S0 = N / 8;
+  extern __shared__ double2 sm[];
+  const int col = blockIdx.y;
+  const int64_t p = blockIdx.x;
+  double2* row = a.Y + (int64_t)col * a.L + p * a.L1;
+  F f;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) f.x[k][r] = row[F::template pos<S0>(u, r)];
+  }
+  f.dif(sm, a.st1, a.tw1);
+  const double2* Bh = a.Bhat + p * a.L1;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) f.x[k][r] = cconj(cmul(f.x[k][r], __ldg(Bh + 8 * u + r)));
+  }
+  f.dit(sm, a.st1, a.tw1);
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) row[F::template pos<S0>(u, r)] = cconj(f.x[k][r]);
+  }
+}
+
+template <int N, int NBL, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_colinv_r1(FftArgs a) {
+  using F = RegFft<N, NBL, T>;
+  constexpr int S0 = N / 8;
+  extern __shared__ double2 sm[];
+  const int col = blockIdx.y;
+  const int64_t c0 = (int64_t)blockIdx.x * F::NB;
+  const double2* Y = a.Y + (int64_t)col * a.L;
+  F f;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+    const int64_t n1 = c0 + F::vec(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int p = 8 * u + r;
+      f.x[k][r] = make_double2(0.0, 0.0);
+      if (n1 < a.L1)
+        f.x[k][r] = cmul(cconj(Y[n1 + a.L1 * (int64_t)p]),
+                         wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)rev8<N>(p)));
+    }
+  }
+  f.dit(sm, a.st2, a.tw2);
+  double2* h = a.h + (int64_t)col * a.Kout;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+    const int64_t n1 = c0 + F::vec(k);
+    if (n1 >= a.L1) continue;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int64_t kk = n1 + a.L1 * (int64_t)F::template pos<S0>(u, r);
+      if (kk < a.Kout) h[kk] = cmul(cconj(f.x[k][r]), __ldg(a.Q + kk));
     }
   }
 }
@@ -1120,6 +1231,12 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_reg_smem<2, 256, 3>();
   set_reg_smem<2, 256, 4>();
   set_reg_smem<3, 512, 1>();
+  set_smem(k_colfwd_r1<1024, 1, 256, 3>, sizeof(double2) * 2048);
+  set_smem(k_colinv_r1<1024, 1, 256, 3>, sizeof(double2) * 2048);
+  set_smem(k_colfwd_r1<1024, 2, 512, 1>, sizeof(double2) * 4096);
+  set_smem(k_colinv_r1<1024, 2, 512, 1>, sizeof(double2) * 4096);
+  set_smem(k_rowmul_r1<4096, 512, 1>, sizeof(double2) * 4096);
+  set_smem(k_rowmul_r1<4096, 256, 2>, sizeof(double2) * 4096);
   FftPlan& f = p.fft;
   const Geometry& g = p.g;
   const int64_t Lmin = g.K + f.Kout - 1;
@@ -1260,16 +1377,16 @@ bool fft_supports_point_major(const NnfftPlanImpl& p) {
 // 4 = as 2 with 4 CTAs/SM (64 registers)
 static int reg_variant(const FftPlan& f) {
   if (!(f.L1 == 512 && f.L2 == 512 && f.st1.n == 512 && f.st2.n == 512)) return 0;
-  int v = 2;  // measured best (config 4 FFT 2.20 -> 1.90 ms)
+  int v = 4;  // measured best (config 4 FFT 2.20 -> 1.77 ms)
   if (const char* e = getenv("SFB_FFT_REG")) v = atoi(e);
-  return (v >= 0 && v <= 4) ? v : 2;
+  return (v >= 0 && v <= 4) ? v : 4;
 }
 
 template <int NBL, int T, int MINB>
 static void launch_reg(const FftBArgs& x, int64_t L1, int64_t L2, cudaStream_t s) {
   const size_t sm = sizeof(double2) * ((size_t)512 << NBL);
-  const dim3 gc((unsigned)L1, (unsigned)ceil_div(x.B, 1 << NBL));
-  const dim3 gr((unsigned)L2, (unsigned)ceil_div(x.B, 1 << NBL));
+  const dim3 gc((unsigned)ceil_div(x.B, 1 << NBL), (unsigned)L1);
+  const dim3 gr((unsigned)ceil_div(x.B, 1 << NBL), (unsigned)L2);
   k_colfwd_rb<512, NBL, T, MINB><<<gc, T, sm, s>>>(x);
   SF_LAUNCH_CHECK();
   k_rowmul_rb<512, NBL, T, MINB><<<gr, T, sm, s>>>(x);
@@ -1336,6 +1453,38 @@ void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h
   launch_fix(p, grid, h, batch, 1, s);
 }
 
+// register-resident single-column passes for the config-3 shape (4096 x
+// 1024): 0 = smem kernels; 1 = columns 2 x 256 threads, rows 512 threads;
+// 2 = columns 4 x 512 threads, rows 512 threads; 3 = columns 2 x 256, rows 256
+// threads (2 butterflies each)
+static int reg1_variant(const FftPlan& f) {
+  if (!(f.L1 == 4096 && f.L2 == 1024 && f.st1.n == 4096 && f.st2.n == 1024)) return 0;
+  int v = 3;  // measured best (0.217 -> 0.199 ms; a persistent cp.async-pipelined
+              // version of these passes measured 9 % slower)
+  if (const char* e = getenv("SFB_FFT_REG1")) v = atoi(e);
+  return (v >= 0 && v <= 3) ? v : 3;
+}
+
+template <int CBL, int CT, int CMINB, int RT, int RMINB>
+static void launch_reg1(const FftArgs& a, const FftPlan& f, int batch, cudaStream_t s) {
+  const size_t smc = sizeof(double2) * ((size_t)1024 << CBL), smr = sizeof(double2) * 4096;
+  const dim3 gc((unsigned)ceil_div(f.L1, (int64_t)1 << CBL), batch);
+  k_colfwd_r1<1024, CBL, CT, CMINB><<<gc, CT, smc, s>>>(a);
+  SF_LAUNCH_CHECK();
+  k_rowmul_r1<4096, RT, RMINB><<<dim3((unsigned)f.L2, batch), RT, smr, s>>>(a);
+  SF_LAUNCH_CHECK();
+  k_colinv_r1<1024, CBL, CT, CMINB><<<gc, CT, smc, s>>>(a);
+  SF_LAUNCH_CHECK();
+}
+
+static void run_reg1(const FftArgs& a, const FftPlan& f, int batch, int v, cudaStream_t s) {
+  switch (v) {
+    case 1: launch_reg1<1, 256, 3, 512, 1>(a, f, batch, s); break;
+    case 2: launch_reg1<2, 512, 1, 512, 1>(a, f, batch, s); break;
+    default: launch_reg1<1, 256, 3, 256, 2>(a, f, batch, s); break;
+  }
+}
+
 void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work, int batch,
              cudaStream_t s) {
   const FftPlan& f = p.fft;
@@ -1360,6 +1509,11 @@ void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* w
     const size_t sm = smem_bytes(f.L);
     k_single<IN_GP><<<dim3(1, batch), 512, sm, s>>>(a, 0);
     SF_LAUNCH_CHECK();
+    return;
+  }
+  if (reg1_variant(f)) {
+    run_reg1(a, f, batch, reg1_variant(f), s);
+    launch_fix(p, grid, h, batch, 0, s);
     return;
   }
   const size_t smc = smem_bytes(f.L2 * f.C), smr = smem_bytes(f.L1);

@@ -14,8 +14,8 @@
 // read own next inputs: 2 x 16 bytes per element per exchange).  The fused
 // row pass keeps the last DIF stage and the first DIT stage (both stride 1,
 // same thread, same 8 positions) in registers with the B-hat multiply between
-// them.  Length N = 8^a (the shapes the planner picks for the batched path:
-// 512 x 512), NB = 2^NBL interleaved vectors (columns) per CTA, T threads.
+// them.  Length N = 8^a * R0 with R0 in {1, 2, 4} (config 4: 512 x 512,
+// config 3: 4096 x 1024), NB = 2^NBL interleaved vectors per CTA, T threads.
 //
 // Position conventions are exactly those of fft_stage<8, DIT> (fft.cuh):
 // butterfly u of a stage with stride S = N / 8^(q+1) has legs
@@ -29,40 +29,58 @@
 
 namespace sfb {
 
-__host__ __device__ constexpr int ilog8(int n) { return n <= 1 ? 0 : 1 + ilog8(n / 8); }
+__host__ __device__ constexpr int ilog8(int n) { return n < 8 ? 0 : 1 + ilog8(n / 8); }
+__host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
 
-// frequency held by position p after a radix-8 DIF of length N = 8^a: the
-// base-8 digits of p reversed (= digit_reverse() of fft.cu, without a load)
+// N = 8^a * R0, R0 in {1, 2, 4}: make_stages() order (radix 8 first, then
+// one radix-R0 stage of stride 1)
+template <int N>
+struct RegShape {
+  static constexpr int A = ilog8(N);           // radix-8 stages
+  static constexpr int R0 = N >> (3 * A);      // final radix (1: none)
+  static constexpr int LOG2N = ilog2c(N);
+  static_assert(R0 == 1 || R0 == 2 || R0 == 4, "N must be 8^a * {1,2,4}");
+  static_assert((1 << LOG2N) == N, "N must be a power of two");
+};
+
+// frequency held by position p after the DIF of length N (the digit reversal
+// of fft.cu's digit_reverse(), without a load): p = sum_q d_q S_q,
+// k = sum_q d_q 8^q with S_q = N / 8^(q+1) and the radix-R0 digit last
 template <int N>
 __device__ __forceinline__ int rev8(int p) {
+  using Sh = RegShape<N>;
   int k = 0;
 #pragma unroll
-  for (int q = 0; q < ilog8(N); ++q) k = (k << 3) | ((p >> (3 * q)) & 7);
+  for (int q = 0; q < Sh::A; ++q) k |= ((p >> (Sh::LOG2N - 3 * (q + 1))) & 7) << (3 * q);
+  if (Sh::R0 > 1) k |= (p & (Sh::R0 - 1)) << (3 * Sh::A);
   return k;
 }
 
-template <int N, int NBL, int T>
+template <int N_, int NBL, int T>
 struct RegFft {
+  using Sh = RegShape<N_>;
+  static constexpr int R0 = Sh::R0;
+  static constexpr int N = N_;
+  static constexpr int NBLOG = NBL;
   static constexpr int NB = 1 << NBL;
-  static constexpr int NQ = (N / 8) << NBL;  // butterflies per stage (all vectors)
+  static constexpr int NQ = (N / 8) << NBL;  // 8-element groups per stage (all vectors)
   static constexpr int BPT = NQ / T;
-  static constexpr int NST = ilog8(N);
   static_assert(NQ % T == 0 && BPT >= 1, "threads must divide the butterflies");
-  static_assert((1 << (3 * NST)) == N, "N must be a power of 8");
 
   double2 x[BPT][8];
 
-  // vector (column) of this thread's k-th butterfly, and its index u
+  // vector (column) of this thread's k-th group, and the group index u
   static __device__ __forceinline__ int vec(int k) { return (threadIdx.x + k * T) & (NB - 1); }
   static __device__ __forceinline__ int but(int k) { return (threadIdx.x + k * T) >> NBL; }
-  // position of leg r of butterfly u in a stage of stride S
+  // position of leg r of radix-8 butterfly u in a stage of stride S; S = 1
+  // is also the layout of the final radix-R0 stage (positions 8u + r)
   template <int S>
   static __device__ __forceinline__ int pos(int u, int r) {
     return (u / S) * 8 * S + (u % S) + r * S;
   }
-  // DIF/DIT stage index of stride S (S = N / 8^(q+1))
+  // DIF/DIT stage index of radix-8 stride S (S = N / 8^(q+1))
   template <int S>
-  static constexpr int stage() { return NST - 1 - ilog8(S); }
+  static constexpr int stage() { return ilog8(N / S) - 1; }
 
   template <int S>
   __device__ __forceinline__ void to_smem(double2* sm) const {
@@ -82,6 +100,14 @@ struct RegFft {
       for (int r = 0; r < 8; ++r) x[k][r] = sm[spad((pos<S>(u, r) << NBL) + b)];
     }
   }
+  // write own stride-S outputs, barrier, read own stride-S2 inputs (the
+  // positions a thread reads are the ones it writes next: no second barrier)
+  template <int S, int S2>
+  __device__ __forceinline__ void exchange(double2* sm) {
+    to_smem<S>(sm);
+    __syncthreads();
+    from_smem<S2>(sm);
+  }
   template <int S, bool DIT>
   __device__ __forceinline__ void butterflies(const FftStages& st, const double2* __restrict__ tw) {
     const double2* t = tw + st.toff[stage<S>()];
@@ -96,31 +122,52 @@ struct RegFft {
       if (!DIT && twid) apply_twiddles<8>(x[k], w1);
     }
   }
+  // the stride-1 radix-R0 stage: 8/R0 butterflies on positions 8u + r (no twiddles)
+  __device__ __forceinline__ void radix_r0() {
+#pragma unroll
+    for (int k = 0; k < BPT; ++k)
+#pragma unroll
+      for (int c = 0; c < 8 / R0; ++c) Dft<R0>::run(&x[k][c * R0]);
+  }
 
-  // DIF stages of strides S, S/8, ..., 1 (data of stride S already in x);
-  // ends with the stride-1 outputs in registers (no barrier after)
+  // DIF from the radix-8 stage of stride S (its inputs in x); ends with the
+  // final-stage outputs (positions 8u + r) in registers, no barrier after
   template <int S>
   __device__ __forceinline__ void dif_from(double2* sm, const FftStages& st,
                                            const double2* __restrict__ tw) {
     butterflies<S, false>(st, tw);
-    if constexpr (S > 1) {
-      to_smem<S>(sm);
-      __syncthreads();
-      from_smem<S / 8>(sm);
+    if constexpr (S > R0) {
+      exchange<S, S / 8>(sm);
       dif_from<S / 8>(sm, st, tw);
+    } else if constexpr (R0 > 1) {
+      exchange<S, 1>(sm);
+      radix_r0();
     }
   }
-  // DIT stages of strides S, 8S, ..., N/8 (data of stride S in x); ends with
-  // the stride-N/8 (natural-order) outputs in registers
+  __device__ __forceinline__ void dif(double2* sm, const FftStages& st,
+                                      const double2* __restrict__ tw) {
+    dif_from<N / 8>(sm, st, tw);
+  }
+  // DIT from the radix-8 stage of stride S; ends with the stride-N/8
+  // (natural-order) outputs in registers
   template <int S>
   __device__ __forceinline__ void dit_from(double2* sm, const FftStages& st,
                                            const double2* __restrict__ tw) {
     butterflies<S, true>(st, tw);
     if constexpr (S < N / 8) {
-      to_smem<S>(sm);
-      __syncthreads();
-      from_smem<S * 8>(sm);
+      exchange<S, S * 8>(sm);
       dit_from<S * 8>(sm, st, tw);
+    }
+  }
+  // full DIT from the final-stage layout (positions 8u + r, digit-reversed)
+  __device__ __forceinline__ void dit(double2* sm, const FftStages& st,
+                                      const double2* __restrict__ tw) {
+    if constexpr (R0 > 1) {
+      radix_r0();
+      exchange<1, R0>(sm);
+      dit_from<R0>(sm, st, tw);
+    } else {
+      dit_from<1>(sm, st, tw);
     }
   }
 };
