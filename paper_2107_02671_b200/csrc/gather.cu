@@ -130,28 +130,17 @@ __device__ __forceinline__ double2 gather_one(const GatherArgs& a, const double2
 #ifndef SFB_GATHER2_MINB
 #define SFB_GATHER2_MINB (8 * 128 / SFB_GATHER_THREADS)  // 64 registers (0.381 -> 0.299 ms at config 3)
 #endif
+// kGatherTPT = 2 * NP: each thread interpolates NP pairs of targets (j, j +
+// kGatherThreads) of its group, one window_dot2 per pair, after ONE staged
+// copy of the group's h span -- more targets per CTA amortise the copy
+// latency every CTA exposes at its start.
 template <int M>
 __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(GatherArgs a,
                                                                             WinCoef C) {
+  constexpr int NP = kGatherTPT / 2;
   __shared__ double2 hs[kGatherSpan];
-  const int64_t j0 = (int64_t)blockIdx.x * (2 * kGatherThreads) + threadIdx.x;
-  const int64_t j1 = j0 + kGatherThreads;
+  const int64_t jb = (int64_t)blockIdx.x * kGatherGroup + threadIdx.x;
   const int col = blockIdx.y;
-  const bool act0 = j0 < a.M2, act1 = j1 < a.M2;
-  double pos0 = 0.0, sc0 = 0.0, pos1 = 0.0, sc1 = 0.0;
-  int dst0 = 0, dst1 = 0;
-  if (act0) {
-    pos0 = __ldg(a.pos + j0);
-    sc0 = __ldg(a.scale + j0);
-    dst0 = __ldg(a.perm + j0);
-  }
-  if (act1) {
-    pos1 = __ldg(a.pos + j1);
-    sc1 = __ldg(a.scale + j1);
-    dst1 = __ldg(a.perm + j1);
-  } else {
-    pos1 = pos0;  // keep the second window in range
-  }
   const double2* h = a.h + (int64_t)col * a.Kout;
   const int2 sp = __ldg(a.span + blockIdx.x);
   const int64_t klo = sp.x, khi = sp.y;
@@ -160,22 +149,46 @@ __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(Ga
     for (int64_t i = threadIdx.x; i <= khi - klo; i += kGatherThreads)
       cp_async16(hs + i, h + klo + i);
     cp_async_commit();
+  }
+  double pos[2 * NP], sc[2 * NP];
+  int dst[2 * NP];
+#pragma unroll
+  for (int t = 0; t < 2 * NP; ++t) {
+    const int64_t j = jb + (int64_t)t * kGatherThreads;
+    pos[t] = t > 0 ? pos[0] : 0.0;  // inactive targets keep a window in range
+    sc[t] = 0.0;
+    dst[t] = -1;
+    if (j < a.M2) {
+      pos[t] = __ldg(a.pos + j);
+      sc[t] = __ldg(a.scale + j);
+      dst[t] = __ldg(a.perm + j);
+    }
+  }
+  if (staged) {
     cp_async_wait<0>();
     __syncthreads();
   }
-  if (!act0) return;
-  double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
-  if (staged) {
-    const double c0 = floor(pos0), c1 = floor(pos1);
-    const int64_t k0 = (int64_t)c0 + (1 - M) - a.s_lo, k1 = (int64_t)c1 + (1 - M) - a.s_lo;
-    window_dot2<M>(C, pos0 - c0, pos1 - c1, hs + (k0 - klo), hs + (k1 - klo), s0, s1);
-  } else {
-    s0 = gather_one<M>(a, h, pos0, C);
-    if (act1) s1 = gather_one<M>(a, h, pos1, C);
-  }
+  if (dst[0] < 0) return;
   const double sg = a.conj_out ? -1.0 : 1.0;
-  a.out[(int64_t)dst0 * a.batch + col] = make_double2(s0.x * sc0, sg * (s0.y * sc0));
-  if (act1) a.out[(int64_t)dst1 * a.batch + col] = make_double2(s1.x * sc1, sg * (s1.y * sc1));
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const double p0 = pos[2 * q], p1 = dst[2 * q + 1] >= 0 ? pos[2 * q + 1] : p0;
+    double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
+    if (dst[2 * q] < 0) break;
+    if (staged) {
+      const double c0 = floor(p0), c1 = floor(p1);
+      const int64_t k0 = (int64_t)c0 + (1 - M) - a.s_lo, k1 = (int64_t)c1 + (1 - M) - a.s_lo;
+      window_dot2<M>(C, p0 - c0, p1 - c1, hs + (k0 - klo), hs + (k1 - klo), s0, s1);
+    } else {
+      s0 = gather_one<M>(a, h, p0, C);
+      if (dst[2 * q + 1] >= 0) s1 = gather_one<M>(a, h, p1, C);
+    }
+    a.out[(int64_t)dst[2 * q] * a.batch + col] =
+        make_double2(s0.x * sc[2 * q], sg * (s0.y * sc[2 * q]));
+    if (dst[2 * q + 1] >= 0)
+      a.out[(int64_t)dst[2 * q + 1] * a.batch + col] =
+          make_double2(s1.x * sc[2 * q + 1], sg * (s1.y * sc[2 * q + 1]));
+  }
 }
 
 void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batch,
@@ -186,7 +199,7 @@ void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batc
   switch (p.g.m2) {
 #define SF_CASE(MM)                                          \
   case MM:                                                   \
-    if (kGatherTPT == 2) k_gather2<MM><<<grid, kGatherThreads, 0, s>>>(a, p.c2); \
+    if (kGatherTPT >= 2) k_gather2<MM><<<grid, kGatherThreads, 0, s>>>(a, p.c2); \
     else k_gather<MM><<<grid, kGatherThreads, 0, s>>>(a, p.c2);              \
     break;
     SF_CASE(2) SF_CASE(3) SF_CASE(4) SF_CASE(5) SF_CASE(6) SF_CASE(7) SF_CASE(8) SF_CASE(9)
