@@ -16,6 +16,7 @@ from .fast_sinc import SincMode, SincPlan, fast_sinc_transform, sinc_plan
 from .nnfft import (NnfftGeometry, NnfftPlan, WindowSpec, nnfft_adjoint, nnfft_plan,
                     nnfft_trafo, nnfft_trafo_into, rescale_frequencies)
 from .quadrature import CcQuadrature, cc_quadrature, cc_weights_direct, cc_weights_fast
+from .sinc_approx import sinc_expsum_eval, sinc_expsum_eval_grid, sinc_expsum_max_error
 
 __version__ = "0.1.0"
 
@@ -27,5 +28,6 @@ __all__ = [
     "SincMode", "SincPlan", "sinc_plan", "fast_sinc_transform",
     "NfftPlan", "nfft_plan", "nfft_trafo", "nfft_adjoint",
     "nndft_direct", "ndft_direct", "sinc_transform_direct",
+    "sinc_expsum_eval", "sinc_expsum_eval_grid", "sinc_expsum_max_error",
     "bounds", "direct", "__version__",
 ]
