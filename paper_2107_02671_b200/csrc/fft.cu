@@ -1237,6 +1237,10 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_colinv_r1<1024, 2, 512, 1>, sizeof(double2) * 4096);
   set_smem(k_rowmul_r1<4096, 512, 1>, sizeof(double2) * 4096);
   set_smem(k_rowmul_r1<4096, 256, 2>, sizeof(double2) * 4096);
+  set_smem(k_colfwd_r1<1024, 1, 256, 4>, sizeof(double2) * 2048);
+  set_smem(k_colinv_r1<1024, 1, 256, 4>, sizeof(double2) * 2048);
+  set_smem(k_colfwd_r1<1024, 2, 256, 2>, sizeof(double2) * 4096);
+  set_smem(k_colinv_r1<1024, 2, 256, 2>, sizeof(double2) * 4096);
   FftPlan& f = p.fft;
   const Geometry& g = p.g;
   const int64_t Lmin = g.K + f.Kout - 1;
@@ -1456,13 +1460,14 @@ void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h
 // register-resident single-column passes for the config-3 shape (4096 x
 // 1024): 0 = smem kernels; 1 = columns 2 x 256 threads, rows 512 threads;
 // 2 = columns 4 x 512 threads, rows 512 threads; 3 = columns 2 x 256, rows 256
-// threads (2 butterflies each)
+// threads (2 butterflies each); 4 = as 3 with the column kernels at 4 CTAs/SM
+// (64 registers); 5 = columns 4 x 256 threads
 static int reg1_variant(const FftPlan& f) {
   if (!(f.L1 == 4096 && f.L2 == 1024 && f.st1.n == 4096 && f.st2.n == 1024)) return 0;
-  int v = 3;  // measured best (0.217 -> 0.199 ms; a persistent cp.async-pipelined
+  int v = 4;  // measured best (0.217 -> 0.192 ms; a persistent cp.async-pipelined
               // version of these passes measured 9 % slower)
   if (const char* e = getenv("SFB_FFT_REG1")) v = atoi(e);
-  return (v >= 0 && v <= 3) ? v : 3;
+  return (v >= 0 && v <= 5) ? v : 4;
 }
 
 template <int CBL, int CT, int CMINB, int RT, int RMINB>
@@ -1481,6 +1486,8 @@ static void run_reg1(const FftArgs& a, const FftPlan& f, int batch, int v, cudaS
   switch (v) {
     case 1: launch_reg1<1, 256, 3, 512, 1>(a, f, batch, s); break;
     case 2: launch_reg1<2, 512, 1, 512, 1>(a, f, batch, s); break;
+    case 4: launch_reg1<1, 256, 4, 256, 2>(a, f, batch, s); break;
+    case 5: launch_reg1<2, 256, 2, 256, 2>(a, f, batch, s); break;
     default: launch_reg1<1, 256, 3, 256, 2>(a, f, batch, s); break;
   }
 }
