@@ -289,14 +289,30 @@ def run_b200(args, cfg):
     # shard sources and targets (contiguous index ranges)
     s0, s1 = rank * cfg["M1"] // world, (rank + 1) * cfg["M1"] // world
     t0_, t1_ = rank * cfg["M2"] // world, (rank + 1) * cfg["M2"] // world
+    # N > 1: sources and targets are partitioned by POSITION (quantile ranges
+    # of v and x): a rank's sources fill 1/P of the K-grid at full density
+    # (index shards of clustered nodes cover the whole grid at 1/P density:
+    # sparse chunks, and every rank flushes the whole grid)
+    src_idx = np.argsort(vs, kind="stable")[s0:s1] if world > 1 else slice(None)
+    tgt_idx = np.argsort(x, kind="stable")[t0_:t1_] if world > 1 else slice(None)
     torch.cuda.synchronize()
     tp = time.perf_counter()
-    plan = sf.nnfft_plan(n_star, vs[s0:s1], x[t0_:t1_], m1=m, m2=m, device=local)
+    # N > 1: the FFT is split over the ranks too (sharding.DistributedFftNnfft,
+    # plans share one FFT via the geometric h window) unless --replicated-fft
+    # or the plan shape is outside the distributed kernels' envelope
+    want_dist = world > 1 and not cfg["batch"] and not args.replicated_fft
+    plan = sf.nnfft_plan(n_star, vs[src_idx], x[tgt_idx], m1=m, m2=m, device=local,
+                         h_window="full" if want_dist else "data")
+    dist_fft = None
+    if want_dist:
+        from paper_2107_02671_b200.sharding import DistributedFftNnfft, dist_layout
+        if dist_layout(plan, world) is not None:
+            dist_fft = DistributedFftNnfft(plan)
     torch.cuda.synchronize()
     plan_ms = (time.perf_counter() - tp) * 1e3
     geo = plan.backend_geometry
     B = max(cfg["batch"], 1)
-    fshard = np.ascontiguousarray(f[s0:s1])
+    fshard = np.ascontiguousarray(f[src_idx])
     d_f = torch.from_numpy(fshard).to(dev)
     d_out = torch.empty((t1_ - t0_,) + ((B,) if cfg["batch"] else ()), dtype=torch.complex128,
                         device=dev)
@@ -308,6 +324,8 @@ def run_b200(args, cfg):
         if world == 1:
             _lib.check(L.sincfft_nnfft_execute(ph, d_f.data_ptr(), d_out.data_ptr(), B,
                                                _lib.PTR_DEVICE, sh))
+        elif dist_fft is not None:
+            d_out.copy_(dist_fft(d_f))
         else:
             _lib.check(L.sincfft_nnfft_spread(ph, d_f.data_ptr(), d_grid.data_ptr(), B,
                                               _lib.PTR_DEVICE, sh))
@@ -350,7 +368,7 @@ def run_b200(args, cfg):
     if args.check_shards and world > 1:
         # the unsharded transform of the same inputs (one plan over everything)
         full = sf.nnfft_plan(n_star, vs, x, m1=m, m2=m, device=local)
-        ref = sf.nnfft_trafo(full, f)[t0_:t1_]
+        ref = sf.nnfft_trafo(full, f)[tgt_idx]
         torch.cuda.synchronize()
         shard_dev = float(np.max(np.abs(dev_out - ref)) / np.abs(f).sum())
         del full
@@ -499,6 +517,9 @@ def run_b200(args, cfg):
         del rp, tmp
 
     launches = L.sincfft_nnfft_launches_per_execute(ph, B) * args.steps
+    if dist_fft is not None:  # grid memset + spread, pack (+ tail fix), 3 passes
+        fix = 1 if geo["L"] < geo["K"] + geo["Kout"] - 1 else 0  # (+ rank-0 fix add), unpack, gather
+        launches = (2 + 1 + fix + 3 + (fix if rank == 0 else 0) + 1 + 1) * args.steps
     fp64_peak, fp64_note = 148 * 64 * 2 * (clk.max_mhz or 1965) * 1e6 / 1e12, \
         "derived: 148 SMs x 64 DFMA/clk x 2 flops x max SM clock"
     pf = os.path.join(ROOT, "profiles", "fp64_peak.json")
@@ -524,7 +545,10 @@ def run_b200(args, cfg):
                        "fft_length_L": geo["L"], "fft_L1xL2": [geo["L1"], geo["L2"]], "l2": "inputs larger than L2 "
                        "(f and out 256 MiB each per column vs 126 MB L2)",
                        "parallelism": f"sources+targets sharded x{world}" +
-                       (", NCCL all-reduce of the K-grid" if world > 1 else "")},
+                       (" by position (quantiles of v and x)" if world > 1 else "") +
+                       (("; distributed FFT: reduce-scatter + 2 all-to-all + all-gather"
+                         if dist_fft is not None else ", NCCL all-reduce of the K-grid")
+                        if world > 1 else "")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "alg_bytes_per_launch": alg[dom],
@@ -572,6 +596,9 @@ def main():
     ap.add_argument("--same-device", action="store_true",
                     help="map every rank to cuda:0 (with gloo: test the sharded path on one "
                          "GPU; kernels of different ranks never wait on each other)")
+    ap.add_argument("--replicated-fft", action="store_true",
+                    help="N > 1: all-reduce the K-grid and replicate the FFT (the "
+                         "north star's baseline partitioning) instead of splitting it")
     ap.add_argument("--check-shards", action="store_true",
                     help="N > 1: compare this rank's output shard with a single-rank "
                          "transform of the same inputs and report the max deviation")

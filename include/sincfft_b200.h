@@ -97,6 +97,18 @@ SINCFFT_API int sincfft_nnfft_plan_create(sincfft_nnfft_plan *plan, int64_t N, i
                               const double *v, const double *x, int32_t ptr_kind,
                               int32_t device, void *stream);
 
+/* As sincfft_nnfft_plan_create, with flags.  SINCFFT_PLAN_FULL_WINDOW: size
+ * the gather's h window [s_lo, s_lo + Kout) from the geometry (every
+ * |x| <= 1/2) instead of this plan's target extent, so plans built over
+ * different target shards of one problem share an identical FFT (required by
+ * the distributed FFT below; outputs equal the default plan's to rounding). */
+#define SINCFFT_PLAN_FULL_WINDOW 1
+SINCFFT_API int sincfft_nnfft_plan_create_ex(sincfft_nnfft_plan *plan, int64_t N, int64_t M1,
+                                             int64_t M2, double sigma1, double sigma2, int32_t m1,
+                                             int32_t m2, const double *v, const double *x,
+                                             int32_t ptr_kind, int32_t device, int32_t flags,
+                                             void *stream);
+
 SINCFFT_API int sincfft_nnfft_plan_destroy(sincfft_nnfft_plan plan);
 
 SINCFFT_API int sincfft_nnfft_plan_geometry(sincfft_nnfft_plan plan, sincfft_geometry *geo);
@@ -115,6 +127,35 @@ SINCFFT_API int sincfft_nnfft_spread(sincfft_nnfft_plan plan, const double *f, d
                          int64_t batch, int32_t ptr_kind, void *stream);
 SINCFFT_API int sincfft_nnfft_finish(sincfft_nnfft_plan plan, const double *grid_dev, double *out,
                          int64_t batch, int32_t ptr_kind, void *stream);
+
+/* Distributed FFT for source- and target-sharded runs (
+ * additive, no reference counterpart).  Instead of all-reducing the K-grid
+ * and replicating the FFT, the three Bluestein passes are split over the
+ * `world` ranks (rank r: columns [r Bc, (r+1) Bc) and rows [r Br, (r+1) Br))
+ * and the caller runs four collectives between five steps (all device
+ * pointers, complex doubles, single column, stream-ordered):
+ *   dist_pack(grid)            -> send[world * Sb]   ; reduce-scatter(sum) -> block[Sb]
+ *   dist_colfwd(block)         -> cols[L2 * Bc]      ; all-to-all (equal splits) -> rows
+ *   dist_rowmul(rows)             in place           ; all-to-all -> cols2[L2 * Bc]
+ *   dist_colinv(cols2, block)  -> hblk[K2 * Bc]      ; all-gather -> hall[world * K2 * Bc]
+ *   dist_gather(hall)          -> out[M2] for this plan's targets
+ * Plans of all ranks must be built with SINCFFT_PLAN_FULL_WINDOW over the
+ * same N, sigma, m.  dist_layout: sizes[0] = 1 if the plan and world size are
+ * supported (the config-3 shape 4096 x 1024, world a power of two dividing
+ * both), sizes[1] = Sb, sizes[2] = L2 * Bc, sizes[3] = K2 * Bc, sizes[4] = Bc,
+ * sizes[5] = Br (element counts of complex doubles). */
+SINCFFT_API int sincfft_nnfft_dist_layout(sincfft_nnfft_plan plan, int32_t world, int64_t *sizes);
+SINCFFT_API int sincfft_nnfft_dist_pack(sincfft_nnfft_plan plan, int32_t world,
+                                        const double *grid_dev, double *send_dev, void *stream);
+SINCFFT_API int sincfft_nnfft_dist_colfwd(sincfft_nnfft_plan plan, int32_t world, int32_t rank,
+                                          const double *block_dev, double *cols_dev, void *stream);
+SINCFFT_API int sincfft_nnfft_dist_rowmul(sincfft_nnfft_plan plan, int32_t world, int32_t rank,
+                                          double *rows_dev, void *stream);
+SINCFFT_API int sincfft_nnfft_dist_colinv(sincfft_nnfft_plan plan, int32_t world, int32_t rank,
+                                          const double *cols_dev, const double *block_dev,
+                                          double *hblk_dev, void *stream);
+SINCFFT_API int sincfft_nnfft_dist_gather(sincfft_nnfft_plan plan, int32_t world,
+                                          const double *hall_dev, double *out_dev, void *stream);
 
 /* Observability: one execute with DEVICE pointers and CUDA events recorded
  * on `stream` between the stages; returns after synchronizing the stream

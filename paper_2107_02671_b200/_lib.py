@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("SINCFFT_B200_LIB") or os.path.join(
 
 OK, EPARAM, EPOSITIVITY, ECUDA, ENOMEM, EUNSUPPORTED = range(6)
 PTR_HOST, PTR_DEVICE, PTR_HOST_ASYNC = 0, 1, 2
+PLAN_FULL_WINDOW = 1  # sincfft_nnfft_plan_create_ex flags
 
 
 class Geometry(C.Structure):
@@ -53,7 +54,17 @@ SIGNATURES = {
     "sincfft_nnfft_plan_create": (C.c_int, [C.POINTER(_vp), C.c_int64, C.c_int64, C.c_int64,
                                             C.c_double, C.c_double, C.c_int32, C.c_int32,
                                             _vp, _vp, C.c_int32, C.c_int32, _vp]),
+    "sincfft_nnfft_plan_create_ex": (C.c_int, [C.POINTER(_vp), C.c_int64, C.c_int64,
+                                               C.c_int64, C.c_double, C.c_double, C.c_int32,
+                                               C.c_int32, _vp, _vp, C.c_int32, C.c_int32,
+                                               C.c_int32, _vp]),
     "sincfft_nnfft_plan_destroy": (C.c_int, [_vp]),
+    "sincfft_nnfft_dist_layout": (C.c_int, [_vp, C.c_int32, _i64p]),
+    "sincfft_nnfft_dist_pack": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp]),
+    "sincfft_nnfft_dist_colfwd": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp]),
+    "sincfft_nnfft_dist_rowmul": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp]),
+    "sincfft_nnfft_dist_colinv": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]),
+    "sincfft_nnfft_dist_gather": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp]),
     "sincfft_nnfft_plan_geometry": (C.c_int, [_vp, C.POINTER(Geometry)]),
     "sincfft_nnfft_execute": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, _vp]),
     "sincfft_nnfft_spread": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, _vp]),

@@ -343,7 +343,16 @@ int sincfft_nnfft_plan_create(sincfft_nnfft_plan* plan, int64_t N, int64_t M1, i
                               double sigma1, double sigma2, int32_t m1, int32_t m2,
                               const double* v, const double* x, int32_t ptr_kind, int32_t device,
                               void* stream) {
+  return sincfft_nnfft_plan_create_ex(plan, N, M1, M2, sigma1, sigma2, m1, m2, v, x, ptr_kind,
+                                      device, 0, stream);
+}
+
+int sincfft_nnfft_plan_create_ex(sincfft_nnfft_plan* plan, int64_t N, int64_t M1, int64_t M2,
+                                 double sigma1, double sigma2, int32_t m1, int32_t m2,
+                                 const double* v, const double* x, int32_t ptr_kind,
+                                 int32_t device, int32_t flags, void* stream) {
   return guarded([&] {
+    if (flags & ~SINCFFT_PLAN_FULL_WINDOW) sfb::fail(1, "nnfft_plan: unknown flags");
     if (!plan) sfb::fail(1, "plan pointer is NULL");
     *plan = nullptr;
     check_ptr_kind(ptr_kind);
@@ -355,6 +364,7 @@ int sincfft_nnfft_plan_create(sincfft_nnfft_plan* plan, int64_t N, int64_t M1, i
     auto* h = new sincfft_nnfft_plan_s();
     try {
       InBuf vb(v, sizeof(double) * M1, ptr_kind, s), xb(x, sizeof(double) * M2, ptr_kind, s);
+      h->impl.full_window = (flags & SINCFFT_PLAN_FULL_WINDOW) != 0;
       build_nnfft(h->impl, N, M1, M2, sigma1, sigma2, m1, m2, (const double*)vb.ptr,
                   (const double*)xb.ptr, device, s);
       SF_CUDA(cudaStreamSynchronize(s));
@@ -442,6 +452,70 @@ int sincfft_nnfft_finish(sincfft_nnfft_plan plan, const double* grid_dev, double
       SF_CUDA(cudaMemcpyAsync(out, o.p, ob, cudaMemcpyDeviceToHost, s));
       if (ptr_kind == SINCFFT_PTR_HOST) SF_CUDA(cudaStreamSynchronize(s));
     }
+  });
+}
+
+int sincfft_nnfft_dist_layout(sincfft_nnfft_plan plan, int32_t world, int64_t* sizes) {
+  return guarded([&] {
+    if (!plan || !sizes) sfb::fail(1, "NULL argument");
+    sfb::DistLayout l;
+    const bool ok = sfb::dist_layout(plan->impl, world, &l);
+    sizes[0] = ok ? 1 : 0;
+    sizes[1] = ok ? l.Sb : 0;                    // reduce-scatter block (per rank)
+    sizes[2] = ok ? plan->impl.fft.L2 * l.Bc : 0;  // column-pass output = all-to-all buffer
+    sizes[3] = ok ? l.K2 * l.Bc : 0;              // h block (per rank, all-gather)
+    sizes[4] = ok ? l.Bc : 0;
+    sizes[5] = ok ? l.Br : 0;
+  });
+}
+
+#define SF_DIST_PROLOGUE(...)                                      \
+  if (!plan || __VA_ARGS__) sfb::fail(1, "NULL argument");        \
+  const sfb::NnfftPlanImpl& p = plan->impl;                       \
+  set_device(p.device);                                           \
+  cudaStream_t s = as_stream(stream)
+
+int sincfft_nnfft_dist_pack(sincfft_nnfft_plan plan, int32_t world, const double* grid_dev,
+                            double* send_dev, void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!grid_dev || !send_dev);
+    sfb::run_dist_pack(p, world, (const double2*)grid_dev, (double2*)send_dev, s);
+  });
+}
+
+int sincfft_nnfft_dist_colfwd(sincfft_nnfft_plan plan, int32_t world, int32_t rank,
+                              const double* block_dev, double* cols_dev, void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!block_dev || !cols_dev);
+    sfb::run_dist_colfwd(p, world, rank, (const double2*)block_dev, (double2*)cols_dev, s);
+  });
+}
+
+int sincfft_nnfft_dist_rowmul(sincfft_nnfft_plan plan, int32_t world, int32_t rank,
+                              double* rows_dev, void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!rows_dev);
+    sfb::run_dist_rowmul(p, world, rank, (double2*)rows_dev, s);
+  });
+}
+
+int sincfft_nnfft_dist_colinv(sincfft_nnfft_plan plan, int32_t world, int32_t rank,
+                              const double* cols_dev, const double* block_dev, double* hblk_dev,
+                              void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!cols_dev || !block_dev || !hblk_dev);
+    sfb::run_dist_colinv(p, world, rank, (const double2*)cols_dev, (const double2*)block_dev,
+                         (double2*)hblk_dev, s);
+  });
+}
+
+int sincfft_nnfft_dist_gather(sincfft_nnfft_plan plan, int32_t world, const double* hall_dev,
+                              double* out_dev, void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!hall_dev || !out_dev);
+    sfb::Scratch h(sizeof(double2) * (size_t)p.fft.Kout, s);
+    sfb::run_dist_unpack(p, world, (const double2*)hall_dev, h.as<double2>(), s);
+    sfb::run_gather(p, h.as<double2>(), (double2*)out_dev, 1, s);
   });
 }
 

@@ -774,6 +774,165 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_r1(FftArgs a) {
   }
 }
 
+// ------------------------------------------- distributed (column-split) FFT
+// The three Bluestein passes split over P ranks: rank r
+// owns the Bc = L1/P columns n1 in [r Bc, (r+1) Bc) for the column passes and
+// the Br = L2/P rows p in [r Br, (r+1) Br) for the row pass.  Host-side
+// collectives (sharding.py) move the data between the layouts below:
+//   pack      partial grid g[K] -> S[P][Sb], S[q] = columns of rank q as
+//             [i][c] (g[q Bc + c + L1 i], i < I = ceil(K/L1)), plus the
+//             Bluestein tail fix of THIS rank's partial grid in rank 0's block
+//             (linear, so the reduce-scatter sums it too)      -> reduce-scatter
+//   colfwd    own block [i][c] -> Yc[p][c] (p in [0, L2): rank-major rows
+//             for the all-to-all)                              -> all-to-all
+//   rowmul    rows [q][p_local][c] in place (q = source rank)  -> all-to-all
+//   colinv    [p][c] -> H[k2][c] = h[r Bc + c + L1 k2], k2 < K2 = ceil(Kout/L1)
+//             (rank 0 adds the summed tail fix)                -> all-gather
+//   unpack    [P][K2][Bc] -> h[Kout] natural, then the ordinary gather.
+// Instantiated for the config-3 shape (L1 = 4096 rows, L2 = 1024 columns); a
+// plan without it keeps the replicated FFT after an all-reduce.
+struct DistArgs {
+  FftArgs a;
+  int rank, world;
+  int64_t Bc, Br, I, K2, Sb;
+  int bc_log2;
+};
+
+__global__ void k_dpack(const double2* __restrict__ g, double2* __restrict__ S, DistArgs d) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= d.world * d.Sb) return;
+  const int64_t q = o / d.Sb, e = o - q * d.Sb;
+  double2 v = make_double2(0.0, 0.0);
+  if (e < d.I * d.Bc) {
+    const int64_t i = e >> d.bc_log2, c = e & (d.Bc - 1);
+    const int64_t n = q * d.Bc + c + d.a.L1 * i;
+    if (n < d.a.K) v = g[n];
+  }
+  S[o] = v;
+}
+
+template <int N, int NBL, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_dcolfwd(DistArgs d, const double2* __restrict__ R,
+                                                    double2* __restrict__ Yc) {
+  using F = RegFft<N, NBL, T>;
+  constexpr int S0 = N / 8;
+  extern __shared__ double2 sm[];
+  const FftArgs& a = d.a;
+  const int64_t c0 = (int64_t)blockIdx.x * F::NB;
+  F f;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+    const int64_t c = c0 + F::vec(k), n1 = d.rank * d.Bc + c;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int64_t i = F::template pos<S0>(u, r);
+      const int64_t n = n1 + a.L1 * i;
+      f.x[k][r] = make_double2(0.0, 0.0);
+      if (i < d.I && n < a.K) f.x[k][r] = cmul(__ldg(R + (i << d.bc_log2) + c), __ldg(a.P + n));
+    }
+  }
+  f.dif(sm, a.st2, a.tw2);
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+    const int64_t c = c0 + F::vec(k), n1 = d.rank * d.Bc + c;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int p = 8 * u + r;
+      Yc[((int64_t)p << d.bc_log2) + c] =
+          cmul(f.x[k][r], wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)rev8<N>(p)));
+    }
+  }
+}
+
+template <int N, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_drowmul(DistArgs d, double2* __restrict__ Rr) {
+  using F = RegFft<N, 0, T>;
+  constexpr int S0 = N / 8;
+  extern __shared__ double2 sm[];
+  const FftArgs& a = d.a;
+  const int64_t pl = blockIdx.x, p = d.rank * d.Br + pl;
+  // element n1 of local row pl: block (n1 / Bc) of the all-to-all, [pl][n1 % Bc]
+  auto at = [&](int n1) -> int64_t {
+    return ((((int64_t)(n1 >> d.bc_log2)) * d.Br + pl) << d.bc_log2) + (n1 & (d.Bc - 1));
+  };
+  F f;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) f.x[k][r] = Rr[at(F::template pos<S0>(u, r))];
+  }
+  f.dif(sm, a.st1, a.tw1);
+  const double2* Bh = a.Bhat + p * a.L1;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) f.x[k][r] = cconj(cmul(f.x[k][r], __ldg(Bh + 8 * u + r)));
+  }
+  f.dit(sm, a.st1, a.tw1);
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) Rr[at(F::template pos<S0>(u, r))] = cconj(f.x[k][r]);
+  }
+}
+
+template <int N, int NBL, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_dcolinv(DistArgs d, const double2* __restrict__ Y2,
+                                                    double2* __restrict__ H) {
+  using F = RegFft<N, NBL, T>;
+  constexpr int S0 = N / 8;
+  extern __shared__ double2 sm[];
+  const FftArgs& a = d.a;
+  const int64_t c0 = (int64_t)blockIdx.x * F::NB;
+  F f;
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+    const int64_t c = c0 + F::vec(k), n1 = d.rank * d.Bc + c;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int p = 8 * u + r;
+      f.x[k][r] = cmul(cconj(__ldg(Y2 + ((int64_t)p << d.bc_log2) + c)),
+                       wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)rev8<N>(p)));
+    }
+  }
+  f.dit(sm, a.st2, a.tw2);
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+    const int64_t c = c0 + F::vec(k), n1 = d.rank * d.Bc + c;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int64_t k2 = F::template pos<S0>(u, r);
+      const int64_t kk = n1 + a.L1 * k2;
+      if (k2 < d.K2 && kk < a.Kout) {
+        H[(k2 << d.bc_log2) + c] = cmul(cconj(f.x[k][r]), __ldg(a.Q + kk));
+      }
+    }
+  }
+}
+
+__global__ void k_dfix_add(double2* H, const double2* __restrict__ fix, int64_t D) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < D) {  // k' < D <= Bc: column k', k2 = 0 of rank 0's block
+    H[k].x += fix[k].x;
+    H[k].y += fix[k].y;
+  }
+}
+
+__global__ void k_dunpack(const double2* __restrict__ Hall, double2* __restrict__ h, DistArgs d) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= d.a.Kout) return;
+  const int64_t n1 = k % d.a.L1, k2 = k / d.a.L1;
+  const int64_t q = n1 >> d.bc_log2, c = n1 & (d.Bc - 1);
+  h[k] = Hall[((q * d.K2 + k2) << d.bc_log2) + c];
+}
+
 // ------------------------------------------------------ direct four-step
 // n = P n1 + n2 (n1 < A, n2 < P),  k = k1 + A k2:
 //   X[k1 + A k2] = sum_n2 W_P^{n2 k2} [ W_N2^{n2 k1} sum_n1 x[P n1 + n2] W_A^{n1 k1} ]
@@ -1238,6 +1397,7 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_rowmul_r1<4096, 512, 1>, sizeof(double2) * 4096);
   set_smem(k_rowmul_r1<4096, 256, 2>, sizeof(double2) * 4096);
   set_smem(k_colfwd_r1<1024, 1, 256, 4>, sizeof(double2) * 2048);
+  set_smem(k_drowmul<4096, 256, 2>, sizeof(double2) * 4096);
   set_smem(k_colinv_r1<1024, 1, 256, 4>, sizeof(double2) * 2048);
   set_smem(k_colfwd_r1<1024, 2, 256, 2>, sizeof(double2) * 4096);
   set_smem(k_colinv_r1<1024, 2, 256, 2>, sizeof(double2) * 4096);
@@ -1541,6 +1701,93 @@ void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* w
   else k_colinv<0, 0><<<gc, 256, smc, s>>>(a);
   SF_LAUNCH_CHECK();
   launch_fix(p, grid, h, batch, 0, s);
+}
+
+
+// ---------------------------------------------------- distributed FFT (host)
+static bool dist_shape(const FftPlan& f) {
+  return !f.direct && !f.single && !f.conj_in && f.L1 == 4096 && f.L2 == 1024 &&
+         f.st1.n == 4096 && f.st2.n == 1024;
+}
+
+bool dist_layout(const NnfftPlanImpl& p, int world, DistLayout* out) {
+  const FftPlan& f = p.fft;
+  DistLayout d{};
+  d.ok = false;
+  if (world >= 1 && (world & (world - 1)) == 0 && dist_shape(f) && f.L1 % world == 0 &&
+      f.L2 % world == 0 && f.L1 / world >= 2 && f.fixD <= f.L1 / world) {
+    d.Bc = f.L1 / world;
+    d.Br = f.L2 / world;
+    d.I = ceil_div(p.g.K, f.L1);
+    d.K2 = ceil_div(f.Kout, f.L1);
+    d.Sb = d.I * d.Bc + (f.fixD + 7) / 8 * 8;
+    d.ok = true;
+  }
+  *out = d;
+  return d.ok;
+}
+
+static DistArgs dist_args(const NnfftPlanImpl& p, int world, int rank) {
+  DistLayout l;
+  if (!dist_layout(p, world, &l)) fail(1, "distributed FFT: unsupported plan shape or world size");
+  if (rank < 0 || rank >= world) fail(1, "distributed FFT: rank out of range");
+  DistArgs d{};
+  d.a = make_args(p);
+  d.rank = rank;
+  d.world = world;
+  d.Bc = l.Bc;
+  d.Br = l.Br;
+  d.I = l.I;
+  d.K2 = l.K2;
+  d.Sb = l.Sb;
+  d.bc_log2 = log2i((int)l.Bc);
+  return d;
+}
+
+void run_dist_pack(const NnfftPlanImpl& p, int world, const double2* grid, double2* S,
+                   cudaStream_t s) {
+  const DistArgs d = dist_args(p, world, 0);
+  const int64_t n = (int64_t)world * d.Sb;
+  k_dpack<<<(unsigned)ceil_div(n, (int64_t)256), 256, 0, s>>>(grid, S, d);
+  SF_LAUNCH_CHECK();
+  const FftPlan& f = p.fft;
+  if (f.fixD > 0) {  // this rank's share of the tail fix, into rank 0's block
+    k_bluestein_fix<<<dim3((unsigned)ceil_div(f.fixD * 32, 256), 1), 256, 0, s>>>(
+        grid, f.P.p, f.fixc.p, f.Q.p, S + d.I * d.Bc, p.g.K, f.fixD, f.Kout, 0, 1, 0);
+    SF_LAUNCH_CHECK();
+  }
+}
+
+void run_dist_colfwd(const NnfftPlanImpl& p, int world, int rank, const double2* R, double2* Yc,
+                     cudaStream_t s) {
+  const DistArgs d = dist_args(p, world, rank);
+  k_dcolfwd<1024, 1, 256, 4><<<(unsigned)(d.Bc / 2), 256, sizeof(double2) * 2048, s>>>(d, R, Yc);
+  SF_LAUNCH_CHECK();
+}
+
+void run_dist_rowmul(const NnfftPlanImpl& p, int world, int rank, double2* Rr, cudaStream_t s) {
+  const DistArgs d = dist_args(p, world, rank);
+  k_drowmul<4096, 256, 2><<<(unsigned)d.Br, 256, sizeof(double2) * 4096, s>>>(d, Rr);
+  SF_LAUNCH_CHECK();
+}
+
+void run_dist_colinv(const NnfftPlanImpl& p, int world, int rank, const double2* Y2,
+                     const double2* R, double2* H, cudaStream_t s) {
+  const DistArgs d = dist_args(p, world, rank);
+  k_dcolinv<1024, 1, 256, 4><<<(unsigned)(d.Bc / 2), 256, sizeof(double2) * 2048, s>>>(d, Y2, H);
+  SF_LAUNCH_CHECK();
+  if (rank == 0 && p.fft.fixD > 0) {
+    k_dfix_add<<<(unsigned)ceil_div(p.fft.fixD, (int64_t)256), 256, 0, s>>>(H, R + d.I * d.Bc,
+                                                                          p.fft.fixD);
+    SF_LAUNCH_CHECK();
+  }
+}
+
+void run_dist_unpack(const NnfftPlanImpl& p, int world, const double2* Hall, double2* h,
+                     cudaStream_t s) {
+  const DistArgs d = dist_args(p, world, 0);
+  k_dunpack<<<(unsigned)ceil_div(p.fft.Kout, (int64_t)256), 256, 0, s>>>(Hall, h, d);
+  SF_LAUNCH_CHECK();
 }
 
 }  // namespace sfb

@@ -134,6 +134,10 @@ struct FftPlan {
 struct NnfftPlanImpl {
   Geometry g{};
   int device = 0;
+  // h window [s_lo, s_lo + Kout) from the geometry (|x| <= 1/2) instead of
+  // the targets' extent, so plans over different target shards share one FFT
+  // (the distributed FFT needs identical L, Kout, chirps on every rank)
+  bool full_window = false;
   WinCoef c1{}, c2{};
   SpreadPlan sp;
   GatherPlan gp;
@@ -184,6 +188,23 @@ void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* w
              cudaStream_t stream);
 // point-major variant: grid[K][batch] -> h[Kout][batch] (Bluestein path only)
 bool fft_supports_point_major(const NnfftPlanImpl& p);
+// Distributed (column-split) FFT over `world` ranks (fft.cu; layouts there).
+struct DistLayout {
+  bool ok;
+  int64_t Bc, Br;  // columns / rows per rank
+  int64_t I, K2;   // grid rows ceil(K/L1), output rows ceil(Kout/L1)
+  int64_t Sb;      // elements per rank block of the reduce-scatter buffer
+};
+bool dist_layout(const NnfftPlanImpl& p, int world, DistLayout* out);
+void run_dist_pack(const NnfftPlanImpl& p, int world, const double2* grid, double2* S,
+                   cudaStream_t s);
+void run_dist_colfwd(const NnfftPlanImpl& p, int world, int rank, const double2* R, double2* Yc,
+                     cudaStream_t s);
+void run_dist_rowmul(const NnfftPlanImpl& p, int world, int rank, double2* Rr, cudaStream_t s);
+void run_dist_colinv(const NnfftPlanImpl& p, int world, int rank, const double2* Y2,
+                     const double2* R, double2* H, cudaStream_t s);
+void run_dist_unpack(const NnfftPlanImpl& p, int world, const double2* Hall, double2* h,
+                     cudaStream_t s);
 // columns per group of the point-major FFT (its work array holds L x group)
 int fft_point_major_group(int batch);
 void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work,

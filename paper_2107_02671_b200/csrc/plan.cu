@@ -608,7 +608,15 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
   ts.beta1 = g.beta1;
   ts.m1 = g.m1;
   ts.N1 = g.N1;
-  build_targets(p, p.x_clip.p, g.M2, (double)g.N / (double)g.N1, (double)g.N2, g.N2, g.m2, ts, s);
+  int64_t fs_lo = 0, fkout = 0;
+  if (p.full_window) {  // every |x| <= 1/2, one slot of slack each side
+    const double pmax = (double)g.N2 * ((double)g.N / (double)g.N1) * 0.5;
+    fs_lo = (int64_t)std::floor(-pmax) - g.m2;
+    const int64_t s_hi = (int64_t)std::floor(pmax) + g.m2 + 1;
+    fkout = std::min<int64_t>(s_hi - fs_lo + 1, g.N2);
+  }
+  build_targets(p, p.x_clip.p, g.M2, (double)g.N / (double)g.N1, (double)g.N2, g.N2, g.m2, ts, s,
+                fs_lo, fkout);
 
   p.fft.in_scale = 1.0 / ((double)g.N1 * (double)g.N2);
   build_fft(p, s);

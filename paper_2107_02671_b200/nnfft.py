@@ -202,16 +202,24 @@ class NnfftPlan:
 
 
 def nnfft_plan(N, v, x, *, sigma1=2.0, sigma2=2.0, m1=4, m2=4,
-               window1="sinh", window2="sinh", device=None):
+               window1="sinh", window2="sinh", device=None, h_window="data"):
     """Build an :class:`NnfftPlan` (reference nnfft.py:131-207).
 
     ``v``/``x`` may be numpy arrays (copied to the GPU) or CUDA float64 torch
     tensors (validated and clipped on the device).  ``device`` selects the
     GPU (default: the tensor's device, else the current torch device or 0).
+    ``h_window`` (additive): "data" sizes the FFT output window from the
+    targets (default), "full" from the geometry, so plans over different
+    target shards of one problem share one FFT (the distributed FFT of
+    ``sharding.DistributedFftNnfft`` requires it).
     """
     _lib.require_gpu()
+    if h_window not in ("data", "full"):
+        raise ParameterError("nnfft_plan: h_window must be 'data' or 'full'")
+    flags = _lib.PLAN_FULL_WINDOW if h_window == "full" else 0
     if _is_torch(v) or _is_torch(x):
-        return _plan_from_torch(N, v, x, sigma1, sigma2, m1, m2, window1, window2, device)
+        return _plan_from_torch(N, v, x, sigma1, sigma2, m1, m2, window1, window2, device,
+                                flags)
     v = np.ascontiguousarray(v, dtype=float)
     x = np.ascontiguousarray(x, dtype=float)
     if v.ndim != 1 or v.size == 0:
@@ -233,9 +241,9 @@ def nnfft_plan(N, v, x, *, sigma1=2.0, sigma2=2.0, m1=4, m2=4,
     w2 = WindowSpec(window2, geo.m2, geo.sigma2, geo.N2)
     dev = _default_device(device)
     h = C.c_void_p()
-    _lib.check(_lib.lib.sincfft_nnfft_plan_create(
+    _lib.check(_lib.lib.sincfft_nnfft_plan_create_ex(
         C.byref(h), geo.N, geo.M1, geo.M2, float(sigma1), float(sigma2), geo.m1, geo.m2,
-        _vp(v), _vp(x), _lib.PTR_HOST, dev, None))
+        _vp(v), _vp(x), _lib.PTR_HOST, dev, flags, None))
     return NnfftPlan(h, geo, w1, w2, v, x, dev)
 
 
@@ -251,7 +259,7 @@ def _default_device(device):
     return 0
 
 
-def _plan_from_torch(N, v, x, sigma1, sigma2, m1, m2, window1, window2, device):
+def _plan_from_torch(N, v, x, sigma1, sigma2, m1, m2, window1, window2, device, flags=0):
     import torch
     if not (isinstance(v, torch.Tensor) and isinstance(x, torch.Tensor)):
         raise ParameterError("nnfft_plan: pass both v and x as CUDA tensors (or both as arrays)")
@@ -270,9 +278,9 @@ def _plan_from_torch(N, v, x, sigma1, sigma2, m1, m2, window1, window2, device):
     dev = v.device.index if device is None else int(device)
     h = C.c_void_p()
     # the C side checks the band (message names rescale_frequencies) and clips
-    _lib.check(_lib.lib.sincfft_nnfft_plan_create(
+    _lib.check(_lib.lib.sincfft_nnfft_plan_create_ex(
         C.byref(h), geo.N, geo.M1, geo.M2, float(sigma1), float(sigma2), geo.m1, geo.m2,
-        C.c_void_p(v.data_ptr()), C.c_void_p(x.data_ptr()), _lib.PTR_DEVICE, dev,
+        C.c_void_p(v.data_ptr()), C.c_void_p(x.data_ptr()), _lib.PTR_DEVICE, dev, flags,
         _stream_handle(v)))
     return NnfftPlan(h, geo, w1, w2, None, None, dev)
 

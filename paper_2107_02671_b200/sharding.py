@@ -74,3 +74,193 @@ def gpu_stages(plan, batch: int, stream=None):
         return out
 
     return spread, finish
+
+
+# ------------------------------------------------------------ distributed FFT
+def dist_layout(plan, world: int):
+    """Buffer sizes of the distributed FFT for `world` ranks, or None when the
+    plan shape / world size is not supported (then use ShardedNnfft)."""
+    import ctypes as C
+
+    from . import _lib
+
+    sizes = (C.c_int64 * 6)()
+    _lib.check(_lib.lib.sincfft_nnfft_dist_layout(plan.handle, int(world), sizes))
+    if not sizes[0]:
+        return None
+    return {"Sb": sizes[1], "cols": sizes[2], "hblk": sizes[3], "Bc": sizes[4], "Br": sizes[5]}
+
+
+class DistFftRank:
+    """The per-rank steps of the distributed FFT (C ABI ``sincfft_nnfft_dist_*``),
+    with the collectives left to the caller:
+
+        send = pack(f)            reduce-scatter(sum) -> block
+        cols = colfwd(block)      all-to-all          -> rows
+        rowmul(rows)              all-to-all          -> cols2
+        hblk = colinv(cols2)      all-gather          -> hall
+        out  = gather(hall)
+
+    ``plan`` covers this rank's source and target shards and must be built
+    with ``h_window="full"`` (identical FFT on every rank).  Device tensors,
+    complex128, single column, on the current torch stream."""
+
+    def __init__(self, plan, world: int, rank: int):
+        import torch
+
+        self.plan, self.world, self.rank = plan, int(world), int(rank)
+        self.layout = dist_layout(plan, world)
+        if self.layout is None:
+            raise ValueError("distributed FFT not supported for this plan / world size")
+        self.dev = torch.device("cuda", plan.device)
+        self.geo = plan.backend_geometry
+        self.block = None
+
+    def _s(self):
+        import ctypes as C
+
+        import torch
+        return C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+
+    def _empty(self, n):
+        import torch
+        return torch.empty(int(n), dtype=torch.complex128, device=self.dev)
+
+    def pack(self, f):
+        from . import _lib
+        grid = self._empty(self.geo["K"])
+        _lib.check(_lib.lib.sincfft_nnfft_spread(self.plan.handle, f.data_ptr(), grid.data_ptr(),
+                                                 1, _lib.PTR_DEVICE, self._s()))
+        send = self._empty(self.world * self.layout["Sb"])
+        _lib.check(_lib.lib.sincfft_nnfft_dist_pack(self.plan.handle, self.world, grid.data_ptr(),
+                                                    send.data_ptr(), self._s()))
+        return send
+
+    def colfwd(self, block):
+        from . import _lib
+        self.block = block  # colinv reads the reduced tail fix from it (rank 0)
+        cols = self._empty(self.layout["cols"])
+        _lib.check(_lib.lib.sincfft_nnfft_dist_colfwd(self.plan.handle, self.world, self.rank,
+                                                      block.data_ptr(), cols.data_ptr(),
+                                                      self._s()))
+        return cols
+
+    def rowmul(self, rows):
+        from . import _lib
+        _lib.check(_lib.lib.sincfft_nnfft_dist_rowmul(self.plan.handle, self.world, self.rank,
+                                                      rows.data_ptr(), self._s()))
+        return rows
+
+    def colinv(self, cols2):
+        from . import _lib
+        hblk = self._empty(self.layout["hblk"])
+        _lib.check(_lib.lib.sincfft_nnfft_dist_colinv(self.plan.handle, self.world, self.rank,
+                                                      cols2.data_ptr(), self.block.data_ptr(),
+                                                      hblk.data_ptr(), self._s()))
+        return hblk
+
+    def gather(self, hall):
+        from . import _lib
+        out = self._empty(self.geo["M2"])
+        _lib.check(_lib.lib.sincfft_nnfft_dist_gather(self.plan.handle, self.world,
+                                                      hall.data_ptr(), out.data_ptr(), self._s()))
+        return out
+
+
+class TorchCollectives:
+    """The four collectives over a torch.distributed group: NCCL natively
+    (reduce_scatter_tensor / all_to_all_single / all_gather_into_tensor on
+    the fp64 view), other backends (gloo, CPU tests and one-GPU validation)
+    through CPU staging and all_gather."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def reduce_scatter(self, send):
+        import torch
+        import torch.distributed as dist
+        n = send.numel() // self.world
+        if self.nccl:
+            out = torch.empty(n, dtype=send.dtype, device=send.device)
+            dist.reduce_scatter_tensor(torch.view_as_real(out), torch.view_as_real(send),
+                                       group=self.group)
+            return out
+        buf = torch.view_as_real(send).cpu()
+        dist.all_reduce(buf, group=self.group)
+        return torch.view_as_complex(buf)[self.rank * n:(self.rank + 1) * n].to(send.device)
+
+    def all_to_all(self, send):
+        import torch
+        import torch.distributed as dist
+        if self.nccl:
+            out = torch.empty_like(send)
+            dist.all_to_all_single(torch.view_as_real(out), torch.view_as_real(send),
+                                   group=self.group)
+            return out
+        n = send.numel() // self.world
+        full = [torch.empty_like(torch.view_as_real(send).cpu()) for _ in range(self.world)]
+        dist.all_gather(full, torch.view_as_real(send).cpu(), group=self.group)
+        parts = [torch.view_as_complex(b)[self.rank * n:(self.rank + 1) * n] for b in full]
+        return torch.cat(parts).to(send.device)
+
+    def all_gather(self, blk):
+        import torch
+        import torch.distributed as dist
+        if self.nccl:
+            out = torch.empty(blk.numel() * self.world, dtype=blk.dtype, device=blk.device)
+            dist.all_gather_into_tensor(torch.view_as_real(out), torch.view_as_real(blk),
+                                        group=self.group)
+            return out
+        full = [torch.empty_like(torch.view_as_real(blk).cpu()) for _ in range(self.world)]
+        dist.all_gather(full, torch.view_as_real(blk).cpu(), group=self.group)
+        return torch.view_as_complex(torch.cat(full)).to(blk.device)
+
+
+class DistributedFftNnfft:
+    """One NNFFT over the ranks of a torch.distributed group with the FFT
+    split too (no replicated stage): four collectives per transform, sized
+    ~(K + 2 L / P + Kout)/P complex per rank instead of an all-reduce of the
+    whole K-grid followed by the full FFT on every rank."""
+
+    def __init__(self, plan, group=None):
+        self.coll = TorchCollectives(group)
+        self.r = DistFftRank(plan, self.coll.world, self.coll.rank)
+
+    def __call__(self, f_shard):
+        r, c = self.r, self.coll
+        block = c.reduce_scatter(r.pack(f_shard))
+        rows = c.all_to_all(r.colfwd(block))
+        cols2 = c.all_to_all(r.rowmul(rows))
+        return r.gather(c.all_gather(r.colinv(cols2)))
+
+
+def run_ranks_in_process(ranks, f_shards):
+    """All ranks of the distributed FFT in ONE process (e.g. on one GPU): the
+    collectives become tensor sums and slices.  Used to validate the layouts
+    and kernels of every rank against the unsharded transform without a
+    process group; nothing here waits on another rank inside a kernel."""
+    import torch
+
+    world = len(ranks)
+    sends = [r.pack(f) for r, f in zip(ranks, f_shards)]
+    n = sends[0].numel() // world
+    total = torch.stack(sends).sum(dim=0)
+    blocks = [total[q * n:(q + 1) * n].clone() for q in range(world)]
+    cols = [r.colfwd(b) for r, b in zip(ranks, blocks)]
+
+    def a2a(bufs):
+        m = bufs[0].numel() // world
+        return [torch.cat([bufs[src][dst * m:(dst + 1) * m] for src in range(world)])
+                for dst in range(world)]
+
+    rows = a2a(cols)
+    rows = [r.rowmul(x) for r, x in zip(ranks, rows)]
+    cols2 = a2a(rows)
+    hblks = [r.colinv(x) for r, x in zip(ranks, cols2)]
+    hall = torch.cat(hblks)
+    return [r.gather(hall) for r in ranks]

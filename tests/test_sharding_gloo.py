@@ -72,3 +72,41 @@ def test_shard_range_covers_exactly():
             pieces = [shard_range(n, world, r) for r in range(world)]
             assert pieces[0][0] == 0 and pieces[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(pieces, pieces[1:]))
+
+
+def _coll_worker(rank, world, port, result_dir):
+    """TorchCollectives over gloo (CPU): the three collectives of the
+    distributed FFT must match their definitions (and run_ranks_in_process's
+    in-process emulation, which the GPU test checks against the unsharded
+    transform)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2107_02671_b200.sharding import TorchCollectives
+
+        c = TorchCollectives()
+        n = 5
+
+        def buf(r, salt):  # rank r's send buffer, world blocks of n
+            k = torch.arange(world * n, dtype=torch.float64)
+            return torch.complex(k + 100 * r + salt, -k * (r + 1) - salt)
+
+        rs = c.reduce_scatter(buf(rank, 0.5))
+        want = sum(buf(r, 0.5) for r in range(world))[rank * n:(rank + 1) * n]
+        assert torch.equal(rs, want)
+        a2a = c.all_to_all(buf(rank, 1.0))
+        want = torch.cat([buf(src, 1.0)[rank * n:(rank + 1) * n] for src in range(world)])
+        assert torch.equal(a2a, want)
+        ag = c.all_gather(buf(rank, 2.0)[:n])
+        want = torch.cat([buf(r, 2.0)[:n] for r in range(world)])
+        assert torch.equal(ag, want)
+        np.save(os.path.join(result_dir, f"ok{rank}.npy"), np.array([1]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_distributed_fft_collectives_gloo(tmp_path, world):
+    mp.spawn(_coll_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    assert all((tmp_path / f"ok{r}.npy").exists() for r in range(world))
