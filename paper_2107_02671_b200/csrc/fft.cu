@@ -1286,10 +1286,17 @@ int log2i(int x) {
 void build_direct(NnfftPlanImpl& p, cudaStream_t s) {
   DirectFft& d = p.fft.d;
   const Geometry& g = p.g;
-  d.C_log2 = log2i(d.C);
   const int n2len = (int)(d.p_smooth ? d.P : d.LP);
   d.R = 1;
   while (2 * d.R * n2len <= kDirectSmem && d.R < 64) d.R *= 2;
+  // these lengths are launch/latency bound (N2 ~ 16K at configs 2 and 5):
+  // fewer columns/rows per CTA until the grids cover the SMs
+  const int64_t want = 2 * (int64_t)p.sp.n_sms;
+  while (d.R > 1 && ceil_div(d.A, (int64_t)d.R) < want) d.R >>= 1;
+  while (d.C > 2 && ceil_div(d.P, (int64_t)d.C) < want) d.C >>= 1;
+  if (const char* e = getenv("SFB_DIRECT_R")) d.R = std::max(1, atoi(e));
+  if (const char* e = getenv("SFB_DIRECT_C")) d.C = std::max(2, atoi(e));
+  d.C_log2 = log2i(d.C);
   d.R_log2 = log2i(d.R);
   d.stA = make_stages(d.A);
   d.stP = make_stages(n2len);
