@@ -227,6 +227,50 @@ __global__ void __launch_bounds__(kSpreadWarps * 32, 2) k_spread(SpreadArgs a, W
   flush_tile<M>(a, S, tile, col, lane);
 }
 
+// Small inputs (a few hundred blocks: configs 1 and 2, the 16,385 Chebyshev
+// sources of fast-sinc stage 3): the persistent pipeline leaves most SMs idle
+// and each warp pays its full load-latency chain for one block.  Here one
+// thread per source slot evaluates its 2m taps and adds them to the grid with
+// fp64 REDs (L2-resident grid; contention only at the densest cells).
+template <int M, bool REAL>
+__global__ void __launch_bounds__(256) k_spread_small(SpreadArgs a, WinCoef C) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // slot
+  const int col = blockIdx.y;
+  if (s >= a.n_blocks * kBlockChunks * kChunk) return;
+  const int64_t ci = s / kChunk;
+  const int info = __ldg(a.info + ci);
+  if ((int)(s % kChunk) >= (info & 255)) return;
+  const int lcell = info >> 8;
+  const int tile = __ldg(a.blk_tile + ci / kBlockChunks);
+  const double pos = __ldg(a.pos + s);
+  const int src = __ldg(a.perm + s);
+  double2 fv;
+  if (REAL) fv = make_double2(__ldg(static_cast<const double*>(a.f) + src), 0.0);
+  else fv = __ldg(static_cast<const double2*>(a.f) + (int64_t)src * a.batch + col);
+  double2 r[2 * M];
+#pragma unroll
+  for (int k = 0; k < 2 * M; ++k) r[k] = make_double2(0.0, 0.0);
+  window_accumulate<M, REAL>(C, pos - floor(pos), fv, r);
+  double2* grid = a.grid + (int64_t)col * a.K;
+  const int64_t base = (int64_t)tile * kTile - (M - 1) + lcell;  // as flush_tile
+#pragma unroll
+  for (int k = 0; k < 2 * M; ++k) {
+    const int64_t gi = base + k;
+    if (gi >= 0 && gi < a.K) {
+      atomicAdd(&grid[gi].x, r[k].x);
+      if (!REAL) atomicAdd(&grid[gi].y, r[k].y);
+    }
+  }
+}
+
+static int64_t small_spread_blocks() {
+  static const int64_t v = [] {
+    const char* e = getenv("SFB_SPREAD_SMALL_MAX");
+    return e ? (int64_t)atoll(e) : (int64_t)512;
+  }();
+  return v;
+}
+
 template <int M, bool REAL>
 static void launch_spread_m(const NnfftPlanImpl& p, const void* f, double2* grid, int batch,
                             cudaStream_t s) {
@@ -241,6 +285,13 @@ static void launch_spread_m(const NnfftPlanImpl& p, const void* f, double2* grid
   }
   SpreadArgs a{p.sp.pos.p, p.sp.perm.p, p.sp.info.p, p.sp.blk_tile.p, p.sp.wstart.p, f, grid,
                p.g.K, p.sp.n_blocks, batch};
+  if (p.sp.n_blocks <= small_spread_blocks()) {
+    const int64_t slots = p.sp.n_blocks * kBlockChunks * kChunk;
+    k_spread_small<M, REAL><<<dim3((unsigned)ceil_div(slots, (int64_t)256), batch), 256, 0, s>>>(
+        a, p.c1);
+    SF_LAUNCH_CHECK();
+    return;
+  }
   // persistent: n_ctas = min(2 per SM, blocks / 32) CTAs, warp ranges from the plan
   k_spread<M, REAL><<<dim3((unsigned)p.sp.n_ctas, batch), kSpreadWarps * 32, smem, s>>>(a, p.c1);
   SF_LAUNCH_CHECK();
