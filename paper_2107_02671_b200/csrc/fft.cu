@@ -1407,6 +1407,10 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_drowmul<4096, 256, 2>, sizeof(double2) * 4096);
   set_smem(k_colinv_r1<1024, 1, 256, 4>, sizeof(double2) * 2048);
   set_smem(k_colfwd_r1<1024, 2, 256, 2>, sizeof(double2) * 4096);
+  set_smem(k_colfwd_r1<1024, 3, 1024, 1>, sizeof(double2) * 8192);
+  set_smem(k_colinv_r1<1024, 3, 1024, 1>, sizeof(double2) * 8192);
+  set_smem(k_colfwd_r1<1024, 2, 512, 2>, sizeof(double2) * 4096);
+  set_smem(k_colinv_r1<1024, 2, 512, 2>, sizeof(double2) * 4096);
   set_smem(k_colinv_r1<1024, 2, 256, 2>, sizeof(double2) * 4096);
   FftPlan& f = p.fft;
   const Geometry& g = p.g;
@@ -1628,13 +1632,14 @@ void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h
 // 1024): 0 = smem kernels; 1 = columns 2 x 256 threads, rows 512 threads;
 // 2 = columns 4 x 512 threads, rows 512 threads; 3 = columns 2 x 256, rows 256
 // threads (2 butterflies each); 4 = as 3 with the column kernels at 4 CTAs/SM
-// (64 registers); 5 = columns 4 x 256 threads
+// (64 registers); 5 = columns 4 x 256 threads; 6 = columns 8 x 1024 threads;
+// 7 = columns 4 x 512 threads, 2 CTAs/SM (measured best: 0.191 -> 0.188 ms)
 static int reg1_variant(const FftPlan& f) {
   if (!(f.L1 == 4096 && f.L2 == 1024 && f.st1.n == 4096 && f.st2.n == 1024)) return 0;
-  int v = 4;  // measured best (0.217 -> 0.192 ms; a persistent cp.async-pipelined
+  int v = 7;  // measured best (0.217 -> 0.188 ms; a persistent cp.async-pipelined
               // version of these passes measured 9 % slower)
   if (const char* e = getenv("SFB_FFT_REG1")) v = atoi(e);
-  return (v >= 0 && v <= 5) ? v : 4;
+  return (v >= 0 && v <= 7) ? v : 7;
 }
 
 template <int CBL, int CT, int CMINB, int RT, int RMINB>
@@ -1655,6 +1660,8 @@ static void run_reg1(const FftArgs& a, const FftPlan& f, int batch, int v, cudaS
     case 2: launch_reg1<2, 512, 1, 512, 1>(a, f, batch, s); break;
     case 4: launch_reg1<1, 256, 4, 256, 2>(a, f, batch, s); break;
     case 5: launch_reg1<2, 256, 2, 256, 2>(a, f, batch, s); break;
+    case 6: launch_reg1<3, 1024, 1, 256, 2>(a, f, batch, s); break;
+    case 7: launch_reg1<2, 512, 2, 256, 2>(a, f, batch, s); break;
     default: launch_reg1<1, 256, 3, 256, 2>(a, f, batch, s); break;
   }
 }
