@@ -265,7 +265,14 @@ void build_nnfft(sfb::NnfftPlanImpl& p, int64_t N, int64_t M1, int64_t M2, doubl
 
 bool use_graph(const sfb::NnfftPlanImpl& p, int64_t batch) {
   static const bool off = getenv("SINCFFT_NO_GRAPHS") != nullptr;
-  return !off && (p.g.M1 + p.g.M2) * batch <= ((int64_t)1 << 19);
+  static const int64_t lim = [] {
+    const char* e = getenv("SINCFFT_GRAPH_MAX_NODES");
+    return e ? (int64_t)atoll(e) : ((int64_t)1 << 19);
+  }();
+  // single columns of any size: replaying the captured spread/FFT/gather
+  // sequence saves the inter-launch gaps (config 3: 0.851 -> 0.840 ms); large
+  // batches stay uncaptured (their scratch would be pinned per cached graph)
+  return !off && (batch == 1 || (p.g.M1 + p.g.M2) * batch <= lim);
 }
 
 void launch_graph(sincfft_nnfft_plan plan, const double2* f, double2* out, int64_t batch,
