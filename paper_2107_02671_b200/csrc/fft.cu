@@ -1393,25 +1393,11 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_colfwd_b<512, 3>, smem_bytes(kColElemsB));
   set_smem(k_rowmul_b<512, 3>, smem_bytes(kColElemsB));
   set_smem(k_colinv_b<512, 3>, smem_bytes(kColElemsB));
-  set_reg_smem<3, 256, 2>();
-  set_reg_smem<2, 256, 3>();
   set_reg_smem<2, 256, 4>();
-  set_reg_smem<3, 512, 1>();
-  set_smem(k_colfwd_r1<1024, 1, 256, 3>, sizeof(double2) * 2048);
-  set_smem(k_colinv_r1<1024, 1, 256, 3>, sizeof(double2) * 2048);
-  set_smem(k_colfwd_r1<1024, 2, 512, 1>, sizeof(double2) * 4096);
-  set_smem(k_colinv_r1<1024, 2, 512, 1>, sizeof(double2) * 4096);
-  set_smem(k_rowmul_r1<4096, 512, 1>, sizeof(double2) * 4096);
-  set_smem(k_rowmul_r1<4096, 256, 2>, sizeof(double2) * 4096);
-  set_smem(k_colfwd_r1<1024, 1, 256, 4>, sizeof(double2) * 2048);
-  set_smem(k_drowmul<4096, 256, 2>, sizeof(double2) * 4096);
-  set_smem(k_colinv_r1<1024, 1, 256, 4>, sizeof(double2) * 2048);
-  set_smem(k_colfwd_r1<1024, 2, 256, 2>, sizeof(double2) * 4096);
-  set_smem(k_colfwd_r1<1024, 3, 1024, 1>, sizeof(double2) * 8192);
-  set_smem(k_colinv_r1<1024, 3, 1024, 1>, sizeof(double2) * 8192);
   set_smem(k_colfwd_r1<1024, 2, 512, 2>, sizeof(double2) * 4096);
   set_smem(k_colinv_r1<1024, 2, 512, 2>, sizeof(double2) * 4096);
-  set_smem(k_colinv_r1<1024, 2, 256, 2>, sizeof(double2) * 4096);
+  set_smem(k_rowmul_r1<4096, 256, 2>, sizeof(double2) * 4096);
+  set_smem(k_drowmul<4096, 256, 2>, sizeof(double2) * 4096);
   FftPlan& f = p.fft;
   const Geometry& g = p.g;
   const int64_t Lmin = g.K + f.Kout - 1;
@@ -1543,24 +1529,21 @@ bool fft_supports_point_major(const NnfftPlanImpl& p) {
   return !p.fft.direct && !p.fft.single;
 }
 
-// Columns are transformed in groups of G: the group's work array Y (L x G
-// complex) stays L2-resident across the three passes, so only the grid reads
-// and the h writes go to DRAM (all 256 columns at once: 3 x 2 x 1.1 GB).
-// register-resident kernel variant for this plan's point-major shape: 0 = none
-// (smem kernels); 1 = 8 columns x 256 threads (2 butterflies per thread);
-// 2 = 4 columns x 256 threads, 3 CTAs/SM; 3 = 8 columns x 512 threads;
-// 4 = as 2 with 4 CTAs/SM (64 registers)
-static int reg_variant(const FftPlan& f) {
-  if (!(f.L1 == 512 && f.L2 == 512 && f.st1.n == 512 && f.st2.n == 512)) return 0;
-  int v = 4;  // measured best (config 4 FFT 2.20 -> 1.77 ms)
-  if (const char* e = getenv("SFB_FFT_REG")) v = atoi(e);
-  return (v >= 0 && v <= 4) ? v : 4;
+// Register-resident passes for this plan's point-major shape (512 x 512,
+// config 4): 4 columns x 256 threads, 64 registers, 4 CTAs/SM.  Measured
+// alternatives: 8 columns x 256 (2 butterflies per thread: spills), 8 x 512,
+// 4 x 256 at 3 CTAs/SM -- 1.89-2.75 ms against 1.77 ms; the shared-memory
+// kernels k_*_b (SFB_FFT_REG=0) 2.20 ms.
+static bool reg_point_major(const FftPlan& f) {
+  if (!(f.L1 == 512 && f.L2 == 512 && f.st1.n == 512 && f.st2.n == 512)) return false;
+  const char* e = getenv("SFB_FFT_REG");
+  return !(e && atoi(e) == 0);
 }
 
-template <int NBL, int T, int MINB>
-static void launch_reg(const FftBArgs& x, int64_t L1, int64_t L2, cudaStream_t s) {
+static void launch_reg_point_major(const FftBArgs& x, int64_t L1, int64_t L2, cudaStream_t s) {
+  constexpr int NBL = 2, T = 256, MINB = 4;
   const size_t sm = sizeof(double2) * ((size_t)512 << NBL);
-  const dim3 gc((unsigned)ceil_div(x.B, 1 << NBL), (unsigned)L1);
+  const dim3 gc((unsigned)ceil_div(x.B, 1 << NBL), (unsigned)L1);  // column groups fastest
   const dim3 gr((unsigned)ceil_div(x.B, 1 << NBL), (unsigned)L2);
   k_colfwd_rb<512, NBL, T, MINB><<<gc, T, sm, s>>>(x);
   SF_LAUNCH_CHECK();
@@ -1570,15 +1553,9 @@ static void launch_reg(const FftBArgs& x, int64_t L1, int64_t L2, cudaStream_t s
   SF_LAUNCH_CHECK();
 }
 
-static void run_reg_point_major(const FftBArgs& x, int64_t L1, int64_t L2, int v, cudaStream_t s) {
-  switch (v) {
-    case 1: launch_reg<3, 256, 2>(x, L1, L2, s); break;
-    case 2: launch_reg<2, 256, 3>(x, L1, L2, s); break;
-    case 4: launch_reg<2, 256, 4>(x, L1, L2, s); break;
-    default: launch_reg<3, 512, 1>(x, L1, L2, s); break;
-  }
-}
-
+// Columns can be transformed in groups of G (SFB_FFT_GROUP): the group's work array Y (L x G
+// complex) stays L2-resident across the three passes, so only the grid reads
+// and the h writes go to DRAM (all 256 columns at once: 3 x 2 x 1.1 GB).
 int fft_point_major_group(int batch) {
   int G = 0;  // all columns at once (16-64 column groups measured 7-48 % slower)
   if (const char* e = getenv("SFB_FFT_GROUP")) G = atoi(e);
@@ -1594,7 +1571,7 @@ void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h
   while (cc > 1 && cc * f.L2 > kColElemsB) cc >>= 1;
   while (cr > 1 && cr * f.L1 > kColElemsB) cr >>= 1;
   const size_t smc = smem_bytes(f.L2 * cc), smr = smem_bytes(f.L1 * cr);
-  const int reg = reg_variant(f);
+  const bool reg = reg_point_major(f);
   for (int b0 = 0; b0 < batch; b0 += G) {
     FftBArgs x{};
     x.a = make_args(p);
@@ -1609,7 +1586,7 @@ void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h
     const dim3 gc((unsigned)f.L1, (unsigned)ceil_div(x.B, cc));
     const dim3 gr((unsigned)f.L2, (unsigned)ceil_div(x.B, cr));
     if (reg) {  // register-resident passes (512 x 512, the config-4 shape)
-      run_reg_point_major(x, f.L1, f.L2, reg, s);
+      launch_reg_point_major(x, f.L1, f.L2, s);
       continue;
     }
     // compile-time specialisation of the config-4 shape (512 x 512, 8 columns)
@@ -1628,22 +1605,21 @@ void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h
   launch_fix(p, grid, h, batch, 1, s);
 }
 
-// register-resident single-column passes for the config-3 shape (4096 x
-// 1024): 0 = smem kernels; 1 = columns 2 x 256 threads, rows 512 threads;
-// 2 = columns 4 x 512 threads, rows 512 threads; 3 = columns 2 x 256, rows 256
-// threads (2 butterflies each); 4 = as 3 with the column kernels at 4 CTAs/SM
-// (64 registers); 5 = columns 4 x 256 threads; 6 = columns 8 x 1024 threads;
-// 7 = columns 4 x 512 threads, 2 CTAs/SM (measured best: 0.191 -> 0.188 ms)
-static int reg1_variant(const FftPlan& f) {
-  if (!(f.L1 == 4096 && f.L2 == 1024 && f.st1.n == 4096 && f.st2.n == 1024)) return 0;
-  int v = 7;  // measured best (0.217 -> 0.188 ms; a persistent cp.async-pipelined
-              // version of these passes measured 9 % slower)
-  if (const char* e = getenv("SFB_FFT_REG1")) v = atoi(e);
-  return (v >= 0 && v <= 7) ? v : 7;
+// Register-resident single-column passes for the config-3 shape (4096 x
+// 1024): columns 4 x 512 threads (2 CTAs/SM), rows 256 threads with 2
+// butterflies each.  Measured alternatives (FFT per step): shared-memory
+// kernels (SFB_FFT_REG1=0) 0.217 ms; columns 2 x 256 with rows of 512 threads
+// 0.214; columns 4 x 512 with rows of 512 0.238; columns 2 x 256 at 3 or 4
+// CTAs/SM 0.199 / 0.192; columns 4 x 256 0.219; columns 8 x 1024 0.206; this
+// one 0.188 ms.  A persistent cp.async-pipelined version measured 9 % slower.
+static bool reg_single(const FftPlan& f) {
+  if (!(f.L1 == 4096 && f.L2 == 1024 && f.st1.n == 4096 && f.st2.n == 1024)) return false;
+  const char* e = getenv("SFB_FFT_REG1");
+  return !(e && atoi(e) == 0);
 }
 
-template <int CBL, int CT, int CMINB, int RT, int RMINB>
-static void launch_reg1(const FftArgs& a, const FftPlan& f, int batch, cudaStream_t s) {
+static void launch_reg_single(const FftArgs& a, const FftPlan& f, int batch, cudaStream_t s) {
+  constexpr int CBL = 2, CT = 512, CMINB = 2, RT = 256, RMINB = 2;
   const size_t smc = sizeof(double2) * ((size_t)1024 << CBL), smr = sizeof(double2) * 4096;
   const dim3 gc((unsigned)ceil_div(f.L1, (int64_t)1 << CBL), batch);
   k_colfwd_r1<1024, CBL, CT, CMINB><<<gc, CT, smc, s>>>(a);
@@ -1652,18 +1628,6 @@ static void launch_reg1(const FftArgs& a, const FftPlan& f, int batch, cudaStrea
   SF_LAUNCH_CHECK();
   k_colinv_r1<1024, CBL, CT, CMINB><<<gc, CT, smc, s>>>(a);
   SF_LAUNCH_CHECK();
-}
-
-static void run_reg1(const FftArgs& a, const FftPlan& f, int batch, int v, cudaStream_t s) {
-  switch (v) {
-    case 1: launch_reg1<1, 256, 3, 512, 1>(a, f, batch, s); break;
-    case 2: launch_reg1<2, 512, 1, 512, 1>(a, f, batch, s); break;
-    case 4: launch_reg1<1, 256, 4, 256, 2>(a, f, batch, s); break;
-    case 5: launch_reg1<2, 256, 2, 256, 2>(a, f, batch, s); break;
-    case 6: launch_reg1<3, 1024, 1, 256, 2>(a, f, batch, s); break;
-    case 7: launch_reg1<2, 512, 2, 256, 2>(a, f, batch, s); break;
-    default: launch_reg1<1, 256, 3, 256, 2>(a, f, batch, s); break;
-  }
 }
 
 void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work, int batch,
@@ -1692,8 +1656,8 @@ void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* w
     SF_LAUNCH_CHECK();
     return;
   }
-  if (reg1_variant(f)) {
-    run_reg1(a, f, batch, reg1_variant(f), s);
+  if (reg_single(f)) {
+    launch_reg_single(a, f, batch, s);
     launch_fix(p, grid, h, batch, 0, s);
     return;
   }
