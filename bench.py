@@ -327,9 +327,14 @@ def run_b200(args, cfg):
                          h_window="full" if want_dist else "data")
     dist_fft = None
     if want_dist:
-        from paper_2107_02671_b200.sharding import DistributedFftNnfft, dist_layout
+        from paper_2107_02671_b200.sharding import (DistributedFftNnfft,
+                                                    SparseDistributedFftNnfft, dist_layout)
         if dist_layout(plan, world) is not None:
-            dist_fft = DistributedFftNnfft(plan)
+            # position partitions: exchange only the grid / h rows each rank
+            # touches (sparse) unless --dense-exchange asks for the
+            # reduce-scatter / all-gather form
+            dist_fft = (DistributedFftNnfft(plan) if args.dense_exchange
+                        else SparseDistributedFftNnfft(plan))
     torch.cuda.synchronize()
     plan_ms = (time.perf_counter() - tp) * 1e3
     geo = plan.backend_geometry
@@ -550,7 +555,8 @@ def run_b200(args, cfg):
     launches = L.sincfft_nnfft_launches_per_execute(ph, B) * args.steps
     if dist_fft is not None:  # grid memset + spread, pack (+ tail fix), 3 passes
         fix = 1 if geo["L"] < geo["K"] + geo["Kout"] - 1 else 0  # (+ rank-0 fix add), unpack, gather
-        launches = (2 + 1 + fix + 3 + (fix if rank == 0 else 0) + 1 + 1) * args.steps
+        launches = (2 + 1 + fix + 3 + (fix if rank == 0 else 0) + 1 + 1
+                    + (0 if args.dense_exchange else 2)) * args.steps  # + unpack_rows, pack_hrows
     fp64_peak, fp64_note = 148 * 64 * 2 * (clk.max_mhz or 1965) * 1e6 / 1e12, \
         "derived: 148 SMs x 64 DFMA/clk x 2 flops x max SM clock"
     pf = os.path.join(ROOT, "profiles", "fp64_peak.json")
@@ -577,7 +583,10 @@ def run_b200(args, cfg):
                        "(f and out 256 MiB each per column vs 126 MB L2)",
                        "parallelism": f"sources+targets sharded x{world}" +
                        (" by position (quantiles of v and x)" if world > 1 else "") +
-                       (("; distributed FFT: reduce-scatter + 2 all-to-all + all-gather"
+                       (("; distributed FFT: " + ("reduce-scatter + 2 all-to-all + all-gather"
+                                                   if args.dense_exchange else
+                                                   "4 all-to-alls (grid / h rows exchanged "
+                                                   "sparsely)")
                          if dist_fft is not None else ", NCCL all-reduce of the K-grid")
                         if world > 1 else "")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
@@ -630,6 +639,9 @@ def main():
     ap.add_argument("--replicated-fft", action="store_true",
                     help="N > 1: all-reduce the K-grid and replicate the FFT (the "
                          "north star's baseline partitioning) instead of splitting it")
+    ap.add_argument("--dense-exchange", action="store_true",
+                    help="N > 1 distributed FFT: reduce-scatter / all-gather the whole "
+                         "K-grid and h instead of all-to-alls of the rows each rank touches")
     ap.add_argument("--check-shards", action="store_true",
                     help="N > 1: compare this rank's output shard with a single-rank "
                          "transform of the same inputs and report the max deviation")

@@ -157,6 +157,39 @@ SINCFFT_API int sincfft_nnfft_dist_colinv(sincfft_nnfft_plan plan, int32_t world
 SINCFFT_API int sincfft_nnfft_dist_gather(sincfft_nnfft_plan plan, int32_t world,
                                           const double *hall_dev, double *out_dev, void *stream);
 
+/* Sparse exchange variant of the distributed FFT for POSITION partitions
+ * (each rank's sources cover a contiguous grid range, its targets a
+ * contiguous h range): the reduce-scatter and the all-gather above become
+ * all-to-alls of only the rows a rank touches.  grid row i = grid indices
+ * [i L1, (i+1) L1), h row k2 = h indices [k2 L1, (k2+1) L1).
+ *   dist_support(out4)   -> [n_lo, n_hi] grid indices spread, [k_lo, k_hi] h
+ *                           indices gathered by this plan (host values)
+ *   dist_pack_rows(grid, ilo, nrow) -> send: world chunks, chunk q = rows
+ *                           [ilo, ilo + nrow) of column block q ([i][c]);
+ *                           chunk 0 carries Dpad = ceil8(D) more elements (this
+ *                           rank's Bluestein tail fix)         ; all-to-all(v)
+ *   dist_unpack_rows(recv, ilo[world], nrow[world]) -> block[Sb] (rows of
+ *                           every sender summed; rank 0 also sums the fixes)
+ *   ... dist_colfwd / all-to-all / dist_rowmul / all-to-all / dist_colinv ...
+ *   dist_pack_hrows(hblk, k2lo[world], cnt[world]) -> send: chunk r = rows
+ *                           [k2lo_r, k2lo_r + cnt_r) of this rank's h block
+ *                                                              ; all-to-all(v)
+ *   dist_gather_rows(recv, k2lo, cnt) -> out[M2] (own h rows, then the gather) */
+SINCFFT_API int sincfft_nnfft_dist_support(sincfft_nnfft_plan plan, int64_t *out4, void *stream);
+SINCFFT_API int sincfft_nnfft_dist_pack_rows(sincfft_nnfft_plan plan, int32_t world,
+                                             const double *grid_dev, int64_t ilo, int64_t nrow,
+                                             double *send_dev, void *stream);
+SINCFFT_API int sincfft_nnfft_dist_unpack_rows(sincfft_nnfft_plan plan, int32_t world,
+                                               int32_t rank, const double *recv_dev,
+                                               const int64_t *ilo, const int64_t *nrow,
+                                               double *block_dev, void *stream);
+SINCFFT_API int sincfft_nnfft_dist_pack_hrows(sincfft_nnfft_plan plan, int32_t world,
+                                              const double *hblk_dev, const int64_t *k2lo,
+                                              const int64_t *cnt, double *send_dev, void *stream);
+SINCFFT_API int sincfft_nnfft_dist_gather_rows(sincfft_nnfft_plan plan, int32_t world,
+                                               const double *recv_dev, int64_t k2lo, int64_t cnt,
+                                               double *out_dev, void *stream);
+
 /* Observability: one execute with DEVICE pointers and CUDA events recorded
  * on `stream` between the stages; returns after synchronizing the stream
  * with stage_ms[0..3] = spread (incl. grid zeroing), FFT (deconvolution +

@@ -65,6 +65,14 @@ SIGNATURES = {
     "sincfft_nnfft_dist_rowmul": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp]),
     "sincfft_nnfft_dist_colinv": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]),
     "sincfft_nnfft_dist_gather": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp]),
+    "sincfft_nnfft_dist_support": (C.c_int, [_vp, _i64p, _vp]),
+    "sincfft_nnfft_dist_pack_rows": (C.c_int, [_vp, C.c_int32, _vp, C.c_int64, C.c_int64, _vp,
+                                               _vp]),
+    "sincfft_nnfft_dist_unpack_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _i64p, _i64p,
+                                                 _vp, _vp]),
+    "sincfft_nnfft_dist_pack_hrows": (C.c_int, [_vp, C.c_int32, _vp, _i64p, _i64p, _vp, _vp]),
+    "sincfft_nnfft_dist_gather_rows": (C.c_int, [_vp, C.c_int32, _vp, C.c_int64, C.c_int64, _vp,
+                                                 _vp]),
     "sincfft_nnfft_plan_geometry": (C.c_int, [_vp, C.POINTER(Geometry)]),
     "sincfft_nnfft_execute": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, _vp]),
     "sincfft_nnfft_spread": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, _vp]),

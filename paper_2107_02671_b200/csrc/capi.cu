@@ -526,6 +526,51 @@ int sincfft_nnfft_dist_gather(sincfft_nnfft_plan plan, int32_t world, const doub
   });
 }
 
+int sincfft_nnfft_dist_support(sincfft_nnfft_plan plan, int64_t* out4, void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!out4);
+    sfb::dist_support(p, s, out4);
+  });
+}
+
+int sincfft_nnfft_dist_pack_rows(sincfft_nnfft_plan plan, int32_t world, const double* grid_dev,
+                                 int64_t ilo, int64_t nrow, double* send_dev, void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!grid_dev || !send_dev);
+    sfb::run_dist_pack_rows(p, world, (const double2*)grid_dev, ilo, nrow, (double2*)send_dev, s);
+  });
+}
+
+int sincfft_nnfft_dist_unpack_rows(sincfft_nnfft_plan plan, int32_t world, int32_t rank,
+                                   const double* recv_dev, const int64_t* ilo,
+                                   const int64_t* nrow, double* block_dev, void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!recv_dev || !ilo || !nrow || !block_dev);
+    sfb::run_dist_unpack_rows(p, world, rank, (const double2*)recv_dev, ilo, nrow,
+                              (double2*)block_dev, s);
+  });
+}
+
+int sincfft_nnfft_dist_pack_hrows(sincfft_nnfft_plan plan, int32_t world, const double* hblk_dev,
+                                  const int64_t* k2lo, const int64_t* cnt, double* send_dev,
+                                  void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!hblk_dev || !k2lo || !cnt || !send_dev);
+    sfb::run_dist_pack_hrows(p, world, (const double2*)hblk_dev, k2lo, cnt, (double2*)send_dev,
+                             s);
+  });
+}
+
+int sincfft_nnfft_dist_gather_rows(sincfft_nnfft_plan plan, int32_t world, const double* recv_dev,
+                                   int64_t k2lo, int64_t cnt, double* out_dev, void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!recv_dev || !out_dev);
+    sfb::Scratch h(sizeof(double2) * (size_t)p.fft.Kout, s);
+    sfb::run_dist_unpack_hrows(p, world, (const double2*)recv_dev, k2lo, cnt, h.as<double2>(), s);
+    sfb::run_gather(p, h.as<double2>(), (double2*)out_dev, 1, s);
+  });
+}
+
 int sincfft_nnfft_execute_profiled(sincfft_nnfft_plan plan, const double* f, double* out,
                                    int64_t batch, void* stream, double* stage_ms) {
   return guarded([&] {

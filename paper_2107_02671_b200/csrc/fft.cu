@@ -933,6 +933,83 @@ __global__ void k_dunpack(const double2* __restrict__ Hall, double2* __restrict_
   h[k] = Hall[((q * d.K2 + k2) << d.bc_log2) + c];
 }
 
+// Sparse exchange for position partitions: a rank's partial grid is nonzero
+// only on rows [ilo, ilo + nrow) (row i = grid indices [i L1, (i+1) L1)), and
+// its targets read only h rows [k2lo, k2lo + cnt); so the reduce-scatter and
+// the all-gather become all-to-alls of those rows (per rank ~K/P and
+// ~Kout/P complex instead of K and Kout).  Chunks destined to rank 0 carry
+// the sender's partial tail fix (Dpad extra elements).
+__global__ void k_dpack_rows(const double2* __restrict__ g, double2* __restrict__ S, DistArgs d,
+                             int64_t ilo, int64_t nrow, int64_t dpad) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t seg = nrow * d.Bc;
+  const int64_t total = d.world * seg + dpad;
+  if (o >= total) return;
+  // chunk 0 = [rows of column block 0][fix], then chunks 1.. of seg elements
+  int64_t q, e;
+  if (o < seg + dpad) {
+    q = 0, e = o;
+  } else {
+    q = 1 + (o - seg - dpad) / seg, e = (o - seg - dpad) % seg;
+  }
+  double2 v = make_double2(0.0, 0.0);
+  if (e < seg) {
+    const int64_t i = ilo + (e >> d.bc_log2), c = e & (d.Bc - 1);
+    const int64_t n = q * d.Bc + c + d.a.L1 * i;
+    if (n < d.a.K) v = g[n];
+  }
+  S[o] = v;
+}
+
+__global__ void k_dunpack_rows(const double2* __restrict__ recv, double2* __restrict__ R,
+                               DistArgs d, RowSplit rs, int64_t dfix) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nblk = d.I * d.Bc;
+  if (o >= nblk + dfix) return;
+  double2 acc = make_double2(0.0, 0.0);
+  if (o < nblk) {
+    const int64_t i = o >> d.bc_log2, c = o & (d.Bc - 1);
+    for (int s = 0; s < rs.n; ++s) {
+      const int64_t li = i - rs.lo[s];
+      if (li >= 0 && li < rs.cnt[s]) {
+        const double2 v = recv[rs.off[s] + (li << d.bc_log2) + c];
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+    }
+  } else {  // rank 0: the senders' tail-fix partials follow their rows
+    const int64_t k = o - nblk;
+    for (int s = 0; s < rs.n; ++s) {
+      const double2 v = recv[rs.off[s] + (rs.cnt[s] << d.bc_log2) + k];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+  }
+  R[o] = acc;
+}
+
+__global__ void k_dpack_hrows(const double2* __restrict__ H, double2* __restrict__ S, DistArgs d,
+                              RowSplit rs, int64_t total) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= total) return;
+  int r = 0;
+  while (r + 1 < rs.n && o >= rs.off[r + 1]) ++r;
+  const int64_t e = o - rs.off[r];
+  const int64_t k2 = rs.lo[r] + (e >> d.bc_log2), c = e & (d.Bc - 1);
+  S[o] = k2 < d.K2 ? H[(k2 << d.bc_log2) + c] : make_double2(0.0, 0.0);
+}
+
+__global__ void k_dunpack_hrows(const double2* __restrict__ recv, double2* __restrict__ h,
+                                DistArgs d, int64_t k2lo, int64_t cnt) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t seg = cnt * d.Bc;
+  if (o >= d.world * seg) return;
+  const int64_t q = o / seg, e = o - q * seg;
+  const int64_t k2 = k2lo + (e >> d.bc_log2), c = e & (d.Bc - 1);
+  const int64_t k = q * d.Bc + c + d.a.L1 * k2;
+  if (k < d.a.Kout) h[k] = recv[o];
+}
+
 // ------------------------------------------------------ direct four-step
 // n = P n1 + n2 (n1 < A, n2 < P),  k = k1 + A k2:
 //   X[k1 + A k2] = sum_n2 W_P^{n2 k2} [ W_N2^{n2 k1} sum_n1 x[P n1 + n2] W_A^{n1 k1} ]
@@ -1765,6 +1842,72 @@ void run_dist_unpack(const NnfftPlanImpl& p, int world, const double2* Hall, dou
                      cudaStream_t s) {
   const DistArgs d = dist_args(p, world, 0);
   k_dunpack<<<(unsigned)ceil_div(p.fft.Kout, (int64_t)256), 256, 0, s>>>(Hall, h, d);
+  SF_LAUNCH_CHECK();
+}
+
+
+static int64_t dist_dpad(const NnfftPlanImpl& p) { return (p.fft.fixD + 7) / 8 * 8; }
+
+void run_dist_pack_rows(const NnfftPlanImpl& p, int world, const double2* grid, int64_t ilo,
+                        int64_t nrow, double2* send, cudaStream_t s) {
+  const DistArgs d = dist_args(p, world, 0);
+  if (world > kDistMaxRanks) fail(1, "sparse exchange: at most 16 ranks");
+  const int64_t dpad = dist_dpad(p);
+  const int64_t total = world * nrow * d.Bc + dpad;
+  k_dpack_rows<<<(unsigned)ceil_div(total, (int64_t)256), 256, 0, s>>>(grid, send, d, ilo, nrow,
+                                                                    dpad);
+  SF_LAUNCH_CHECK();
+  const FftPlan& f = p.fft;
+  if (f.fixD > 0) {
+    k_bluestein_fix<<<dim3((unsigned)ceil_div(f.fixD * 32, 256), 1), 256, 0, s>>>(
+        grid, f.P.p, f.fixc.p, f.Q.p, send + nrow * d.Bc, p.g.K, f.fixD, f.Kout, 0, 1, 0);
+    SF_LAUNCH_CHECK();
+  }
+}
+
+void run_dist_unpack_rows(const NnfftPlanImpl& p, int world, int rank, const double2* recv,
+                          const int64_t* ilo, const int64_t* nrow, double2* block,
+                          cudaStream_t s) {
+  const DistArgs d = dist_args(p, world, rank);
+  if (world > kDistMaxRanks) fail(1, "sparse exchange: at most 16 ranks");
+  RowSplit rs{};
+  rs.n = world;
+  const int64_t extra = rank == 0 ? dist_dpad(p) : 0;
+  int64_t off = 0;
+  for (int q = 0; q < world; ++q) {
+    rs.lo[q] = ilo[q];
+    rs.cnt[q] = nrow[q];
+    rs.off[q] = off;
+    off += nrow[q] * d.Bc + extra;
+  }
+  const int64_t dfix = rank == 0 ? p.fft.fixD : 0;
+  const int64_t n = d.I * d.Bc + dfix;
+  k_dunpack_rows<<<(unsigned)ceil_div(n, (int64_t)256), 256, 0, s>>>(recv, block, d, rs, dfix);
+  SF_LAUNCH_CHECK();
+}
+
+void run_dist_pack_hrows(const NnfftPlanImpl& p, int world, const double2* hblk,
+                         const int64_t* k2lo, const int64_t* cnt, double2* send, cudaStream_t s) {
+  const DistArgs d = dist_args(p, world, 0);
+  if (world > kDistMaxRanks) fail(1, "sparse exchange: at most 16 ranks");
+  RowSplit rs{};
+  rs.n = world;
+  int64_t off = 0;
+  for (int r = 0; r < world; ++r) {
+    rs.lo[r] = k2lo[r];
+    rs.cnt[r] = cnt[r];
+    rs.off[r] = off;
+    off += cnt[r] * d.Bc;
+  }
+  k_dpack_hrows<<<(unsigned)ceil_div(off, (int64_t)256), 256, 0, s>>>(hblk, send, d, rs, off);
+  SF_LAUNCH_CHECK();
+}
+
+void run_dist_unpack_hrows(const NnfftPlanImpl& p, int world, const double2* recv, int64_t k2lo,
+                           int64_t cnt, double2* h, cudaStream_t s) {
+  const DistArgs d = dist_args(p, world, 0);
+  const int64_t n = world * cnt * d.Bc;
+  k_dunpack_hrows<<<(unsigned)ceil_div(n, (int64_t)256), 256, 0, s>>>(recv, h, d, k2lo, cnt);
   SF_LAUNCH_CHECK();
 }
 

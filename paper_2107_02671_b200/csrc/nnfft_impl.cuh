@@ -196,6 +196,24 @@ struct DistLayout {
   int64_t Sb;      // elements per rank block of the reduce-scatter buffer
 };
 bool dist_layout(const NnfftPlanImpl& p, int world, DistLayout* out);
+// plan.cu: [n_lo, n_hi] grid indices of the plan's spread, [k_lo, k_hi] h
+// indices of its gather (for the sparse exchange of position partitions)
+void dist_support(const NnfftPlanImpl& p, cudaStream_t s, int64_t out[4]);
+// Sparse (position-partitioned) exchange: row ranges per rank
+constexpr int kDistMaxRanks = 16;
+struct RowSplit {
+  int n;
+  int64_t lo[kDistMaxRanks], cnt[kDistMaxRanks], off[kDistMaxRanks];
+};
+void run_dist_pack_rows(const NnfftPlanImpl& p, int world, const double2* grid, int64_t ilo,
+                        int64_t nrow, double2* send, cudaStream_t s);
+void run_dist_unpack_rows(const NnfftPlanImpl& p, int world, int rank, const double2* recv,
+                          const int64_t* ilo, const int64_t* nrow, double2* block,
+                          cudaStream_t s);
+void run_dist_pack_hrows(const NnfftPlanImpl& p, int world, const double2* hblk,
+                         const int64_t* k2lo, const int64_t* cnt, double2* send, cudaStream_t s);
+void run_dist_unpack_hrows(const NnfftPlanImpl& p, int world, const double2* recv, int64_t k2lo,
+                           int64_t cnt, double2* h, cudaStream_t s);
 void run_dist_pack(const NnfftPlanImpl& p, int world, const double2* grid, double2* S,
                    cudaStream_t s);
 void run_dist_colfwd(const NnfftPlanImpl& p, int world, int rank, const double2* R, double2* Yc,

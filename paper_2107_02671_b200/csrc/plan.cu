@@ -623,6 +623,21 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
   SF_CUDA(cudaStreamSynchronize(s));
 }
 
+// Grid indices the spread can touch, [c + K/2 + 1 - m1, c + K/2 + m1] for the
+// cells c = floor(N1 v) of the plan's sources, and h indices k' = s - s_lo the
+// gather reads (one slot of margin each side for the rounding of N1 v).
+void dist_support(const NnfftPlanImpl& p, cudaStream_t s, int64_t out[4]) {
+  const Geometry& g = p.g;
+  double vlo, vhi, plo, phi;
+  device_minmax(p.v_clip.p, g.M1, s, &vlo, &vhi);
+  device_minmax(p.gp.pos.p, g.M2, s, &plo, &phi);
+  const int64_t h = g.K / 2;
+  out[0] = std::max<int64_t>(0, (int64_t)std::floor((double)g.N1 * vlo) + h + 1 - g.m1 - 1);
+  out[1] = std::min<int64_t>(g.K - 1, (int64_t)std::floor((double)g.N1 * vhi) + h + g.m1 + 1);
+  out[2] = std::max<int64_t>(0, (int64_t)std::floor(plo) + 1 - g.m2 - p.fft.s_lo);
+  out[3] = std::min<int64_t>(p.fft.Kout - 1, (int64_t)std::floor(phi) + g.m2 - p.fft.s_lo);
+}
+
 void fuse_target_weights(NnfftPlanImpl& p, const double* w_dev, cudaStream_t s) {
   k_mul_scale<<<blocks(p.g.M2), 256, 0, s>>>(p.gp.scale.p, p.gp.perm.p, w_dev, p.g.M2);
   SF_LAUNCH_CHECK();

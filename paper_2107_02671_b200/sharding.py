@@ -264,3 +264,184 @@ def run_ranks_in_process(ranks, f_shards):
     hblks = [r.colinv(x) for r, x in zip(ranks, cols2)]
     hall = torch.cat(hblks)
     return [r.gather(hall) for r in ranks]
+
+
+# ------------------------------------------- sparse exchange (position partitions)
+def _i64(vals):
+    import ctypes as C
+    return (C.c_int64 * len(vals))(*[int(v) for v in vals])
+
+
+class SparseRows:
+    """Row ranges of every rank for the sparse exchange: grid rows
+    [ilo, ilo + nrow) a rank's spread touches and h rows [k2lo, k2lo + cnt)
+    its gather reads (row = L1 consecutive indices), from each rank's
+    ``sincfft_nnfft_dist_support``."""
+
+    def __init__(self, supports, L1, Dpad, Bc):
+        self.ilo = [s[0] // L1 for s in supports]
+        self.nrow = [s[1] // L1 - s[0] // L1 + 1 for s in supports]
+        self.k2lo = [s[2] // L1 for s in supports]
+        self.cnt = [s[3] // L1 - s[2] // L1 + 1 for s in supports]
+        self.Dpad, self.Bc, self.world = Dpad, Bc, len(supports)
+
+    def grid_send_splits(self, rank):
+        return [self.nrow[rank] * self.Bc + (self.Dpad if q == 0 else 0)
+                for q in range(self.world)]
+
+    def grid_recv_splits(self, rank):
+        return [self.nrow[s] * self.Bc + (self.Dpad if rank == 0 else 0)
+                for s in range(self.world)]
+
+    def h_send_splits(self, rank):
+        return [self.cnt[r] * self.Bc for r in range(self.world)]
+
+    def h_recv_splits(self, rank):
+        return [self.cnt[rank] * self.Bc for _ in range(self.world)]
+
+
+class SparseDistFftRank(DistFftRank):
+    """DistFftRank with the sparse first and last exchanges
+    (``sincfft_nnfft_dist_pack_rows`` / ``_unpack_rows`` / ``_pack_hrows`` /
+    ``_gather_rows``); the middle two all-to-alls are unchanged."""
+
+    def support(self):
+        import ctypes as C
+
+        from . import _lib
+        out = (C.c_int64 * 4)()
+        _lib.check(_lib.lib.sincfft_nnfft_dist_support(self.plan.handle, out, self._s()))
+        return [int(v) for v in out]
+
+    def set_rows(self, rows: SparseRows):
+        self.rows = rows
+
+    def pack_rows(self, f):
+        from . import _lib
+        grid = self._empty(self.geo["K"])
+        _lib.check(_lib.lib.sincfft_nnfft_spread(self.plan.handle, f.data_ptr(), grid.data_ptr(),
+                                                 1, _lib.PTR_DEVICE, self._s()))
+        rw, r = self.rows, self.rank
+        send = self._empty(sum(rw.grid_send_splits(r)))
+        _lib.check(_lib.lib.sincfft_nnfft_dist_pack_rows(self.plan.handle, self.world,
+                                                         grid.data_ptr(), rw.ilo[r], rw.nrow[r],
+                                                         send.data_ptr(), self._s()))
+        return send
+
+    def unpack_rows(self, recv):
+        from . import _lib
+        rw = self.rows
+        block = self._empty(self.layout["Sb"])
+        _lib.check(_lib.lib.sincfft_nnfft_dist_unpack_rows(
+            self.plan.handle, self.world, self.rank, recv.data_ptr(), _i64(rw.ilo),
+            _i64(rw.nrow), block.data_ptr(), self._s()))
+        return block
+
+    def pack_hrows(self, hblk):
+        from . import _lib
+        rw = self.rows
+        send = self._empty(sum(rw.h_send_splits(self.rank)))
+        _lib.check(_lib.lib.sincfft_nnfft_dist_pack_hrows(
+            self.plan.handle, self.world, hblk.data_ptr(), _i64(rw.k2lo), _i64(rw.cnt),
+            send.data_ptr(), self._s()))
+        return send
+
+    def gather_rows(self, recv):
+        from . import _lib
+        rw, r = self.rows, self.rank
+        out = self._empty(self.geo["M2"])
+        _lib.check(_lib.lib.sincfft_nnfft_dist_gather_rows(
+            self.plan.handle, self.world, recv.data_ptr(), rw.k2lo[r], rw.cnt[r],
+            out.data_ptr(), self._s()))
+        return out
+
+
+def sparse_rows_for(ranks_supports, rank0: DistFftRank):
+    geo = rank0.geo
+    L1 = geo["L1"]
+    I = -(-geo["K"] // L1)
+    return SparseRows(ranks_supports, L1, rank0.layout["Sb"] - I * rank0.layout["Bc"],
+                      rank0.layout["Bc"])
+
+
+def _all_to_all_v(coll, send, in_splits, out_splits):
+    import torch
+    import torch.distributed as dist
+    if coll.nccl:
+        out = torch.empty(sum(out_splits), dtype=send.dtype, device=send.device)
+        dist.all_to_all_single(torch.view_as_real(out), torch.view_as_real(send),
+                               output_split_sizes=out_splits, input_split_sizes=in_splits,
+                               group=coll.group)
+        return out
+    # other backends: pad to the longest send buffer, all-gather, pick chunks
+    n = torch.tensor([send.numel()], dtype=torch.int64)
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(coll.world)]
+    dist.all_gather(sizes, n, group=coll.group)
+    width = int(max(s.item() for s in sizes))
+    splits = torch.tensor(in_splits, dtype=torch.int64)
+    all_splits = [torch.zeros_like(splits) for _ in range(coll.world)]
+    dist.all_gather(all_splits, splits, group=coll.group)
+    buf = torch.zeros((width, 2), dtype=torch.float64)
+    buf[:send.numel()] = torch.view_as_real(send).cpu()
+    full = [torch.empty_like(buf) for _ in range(coll.world)]
+    dist.all_gather(full, buf, group=coll.group)
+    parts = []
+    for s in range(coll.world):
+        off = int(all_splits[s][:coll.rank].sum())
+        parts.append(torch.view_as_complex(full[s][off:off + out_splits[s]].contiguous()))
+    return torch.cat(parts).to(send.device)
+
+
+class SparseDistributedFftNnfft:
+    """DistributedFftNnfft for position partitions: the K-grid and h exchanges
+    move only the rows each rank touches (per rank ~(K + Kout)/P complex
+    instead of K + Kout); plans built with ``h_window="full"``."""
+
+    def __init__(self, plan, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.coll = TorchCollectives(group)
+        self.r = SparseDistFftRank(plan, self.coll.world, self.coll.rank)
+        mine = torch.tensor(self.r.support(), dtype=torch.int64,
+                            device=self.r.dev if self.coll.nccl else "cpu")
+        allsup = [torch.zeros_like(mine) for _ in range(self.coll.world)]
+        dist.all_gather(allsup, mine, group=group)
+        self.r.set_rows(sparse_rows_for([a.tolist() for a in allsup], self.r))
+
+    def __call__(self, f_shard):
+        r, c, rw, k = self.r, self.coll, self.r.rows, self.coll.rank
+        recv = _all_to_all_v(c, r.pack_rows(f_shard), rw.grid_send_splits(k),
+                             rw.grid_recv_splits(k))
+        rows = c.all_to_all(r.colfwd(r.unpack_rows(recv)))
+        hblk = r.colinv(c.all_to_all(r.rowmul(rows)))
+        recv2 = _all_to_all_v(c, r.pack_hrows(hblk), rw.h_send_splits(k), rw.h_recv_splits(k))
+        return r.gather_rows(recv2)
+
+
+def run_sparse_ranks_in_process(ranks, f_shards):
+    """run_ranks_in_process for SparseDistFftRank (one process, one GPU)."""
+    import torch
+
+    world = len(ranks)
+    rows = sparse_rows_for([r.support() for r in ranks], ranks[0])
+    for r in ranks:
+        r.set_rows(rows)
+
+    def a2av(sends, send_splits):
+        chunks = [list(torch.split(s, send_splits(i))) for i, s in enumerate(sends)]
+        return [torch.cat([chunks[src][dst] for src in range(world)]) for dst in range(world)]
+
+    recv = a2av([r.pack_rows(f) for r, f in zip(ranks, f_shards)], rows.grid_send_splits)
+    blocks = [r.unpack_rows(x) for r, x in zip(ranks, recv)]
+    cols = [r.colfwd(b) for r, b in zip(ranks, blocks)]
+
+    def a2a(bufs):
+        m = bufs[0].numel() // world
+        return [torch.cat([bufs[src][dst * m:(dst + 1) * m] for src in range(world)])
+                for dst in range(world)]
+
+    rws = [r.rowmul(x) for r, x in zip(ranks, a2a(cols))]
+    hblks = [r.colinv(x) for r, x in zip(ranks, a2a(rws))]
+    recv2 = a2av([r.pack_hrows(h) for r, h in zip(ranks, hblks)], rows.h_send_splits)
+    return [r.gather_rows(x) for r, x in zip(ranks, recv2)]
