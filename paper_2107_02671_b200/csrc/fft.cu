@@ -64,6 +64,32 @@ __device__ __forceinline__ double2 wbig(const double2* __restrict__ lo,
 }
 
 // ------------------------------------------------------------ table kernels
+// inverse of revr: the position holding frequency k after the DIF of length N
+template <int N, int R>
+__device__ __forceinline__ int posr(int k) {
+  using Sh = RegShape<N, R>;
+  int p = 0;
+#pragma unroll
+  for (int q = 0; q < Sh::A; ++q)
+    p |= ((k >> (Sh::LOGR * q)) & (R - 1)) << (Sh::LOG2N - Sh::LOGR * (q + 1));
+  if (Sh::R0 > 1) p |= (k >> (Sh::LOGR * Sh::A)) & (Sh::R0 - 1);
+  return p;
+}
+
+// B-hat (4096-point rows, 1024 rows; produced in the radix-8 DIF orders of
+// the plan-time kernels) permuted to the radix-16 output orders of the
+// register passes: rows always, the row index (column DIF position) too when
+// the column passes run radix 16
+__global__ void k_bhat_x16(const double2* __restrict__ in, double2* __restrict__ out,
+                           int64_t L, int cols16) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= L) return;
+  const int q = (int)(i & 4095), p = (int)(i >> 12);
+  const int q8 = posr<4096, 8>(revr<4096, 16>(q));
+  const int p8 = cols16 ? posr<1024, 8>(revr<1024, 16>(p)) : p;
+  out[i] = in[((int64_t)p8 << 12) + q8];
+}
+
 __global__ void k_twiddle(double2* tw, int64_t n, int64_t count, int64_t step) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= count) return;
@@ -174,6 +200,12 @@ struct FftArgs {
   int C_log2;
   int conj_in;         // conjugate the input (inverse DFT via conj(F(conj x)))
   FftStages st1, st2;
+  // radix-16 row transforms (register row passes of the config-3 shape):
+  // their per-stage twiddles and B-hat permuted to their output order
+  FftStages st1x, st2x;
+  const double2* tw1x;
+  const double2* tw2x;
+  const double2* Bhatx;
 };
 
 // Global <-> shared copies are issued kU elements per thread at a time so
@@ -666,10 +698,10 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_rb(FftBArgs x) {
 // Single-column (column-major [batch][*]) register-resident passes: the NB
 // vectors of a column CTA are NB consecutive n1 (as k_colfwd's C columns);
 // the row CTA holds one row (NB = 1).
-template <int N, int NBL, int T, int MINB>
+template <int N, int NBL, int T, int MINB, int R = 8>
 __global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
-  using F = RegFft<N, NBL, T>;
-  constexpr int S0 = N / 8;
+  using F = RegFft<N, NBL, T, R>;
+  constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * F::NB;
@@ -680,7 +712,7 @@ __global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
     const int u = F::but(k);
     const int64_t n1 = c0 + F::vec(k);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < R; ++r) {
       const int64_t n = n1 + a.L1 * (int64_t)F::template pos<S0>(u, r);
       f.x[k][r] = make_double2(0.0, 0.0);
       if (n1 < a.L1 && n < a.K) {
@@ -690,7 +722,7 @@ __global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
       }
     }
   }
-  f.dif(sm, a.st2, a.tw2);
+  f.dif(sm, R == 16 ? a.st2x : a.st2, R == 16 ? a.tw2x : a.tw2);
   double2* Y = a.Y + (int64_t)col * a.L;
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
@@ -698,17 +730,17 @@ __global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
     const int64_t n1 = c0 + F::vec(k);
     if (n1 >= a.L1) continue;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int p = 8 * u + r;
-      Y[n1 + a.L1 * (int64_t)p] = cmul(f.x[k][r], wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)rev8<N>(p)));
+    for (int r = 0; r < R; ++r) {
+      const int p = R * u + r;
+      Y[n1 + a.L1 * (int64_t)p] = cmul(f.x[k][r], wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(p)));
     }
   }
 }
 
-template <int N, int T, int MINB>
+template <int N, int T, int MINB, int R = 8>
 __global__ void __launch_bounds__(T, MINB) k_rowmul_r1(FftArgs a) {
-  using F = RegFft<N, 0, T>;
-  constexpr int S0 = N / 8;
+  using F = RegFft<N, 0, T, R>;
+  constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int64_t p = blockIdx.x;
@@ -718,29 +750,29 @@ __global__ void __launch_bounds__(T, MINB) k_rowmul_r1(FftArgs a) {
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) f.x[k][r] = row[F::template pos<S0>(u, r)];
+    for (int r = 0; r < R; ++r) f.x[k][r] = row[F::template pos<S0>(u, r)];
   }
-  f.dif(sm, a.st1, a.tw1);
-  const double2* Bh = a.Bhat + p * a.L1;
+  f.dif(sm, R == 16 ? a.st1x : a.st1, R == 16 ? a.tw1x : a.tw1);
+  const double2* Bh = (R == 16 ? a.Bhatx : a.Bhat) + p * a.L1;
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) f.x[k][r] = cconj(cmul(f.x[k][r], __ldg(Bh + 8 * u + r)));
+    for (int r = 0; r < R; ++r) f.x[k][r] = cconj(cmul(f.x[k][r], __ldg(Bh + R * u + r)));
   }
-  f.dit(sm, a.st1, a.tw1);
+  f.dit(sm, R == 16 ? a.st1x : a.st1, R == 16 ? a.tw1x : a.tw1);
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) row[F::template pos<S0>(u, r)] = cconj(f.x[k][r]);
+    for (int r = 0; r < R; ++r) row[F::template pos<S0>(u, r)] = cconj(f.x[k][r]);
   }
 }
 
-template <int N, int NBL, int T, int MINB>
+template <int N, int NBL, int T, int MINB, int R = 8>
 __global__ void __launch_bounds__(T, MINB) k_colinv_r1(FftArgs a) {
-  using F = RegFft<N, NBL, T>;
-  constexpr int S0 = N / 8;
+  using F = RegFft<N, NBL, T, R>;
+  constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * F::NB;
@@ -751,15 +783,15 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_r1(FftArgs a) {
     const int u = F::but(k);
     const int64_t n1 = c0 + F::vec(k);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int p = 8 * u + r;
+    for (int r = 0; r < R; ++r) {
+      const int p = R * u + r;
       f.x[k][r] = make_double2(0.0, 0.0);
       if (n1 < a.L1)
         f.x[k][r] = cmul(cconj(Y[n1 + a.L1 * (int64_t)p]),
-                         wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)rev8<N>(p)));
+                         wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(p)));
     }
   }
-  f.dit(sm, a.st2, a.tw2);
+  f.dit(sm, R == 16 ? a.st2x : a.st2, R == 16 ? a.tw2x : a.tw2);
   double2* h = a.h + (int64_t)col * a.Kout;
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
@@ -767,7 +799,7 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_r1(FftArgs a) {
     const int64_t n1 = c0 + F::vec(k);
     if (n1 >= a.L1) continue;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < R; ++r) {
       const int64_t kk = n1 + a.L1 * (int64_t)F::template pos<S0>(u, r);
       if (kk < a.Kout) h[kk] = cmul(cconj(f.x[k][r]), __ldg(a.Q + kk));
     }
@@ -811,11 +843,11 @@ __global__ void k_dpack(const double2* __restrict__ g, double2* __restrict__ S, 
   S[o] = v;
 }
 
-template <int N, int NBL, int T, int MINB>
-__global__ void __launch_bounds__(T, MINB) k_dcolfwd(DistArgs d, const double2* __restrict__ R,
+template <int N, int NBL, int T, int MINB, int R = 8>
+__global__ void __launch_bounds__(T, MINB) k_dcolfwd(DistArgs d, const double2* __restrict__ Rb,
                                                     double2* __restrict__ Yc) {
-  using F = RegFft<N, NBL, T>;
-  constexpr int S0 = N / 8;
+  using F = RegFft<N, NBL, T, R>;
+  constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
   const FftArgs& a = d.a;
   const int64_t c0 = (int64_t)blockIdx.x * F::NB;
@@ -825,31 +857,31 @@ __global__ void __launch_bounds__(T, MINB) k_dcolfwd(DistArgs d, const double2* 
     const int u = F::but(k);
     const int64_t c = c0 + F::vec(k), n1 = d.rank * d.Bc + c;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < R; ++r) {
       const int64_t i = F::template pos<S0>(u, r);
       const int64_t n = n1 + a.L1 * i;
       f.x[k][r] = make_double2(0.0, 0.0);
-      if (i < d.I && n < a.K) f.x[k][r] = cmul(__ldg(R + (i << d.bc_log2) + c), __ldg(a.P + n));
+      if (i < d.I && n < a.K) f.x[k][r] = cmul(__ldg(Rb + (i << d.bc_log2) + c), __ldg(a.P + n));
     }
   }
-  f.dif(sm, a.st2, a.tw2);
+  f.dif(sm, R == 16 ? a.st2x : a.st2, R == 16 ? a.tw2x : a.tw2);
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
     const int64_t c = c0 + F::vec(k), n1 = d.rank * d.Bc + c;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int p = 8 * u + r;
+    for (int r = 0; r < R; ++r) {
+      const int p = R * u + r;
       Yc[((int64_t)p << d.bc_log2) + c] =
-          cmul(f.x[k][r], wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)rev8<N>(p)));
+          cmul(f.x[k][r], wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(p)));
     }
   }
 }
 
-template <int N, int T, int MINB>
+template <int N, int T, int MINB, int R = 8>
 __global__ void __launch_bounds__(T, MINB) k_drowmul(DistArgs d, double2* __restrict__ Rr) {
-  using F = RegFft<N, 0, T>;
-  constexpr int S0 = N / 8;
+  using F = RegFft<N, 0, T, R>;
+  constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
   const FftArgs& a = d.a;
   const int64_t pl = blockIdx.x, p = d.rank * d.Br + pl;
@@ -862,30 +894,30 @@ __global__ void __launch_bounds__(T, MINB) k_drowmul(DistArgs d, double2* __rest
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) f.x[k][r] = Rr[at(F::template pos<S0>(u, r))];
+    for (int r = 0; r < R; ++r) f.x[k][r] = Rr[at(F::template pos<S0>(u, r))];
   }
-  f.dif(sm, a.st1, a.tw1);
-  const double2* Bh = a.Bhat + p * a.L1;
+  f.dif(sm, R == 16 ? a.st1x : a.st1, R == 16 ? a.tw1x : a.tw1);
+  const double2* Bh = (R == 16 ? a.Bhatx : a.Bhat) + p * a.L1;
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) f.x[k][r] = cconj(cmul(f.x[k][r], __ldg(Bh + 8 * u + r)));
+    for (int r = 0; r < R; ++r) f.x[k][r] = cconj(cmul(f.x[k][r], __ldg(Bh + R * u + r)));
   }
-  f.dit(sm, a.st1, a.tw1);
+  f.dit(sm, R == 16 ? a.st1x : a.st1, R == 16 ? a.tw1x : a.tw1);
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) Rr[at(F::template pos<S0>(u, r))] = cconj(f.x[k][r]);
+    for (int r = 0; r < R; ++r) Rr[at(F::template pos<S0>(u, r))] = cconj(f.x[k][r]);
   }
 }
 
-template <int N, int NBL, int T, int MINB>
+template <int N, int NBL, int T, int MINB, int R = 8>
 __global__ void __launch_bounds__(T, MINB) k_dcolinv(DistArgs d, const double2* __restrict__ Y2,
                                                     double2* __restrict__ H) {
-  using F = RegFft<N, NBL, T>;
-  constexpr int S0 = N / 8;
+  using F = RegFft<N, NBL, T, R>;
+  constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
   const FftArgs& a = d.a;
   const int64_t c0 = (int64_t)blockIdx.x * F::NB;
@@ -895,19 +927,19 @@ __global__ void __launch_bounds__(T, MINB) k_dcolinv(DistArgs d, const double2* 
     const int u = F::but(k);
     const int64_t c = c0 + F::vec(k), n1 = d.rank * d.Bc + c;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int p = 8 * u + r;
+    for (int r = 0; r < R; ++r) {
+      const int p = R * u + r;
       f.x[k][r] = cmul(cconj(__ldg(Y2 + ((int64_t)p << d.bc_log2) + c)),
-                       wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)rev8<N>(p)));
+                       wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(p)));
     }
   }
-  f.dit(sm, a.st2, a.tw2);
+  f.dit(sm, R == 16 ? a.st2x : a.st2, R == 16 ? a.tw2x : a.tw2);
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
     const int64_t c = c0 + F::vec(k), n1 = d.rank * d.Bc + c;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < R; ++r) {
       const int64_t k2 = F::template pos<S0>(u, r);
       const int64_t kk = n1 + a.L1 * k2;
       if (k2 < d.K2 && kk < a.Kout) {
@@ -1218,6 +1250,28 @@ FftStages make_stages(int64_t n) {
   return st;
 }
 
+// the radix-16 decomposition of a power-of-two n (16s first, then one 8/4/2)
+FftStages make_stages16(int64_t n) {
+  FftStages st{};
+  st.n = (int)n;
+  int64_t r = n;
+  std::vector<int> rad;
+  while (r % 16 == 0) rad.push_back(16), r /= 16;
+  if (r % 8 == 0) rad.push_back(8), r /= 8;
+  if (r % 4 == 0) rad.push_back(4), r /= 4;
+  if (r % 2 == 0) rad.push_back(2), r /= 2;
+  if (r != 1) fail(3, "internal: make_stages16 needs a power of two");
+  st.nst = (int)rad.size();
+  int off = 0, S = (int)n;
+  for (int i = 0; i < st.nst; ++i) {
+    st.rad[i] = rad[i];
+    S /= rad[i];
+    st.toff[i] = off;
+    off += S;
+  }
+  return st;
+}
+
 // position p after DIF holds frequency rev[p]
 std::vector<int> digit_reverse(const FftStages& st) {
   std::vector<int> rev(st.n);
@@ -1317,6 +1371,11 @@ FftArgs make_args(const NnfftPlanImpl& p) {
   a.conj_in = f.conj_in ? 1 : 0;
   a.st1 = f.st1;
   a.st2 = f.st2;
+  a.st1x = f.st1x;
+  a.st2x = f.st2x;
+  a.tw1x = f.tw1x.p;
+  a.tw2x = f.tw2x.p;
+  a.Bhatx = f.Bhatx.p;
   return a;
 }
 
@@ -1473,8 +1532,12 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_reg_smem<2, 256, 4>();
   set_smem(k_colfwd_r1<1024, 2, 512, 2>, sizeof(double2) * 4096);
   set_smem(k_colinv_r1<1024, 2, 512, 2>, sizeof(double2) * 4096);
+  set_smem(k_colfwd_r1<1024, 2, 256, 2, 16>, sizeof(double2) * 4096);
+  set_smem(k_colinv_r1<1024, 2, 256, 2, 16>, sizeof(double2) * 4096);
   set_smem(k_rowmul_r1<4096, 256, 2>, sizeof(double2) * 4096);
   set_smem(k_drowmul<4096, 256, 2>, sizeof(double2) * 4096);
+  set_smem(k_rowmul_r1<4096, 256, 2, 16>, sizeof(double2) * 4096);
+  set_smem(k_drowmul<4096, 256, 2, 16>, sizeof(double2) * 4096);
   FftPlan& f = p.fft;
   const Geometry& g = p.g;
   const int64_t Lmin = g.K + f.Kout - 1;
@@ -1588,6 +1651,25 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
     SF_LAUNCH_CHECK();
     k_rowmul<0><<<dim3((unsigned)f.L2, 1), 256, smr, s>>>(a, 1);
     SF_LAUNCH_CHECK();
+    f.x16 = 0;
+    if (f.L1 == 4096 && f.L2 == 1024 && f.st1.n == 4096 && f.st2.n == 1024) {
+      // radix-16 register passes (rows; columns too at x16 = 2): their
+      // stages, twiddles and B-hat in their output order
+      // rows only: 0.188 -> 0.179 ms; radix-16 columns (x16 = 2: 16 double2
+      // per thread, 128 registers, 16 warps/SM) measured 0.207 ms
+      f.x16 = 1;
+      if (const char* e = getenv("SFB_FFT_X16")) f.x16 = std::max(0, std::min(2, atoi(e)));
+    }
+    if (f.x16 > 0) {
+      f.st1x = make_stages16(4096);
+      launch_stage_twiddles(f.tw1x, f.st1x, s);
+      f.st2x = make_stages16(1024);
+      launch_stage_twiddles(f.tw2x, f.st2x, s);
+      f.Bhatx.alloc(f.L);
+      k_bhat_x16<<<(unsigned)ceil_div(f.L, (int64_t)256), 256, 0, s>>>(f.Bhat.p, f.Bhatx.p, f.L,
+                                                                      f.x16 == 2 ? 1 : 0);
+      SF_LAUNCH_CHECK();
+    }
   }
   SF_CUDA(cudaStreamSynchronize(s));  // b is released at scope exit
 }
@@ -1689,6 +1771,12 @@ void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h
 // 0.214; columns 4 x 512 with rows of 512 0.238; columns 2 x 256 at 3 or 4
 // CTAs/SM 0.199 / 0.192; columns 4 x 256 0.219; columns 8 x 1024 0.206; this
 // one 0.188 ms.  A persistent cp.async-pipelined version measured 9 % slower.
+// radix-16 register passes (plan-time SFB_FFT_X16: 0 off, 1 rows, 2 rows and
+// columns): 4096 = 16^3 and 1024 = 16^2 * 4 take 2 shared-memory exchanges per
+// transform instead of 3 with radix 8
+static bool row16(const FftPlan& f) { return f.x16 >= 1; }
+static bool col16(const FftPlan& f) { return f.x16 >= 2; }
+
 static bool reg_single(const FftPlan& f) {
   if (!(f.L1 == 4096 && f.L2 == 1024 && f.st1.n == 4096 && f.st2.n == 1024)) return false;
   const char* e = getenv("SFB_FFT_REG1");
@@ -1699,11 +1787,14 @@ static void launch_reg_single(const FftArgs& a, const FftPlan& f, int batch, cud
   constexpr int CBL = 2, CT = 512, CMINB = 2, RT = 256, RMINB = 2;
   const size_t smc = sizeof(double2) * ((size_t)1024 << CBL), smr = sizeof(double2) * 4096;
   const dim3 gc((unsigned)ceil_div(f.L1, (int64_t)1 << CBL), batch);
-  k_colfwd_r1<1024, CBL, CT, CMINB><<<gc, CT, smc, s>>>(a);
+  if (col16(f)) k_colfwd_r1<1024, CBL, 256, 2, 16><<<gc, 256, smc, s>>>(a);
+  else k_colfwd_r1<1024, CBL, CT, CMINB><<<gc, CT, smc, s>>>(a);
   SF_LAUNCH_CHECK();
-  k_rowmul_r1<4096, RT, RMINB><<<dim3((unsigned)f.L2, batch), RT, smr, s>>>(a);
+  if (row16(f)) k_rowmul_r1<4096, RT, RMINB, 16><<<dim3((unsigned)f.L2, batch), RT, smr, s>>>(a);
+  else k_rowmul_r1<4096, RT, RMINB><<<dim3((unsigned)f.L2, batch), RT, smr, s>>>(a);
   SF_LAUNCH_CHECK();
-  k_colinv_r1<1024, CBL, CT, CMINB><<<gc, CT, smc, s>>>(a);
+  if (col16(f)) k_colinv_r1<1024, CBL, 256, 2, 16><<<gc, 256, smc, s>>>(a);
+  else k_colinv_r1<1024, CBL, CT, CMINB><<<gc, CT, smc, s>>>(a);
   SF_LAUNCH_CHECK();
 }
 
@@ -1816,20 +1907,27 @@ void run_dist_pack(const NnfftPlanImpl& p, int world, const double2* grid, doubl
 void run_dist_colfwd(const NnfftPlanImpl& p, int world, int rank, const double2* R, double2* Yc,
                      cudaStream_t s) {
   const DistArgs d = dist_args(p, world, rank);
-  k_dcolfwd<1024, 1, 256, 4><<<(unsigned)(d.Bc / 2), 256, sizeof(double2) * 2048, s>>>(d, R, Yc);
+  if (col16(p.fft))
+    k_dcolfwd<1024, 1, 128, 4, 16><<<(unsigned)(d.Bc / 2), 128, sizeof(double2) * 2048, s>>>(d, R, Yc);
+  else
+    k_dcolfwd<1024, 1, 256, 4><<<(unsigned)(d.Bc / 2), 256, sizeof(double2) * 2048, s>>>(d, R, Yc);
   SF_LAUNCH_CHECK();
 }
 
 void run_dist_rowmul(const NnfftPlanImpl& p, int world, int rank, double2* Rr, cudaStream_t s) {
   const DistArgs d = dist_args(p, world, rank);
-  k_drowmul<4096, 256, 2><<<(unsigned)d.Br, 256, sizeof(double2) * 4096, s>>>(d, Rr);
+  if (row16(p.fft)) k_drowmul<4096, 256, 2, 16><<<(unsigned)d.Br, 256, sizeof(double2) * 4096, s>>>(d, Rr);
+  else k_drowmul<4096, 256, 2><<<(unsigned)d.Br, 256, sizeof(double2) * 4096, s>>>(d, Rr);
   SF_LAUNCH_CHECK();
 }
 
 void run_dist_colinv(const NnfftPlanImpl& p, int world, int rank, const double2* Y2,
                      const double2* R, double2* H, cudaStream_t s) {
   const DistArgs d = dist_args(p, world, rank);
-  k_dcolinv<1024, 1, 256, 4><<<(unsigned)(d.Bc / 2), 256, sizeof(double2) * 2048, s>>>(d, Y2, H);
+  if (col16(p.fft))
+    k_dcolinv<1024, 1, 128, 4, 16><<<(unsigned)(d.Bc / 2), 128, sizeof(double2) * 2048, s>>>(d, Y2, H);
+  else
+    k_dcolinv<1024, 1, 256, 4><<<(unsigned)(d.Bc / 2), 256, sizeof(double2) * 2048, s>>>(d, Y2, H);
   SF_LAUNCH_CHECK();
   if (rank == 0 && p.fft.fixD > 0) {
     k_dfix_add<<<(unsigned)ceil_div(p.fft.fixD, (int64_t)256), 256, 0, s>>>(H, R + d.I * d.Bc,

@@ -31,56 +31,66 @@ namespace sfb {
 
 __host__ __device__ constexpr int ilog8(int n) { return n < 8 ? 0 : 1 + ilog8(n / 8); }
 __host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
+__host__ __device__ constexpr int ilogr(int n, int r) { return n < r ? 0 : 1 + ilogr(n / r, r); }
 
-// N = 8^a * R0, R0 in {1, 2, 4}: make_stages() order (radix 8 first, then
-// one radix-R0 stage of stride 1)
-template <int N>
+// N = R^a * R0 with the main radix R in {8, 16} and R0 in {1, 2, 4, 8} (< R):
+// a radix-R stages first, then one radix-R0 stage of stride 1 -- make_stages()
+// order for R = 8 (and its radix-16 counterpart make_stages16)
+template <int N, int R = 8>
 struct RegShape {
-  static constexpr int A = ilog8(N);           // radix-8 stages
-  static constexpr int R0 = N >> (3 * A);      // final radix (1: none)
+  static constexpr int LOGR = ilog2c(R);
+  static constexpr int A = ilogr(N, R);        // radix-R stages
+  static constexpr int R0 = N >> (LOGR * A);   // final radix (1: none)
   static constexpr int LOG2N = ilog2c(N);
-  static_assert(R0 == 1 || R0 == 2 || R0 == 4, "N must be 8^a * {1,2,4}");
+  static_assert(R == 8 || R == 16, "main radix 8 or 16");
+  static_assert(R0 == 1 || R0 == 2 || R0 == 4 || R0 == 8, "N must be R^a * {1,2,4,8}");
   static_assert((1 << LOG2N) == N, "N must be a power of two");
 };
 
 // frequency held by position p after the DIF of length N (the digit reversal
 // of fft.cu's digit_reverse(), without a load): p = sum_q d_q S_q,
-// k = sum_q d_q 8^q with S_q = N / 8^(q+1) and the radix-R0 digit last
-template <int N>
-__device__ __forceinline__ int rev8(int p) {
-  using Sh = RegShape<N>;
+// k = sum_q d_q R^q with S_q = N / R^(q+1) and the radix-R0 digit last
+template <int N, int R = 8>
+__device__ __forceinline__ int revr(int p) {
+  using Sh = RegShape<N, R>;
   int k = 0;
 #pragma unroll
-  for (int q = 0; q < Sh::A; ++q) k |= ((p >> (Sh::LOG2N - 3 * (q + 1))) & 7) << (3 * q);
-  if (Sh::R0 > 1) k |= (p & (Sh::R0 - 1)) << (3 * Sh::A);
+  for (int q = 0; q < Sh::A; ++q)
+    k |= ((p >> (Sh::LOG2N - Sh::LOGR * (q + 1))) & (R - 1)) << (Sh::LOGR * q);
+  if (Sh::R0 > 1) k |= (p & (Sh::R0 - 1)) << (Sh::LOGR * Sh::A);
   return k;
 }
+template <int N>
+__device__ __forceinline__ int rev8(int p) {
+  return revr<N, 8>(p);
+}
 
-template <int N_, int NBL, int T>
+template <int N_, int NBL, int T, int R_ = 8>
 struct RegFft {
-  using Sh = RegShape<N_>;
+  using Sh = RegShape<N_, R_>;
+  static constexpr int R = R_;
   static constexpr int R0 = Sh::R0;
   static constexpr int N = N_;
   static constexpr int NBLOG = NBL;
   static constexpr int NB = 1 << NBL;
-  static constexpr int NQ = (N / 8) << NBL;  // 8-element groups per stage (all vectors)
+  static constexpr int NQ = (N / R) << NBL;  // R-element groups per stage (all vectors)
   static constexpr int BPT = NQ / T;
   static_assert(NQ % T == 0 && BPT >= 1, "threads must divide the butterflies");
 
-  double2 x[BPT][8];
+  double2 x[BPT][R];
 
   // vector (column) of this thread's k-th group, and the group index u
   static __device__ __forceinline__ int vec(int k) { return (threadIdx.x + k * T) & (NB - 1); }
   static __device__ __forceinline__ int but(int k) { return (threadIdx.x + k * T) >> NBL; }
-  // position of leg r of radix-8 butterfly u in a stage of stride S; S = 1
-  // is also the layout of the final radix-R0 stage (positions 8u + r)
+  // position of leg r of radix-R butterfly u in a stage of stride S; S = 1
+  // is also the layout of the final radix-R0 stage (positions R u + r)
   template <int S>
   static __device__ __forceinline__ int pos(int u, int r) {
-    return (u / S) * 8 * S + (u % S) + r * S;
+    return (u / S) * R * S + (u % S) + r * S;
   }
-  // DIF/DIT stage index of radix-8 stride S (S = N / 8^(q+1))
+  // DIF/DIT stage index of radix-R stride S (S = N / R^(q+1))
   template <int S>
-  static constexpr int stage() { return ilog8(N / S) - 1; }
+  static constexpr int stage() { return ilogr(N / S, R) - 1; }
 
   template <int S>
   __device__ __forceinline__ void to_smem(double2* sm) const {
@@ -88,7 +98,7 @@ struct RegFft {
     for (int k = 0; k < BPT; ++k) {
       const int u = but(k), b = vec(k);
 #pragma unroll
-      for (int r = 0; r < 8; ++r) sm[spad((pos<S>(u, r) << NBL) + b)] = x[k][r];
+      for (int r = 0; r < R; ++r) sm[spad((pos<S>(u, r) << NBL) + b)] = x[k][r];
     }
   }
   template <int S>
@@ -97,7 +107,7 @@ struct RegFft {
     for (int k = 0; k < BPT; ++k) {
       const int u = but(k), b = vec(k);
 #pragma unroll
-      for (int r = 0; r < 8; ++r) x[k][r] = sm[spad((pos<S>(u, r) << NBL) + b)];
+      for (int r = 0; r < R; ++r) x[k][r] = sm[spad((pos<S>(u, r) << NBL) + b)];
     }
   }
   // write own stride-S outputs, barrier, read own stride-S2 inputs (the
@@ -117,28 +127,28 @@ struct RegFft {
       const bool twid = S > 1 && j != 0;
       double2 w1 = make_double2(1.0, 0.0);
       if (twid) w1 = __ldg(t + j);
-      if (DIT && twid) apply_twiddles<8>(x[k], w1);
-      Dft<8>::run(x[k]);
-      if (!DIT && twid) apply_twiddles<8>(x[k], w1);
+      if (DIT && twid) apply_twiddles<R>(x[k], w1);
+      Dft<R>::run(x[k]);
+      if (!DIT && twid) apply_twiddles<R>(x[k], w1);
     }
   }
-  // the stride-1 radix-R0 stage: 8/R0 butterflies on positions 8u + r (no twiddles)
+  // the stride-1 radix-R0 stage: R/R0 butterflies on positions R u + r (no twiddles)
   __device__ __forceinline__ void radix_r0() {
 #pragma unroll
     for (int k = 0; k < BPT; ++k)
 #pragma unroll
-      for (int c = 0; c < 8 / R0; ++c) Dft<R0>::run(&x[k][c * R0]);
+      for (int c = 0; c < R / R0; ++c) Dft<R0>::run(&x[k][c * R0]);
   }
 
-  // DIF from the radix-8 stage of stride S (its inputs in x); ends with the
-  // final-stage outputs (positions 8u + r) in registers, no barrier after
+  // DIF from the radix-R stage of stride S (its inputs in x); ends with the
+  // final-stage outputs (positions R u + r) in registers, no barrier after
   template <int S>
   __device__ __forceinline__ void dif_from(double2* sm, const FftStages& st,
                                            const double2* __restrict__ tw) {
     butterflies<S, false>(st, tw);
     if constexpr (S > R0) {
-      exchange<S, S / 8>(sm);
-      dif_from<S / 8>(sm, st, tw);
+      exchange<S, S / R>(sm);
+      dif_from<S / R>(sm, st, tw);
     } else if constexpr (R0 > 1) {
       exchange<S, 1>(sm);
       radix_r0();
@@ -146,7 +156,7 @@ struct RegFft {
   }
   __device__ __forceinline__ void dif(double2* sm, const FftStages& st,
                                       const double2* __restrict__ tw) {
-    dif_from<N / 8>(sm, st, tw);
+    dif_from<N / R>(sm, st, tw);
   }
   // DIT from the radix-8 stage of stride S; ends with the stride-N/8
   // (natural-order) outputs in registers
@@ -154,9 +164,9 @@ struct RegFft {
   __device__ __forceinline__ void dit_from(double2* sm, const FftStages& st,
                                            const double2* __restrict__ tw) {
     butterflies<S, true>(st, tw);
-    if constexpr (S < N / 8) {
-      exchange<S, S * 8>(sm);
-      dit_from<S * 8>(sm, st, tw);
+    if constexpr (S < N / R) {
+      exchange<S, S * R>(sm);
+      dit_from<S * R>(sm, st, tw);
     }
   }
   // full DIT from the final-stage layout (positions 8u + r, digit-reversed)

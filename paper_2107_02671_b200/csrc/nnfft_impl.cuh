@@ -126,6 +126,11 @@ struct FftPlan {
   DevArray<double2> tw1, tw2, tw_lo, tw_hi;
   DevArray<int> rev2;
   DevArray<double2> P, Q, Bhat;
+  // radix-16 register passes of the config-3 shape: x16 = 1 rows, 2 rows and
+  // columns; their stages, twiddles, and Bhat permuted to their output order
+  int x16 = 0;
+  FftStages st1x{}, st2x{};
+  DevArray<double2> tw1x, tw2x, Bhatx;
   DirectFft d;
   // scratch elements per column for run_fft's `work`
   int64_t work_elems() const { return single ? 0 : direct ? d.A * d.P : L; }
