@@ -263,6 +263,20 @@ void build_nnfft(sfb::NnfftPlanImpl& p, int64_t N, int64_t M1, int64_t M2, doubl
   sfb::build_plan(p, v_dev, x_dev, s);
 }
 
+}  // namespace
+
+namespace sfb {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SFB_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+}  // namespace sfb
+
+namespace {
+
 bool use_graph(const sfb::NnfftPlanImpl& p, int64_t batch) {
   static const bool off = getenv("SINCFFT_NO_GRAPHS") != nullptr;
   static const int64_t lim = [] {

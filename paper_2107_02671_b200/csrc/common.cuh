@@ -99,6 +99,38 @@ struct DevArray {
   }
 };
 
+// ---- programmatic dependent launch (PDL): a kernel launched with
+// launch_pdl() may be scheduled while the previous kernel in the stream is
+// still running its last wave; it runs its independent prologue, then
+// pdl_wait() blocks until that kernel has completed and its writes are
+// visible.  pdl_trigger() lets the NEXT kernel be scheduled.  Both are no-ops
+// for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+bool pdl_enabled();  // capi.cu: SFB_PDL (default on)
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args... args) {
+  if (!pdl_enabled()) {
+    kernel<<<grid, block, smem, s>>>(args...);
+    SF_LAUNCH_CHECK();
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SF_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
 // ---- cp.async (global -> shared without registers); src_bytes < size zero-fills
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);

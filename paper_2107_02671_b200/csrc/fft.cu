@@ -157,6 +157,8 @@ __global__ void k_bluestein_fix(const double2* __restrict__ g, const double2* __
                                 const double2* __restrict__ c, const double2* __restrict__ Q,
                                 double2* h, int64_t K, int64_t D, int64_t Kout, int conj_in,
                                 int B, int point_major) {
+  pdl_trigger();
+  pdl_wait();  // reads the previous kernel's output
   const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int col = blockIdx.y;
@@ -700,6 +702,8 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_rb(FftBArgs x) {
 // the row CTA holds one row (NB = 1).
 template <int N, int NBL, int T, int MINB, int R = 8>
 __global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
+  pdl_trigger();
+  pdl_wait();  // reads the previous kernel's output
   using F = RegFft<N, NBL, T, R>;
   constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
@@ -739,6 +743,8 @@ __global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
 
 template <int N, int T, int MINB, int R = 8>
 __global__ void __launch_bounds__(T, MINB) k_rowmul_r1(FftArgs a) {
+  pdl_trigger();
+  pdl_wait();  // reads the previous kernel's output
   using F = RegFft<N, 0, T, R>;
   constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
@@ -771,6 +777,8 @@ __global__ void __launch_bounds__(T, MINB) k_rowmul_r1(FftArgs a) {
 
 template <int N, int NBL, int T, int MINB, int R = 8>
 __global__ void __launch_bounds__(T, MINB) k_colinv_r1(FftArgs a) {
+  pdl_trigger();
+  pdl_wait();  // reads the previous kernel's output
   using F = RegFft<N, NBL, T, R>;
   constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
@@ -1678,10 +1686,9 @@ static void launch_fix(const NnfftPlanImpl& p, const double2* grid, double2* h, 
                        int point_major, cudaStream_t s) {
   const FftPlan& f = p.fft;
   if (f.fixD <= 0) return;
-  k_bluestein_fix<<<dim3((unsigned)ceil_div(f.fixD * 32, 256), batch), 256, 0, s>>>(
-      grid, f.P.p, f.fixc.p, f.Q.p, h, p.g.K, f.fixD, f.Kout, f.conj_in ? 1 : 0, batch,
-      point_major);
-  SF_LAUNCH_CHECK();
+  launch_pdl(k_bluestein_fix, dim3((unsigned)ceil_div(f.fixD * 32, 256), batch), dim3(256), 0, s,
+             grid, (const double2*)f.P.p, (const double2*)f.fixc.p, (const double2*)f.Q.p, h,
+             p.g.K, f.fixD, f.Kout, f.conj_in ? 1 : 0, batch, point_major);
 }
 
 bool fft_supports_point_major(const NnfftPlanImpl& p) {
@@ -1787,15 +1794,15 @@ static void launch_reg_single(const FftArgs& a, const FftPlan& f, int batch, cud
   constexpr int CBL = 2, CT = 512, CMINB = 2, RT = 256, RMINB = 2;
   const size_t smc = sizeof(double2) * ((size_t)1024 << CBL), smr = sizeof(double2) * 4096;
   const dim3 gc((unsigned)ceil_div(f.L1, (int64_t)1 << CBL), batch);
-  if (col16(f)) k_colfwd_r1<1024, CBL, 256, 2, 16><<<gc, 256, smc, s>>>(a);
-  else k_colfwd_r1<1024, CBL, CT, CMINB><<<gc, CT, smc, s>>>(a);
-  SF_LAUNCH_CHECK();
-  if (row16(f)) k_rowmul_r1<4096, RT, RMINB, 16><<<dim3((unsigned)f.L2, batch), RT, smr, s>>>(a);
-  else k_rowmul_r1<4096, RT, RMINB><<<dim3((unsigned)f.L2, batch), RT, smr, s>>>(a);
-  SF_LAUNCH_CHECK();
-  if (col16(f)) k_colinv_r1<1024, CBL, 256, 2, 16><<<gc, 256, smc, s>>>(a);
-  else k_colinv_r1<1024, CBL, CT, CMINB><<<gc, CT, smc, s>>>(a);
-  SF_LAUNCH_CHECK();
+  // programmatic dependent launches: each pass is scheduled during the
+  // previous one's last wave and waits (griddepcontrol.wait) for its output
+  if (col16(f)) launch_pdl(k_colfwd_r1<1024, CBL, 256, 2, 16>, gc, dim3(256), smc, s, a);
+  else launch_pdl(k_colfwd_r1<1024, CBL, CT, CMINB>, gc, dim3(CT), smc, s, a);
+  const dim3 gr((unsigned)f.L2, batch);
+  if (row16(f)) launch_pdl(k_rowmul_r1<4096, RT, RMINB, 16>, gr, dim3(RT), smr, s, a);
+  else launch_pdl(k_rowmul_r1<4096, RT, RMINB>, gr, dim3(RT), smr, s, a);
+  if (col16(f)) launch_pdl(k_colinv_r1<1024, CBL, 256, 2, 16>, gc, dim3(256), smc, s, a);
+  else launch_pdl(k_colinv_r1<1024, CBL, CT, CMINB>, gc, dim3(CT), smc, s, a);
 }
 
 void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work, int batch,

@@ -142,14 +142,12 @@ __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(Ga
   const int64_t jb = (int64_t)blockIdx.x * kGatherGroup + threadIdx.x;
   const int col = blockIdx.y;
   const double2* h = a.h + (int64_t)col * a.Kout;
+  pdl_trigger();
   const int2 sp = __ldg(a.span + blockIdx.x);
   const int64_t klo = sp.x, khi = sp.y;
   const bool staged = klo >= 0 && khi < a.Kout && khi - klo + 1 <= kGatherSpan;
-  if (staged) {
-    for (int64_t i = threadIdx.x; i <= khi - klo; i += kGatherThreads)
-      cp_async16(hs + i, h + klo + i);
-    cp_async_commit();
-  }
+  // the plan's target tables are independent of the previous kernel: their
+  // loads are in flight while this CTA waits for h
   double pos[2 * NP], sc[2 * NP];
   int dst[2 * NP];
 #pragma unroll
@@ -163,6 +161,12 @@ __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(Ga
       sc[t] = __ldg(a.scale + j);
       dst[t] = __ldg(a.perm + j);
     }
+  }
+  pdl_wait();  // h is the previous kernel's output
+  if (staged) {
+    for (int64_t i = threadIdx.x; i <= khi - klo; i += kGatherThreads)
+      cp_async16(hs + i, h + klo + i);
+    cp_async_commit();
   }
   if (staged) {
     cp_async_wait<0>();
@@ -199,7 +203,7 @@ void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batc
   switch (p.g.m2) {
 #define SF_CASE(MM)                                          \
   case MM:                                                   \
-    if (kGatherTPT >= 2) k_gather2<MM><<<grid, kGatherThreads, 0, s>>>(a, p.c2); \
+    if (kGatherTPT >= 2) launch_pdl(k_gather2<MM>, grid, dim3(kGatherThreads), 0, s, a, p.c2); \
     else k_gather<MM><<<grid, kGatherThreads, 0, s>>>(a, p.c2);              \
     break;
     SF_CASE(2) SF_CASE(3) SF_CASE(4) SF_CASE(5) SF_CASE(6) SF_CASE(7) SF_CASE(8) SF_CASE(9)
