@@ -1,6 +1,9 @@
 // window.cu -- plan-time fit of the per-tap window polynomials (host code).
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "window.cuh"
@@ -85,7 +88,41 @@ double validate_m(int m, const WinCoef& C, ld beta) {
 
 }  // namespace
 
+namespace {
+WinCoef fit_window_uncached(int m, double beta_d, double* max_err_out);
+struct FitCache {
+  std::mutex mu;
+  std::map<std::pair<int, double>, std::pair<WinCoef, double>> fits;
+};
+FitCache& fit_cache() {
+  static FitCache c;
+  return c;
+}
+}  // namespace
+
+// The fit and its long-double validation (~10 ms) depend only on (m, beta):
+// memoised per process, so plans that repeat a window (the CLI's thousands of
+// small plans, sinc plans, adjoint sub-plans) pay for it once.
 WinCoef fit_window(int m, double beta_d, double* max_err_out) {
+  FitCache& c = fit_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.fits.find({m, beta_d});
+    if (it != c.fits.end()) {
+      if (max_err_out) *max_err_out = it->second.second;
+      return it->second.first;
+    }
+  }
+  double err = 0.0;
+  const WinCoef w = fit_window_uncached(m, beta_d, &err);  // throws on bad m
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.fits.emplace(std::make_pair(m, beta_d), std::make_pair(w, err));
+  if (max_err_out) *max_err_out = err;
+  return w;
+}
+
+namespace {
+WinCoef fit_window_uncached(int m, double beta_d, double* max_err_out) {
   if (m < 2 || m > kMaxM)
     fail(5, "window cut-off m=" + std::to_string(m) + " outside the supported range [2, 16]");
   WinCoef C;
@@ -118,5 +155,6 @@ WinCoef fit_window(int m, double beta_d, double* max_err_out) {
                 " (max error " + std::to_string(err) + ")");
   return C;
 }
+}  // namespace
 
 }  // namespace sfb
