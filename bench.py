@@ -317,6 +317,14 @@ def run_b200(args, cfg):
     # sparse chunks, and every rank flushes the whole grid)
     src_idx = np.argsort(vs, kind="stable")[s0:s1] if world > 1 else slice(None)
     tgt_idx = np.argsort(x, kind="stable")[t0_:t1_] if world > 1 else slice(None)
+    # batched configs shard the independent COLUMNS instead (no
+    # communication; every rank plans all nodes and transforms B/P columns)
+    col_shard = world > 1 and cfg["batch"] > 0
+    c0 = c1 = 0
+    if col_shard:
+        src_idx = tgt_idx = slice(None)
+        s0, s1, t0_, t1_ = 0, cfg["M1"], 0, cfg["M2"]
+        c0, c1 = rank * cfg["batch"] // world, (rank + 1) * cfg["batch"] // world
     torch.cuda.synchronize()
     tp = time.perf_counter()
     # N > 1: the FFT is split over the ranks too (sharding.DistributedFftNnfft,
@@ -340,6 +348,9 @@ def run_b200(args, cfg):
     geo = plan.backend_geometry
     B = max(cfg["batch"], 1)
     fshard = np.ascontiguousarray(f[src_idx])
+    if col_shard:
+        B = c1 - c0
+        fshard = np.ascontiguousarray(f[:, c0:c1])
     d_f = torch.from_numpy(fshard).to(dev)
     d_out = torch.empty((t1_ - t0_,) + ((B,) if cfg["batch"] else ()), dtype=torch.complex128,
                         device=dev)
@@ -348,7 +359,7 @@ def run_b200(args, cfg):
     ph = plan.handle
 
     def step():
-        if world == 1:
+        if world == 1 or col_shard:
             _lib.check(L.sincfft_nnfft_execute(ph, d_f.data_ptr(), d_out.data_ptr(), B,
                                                _lib.PTR_DEVICE, sh))
         elif dist_fft is not None:
@@ -385,7 +396,7 @@ def run_b200(args, cfg):
         ev1.synchronize()
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
-    total_nodes = (cfg["M1"] + cfg["M2"]) * B
+    total_nodes = (cfg["M1"] + cfg["M2"]) * max(cfg["batch"], 1)  # the whole job
     value = total_nodes / (ms * 1e-3)
 
     # the device-resident output of the timed steps (the per-stage profiling
@@ -396,6 +407,8 @@ def run_b200(args, cfg):
         # the unsharded transform of the same inputs (one plan over everything)
         full = sf.nnfft_plan(n_star, vs, x, m1=m, m2=m, device=local)
         ref = sf.nnfft_trafo(full, f)[tgt_idx]
+        if col_shard:
+            ref = ref[:, c0:c1]
         torch.cuda.synchronize()
         shard_dev = float(np.max(np.abs(dev_out - ref)) / np.abs(f).sum())
         del full
@@ -449,7 +462,7 @@ def run_b200(args, cfg):
 
     def e2e_step(k):
         st = C.c_void_p(streams[k % nbuf].cuda_stream)
-        if world == 1:
+        if world == 1 or col_shard:
             _lib.check(L.sincfft_nnfft_execute(ph, h_f[k % nbuf].data_ptr(),
                                                h_out[k % nbuf].data_ptr(), B,
                                                _lib.PTR_HOST_ASYNC, st))
@@ -581,14 +594,16 @@ def run_b200(args, cfg):
                        "N_star": n_star, "N1": geo["N1"], "K": K, "N2": N2,
                        "fft_length_L": geo["L"], "fft_L1xL2": [geo["L1"], geo["L2"]], "l2": "inputs larger than L2 "
                        "(f and out 256 MiB each per column vs 126 MB L2)",
-                       "parallelism": f"sources+targets sharded x{world}" +
-                       (" by position (quantiles of v and x)" if world > 1 else "") +
+                       "parallelism": (f"batch columns sharded x{world} (no communication)"
+                                       if col_shard else
+                                       f"sources+targets sharded x{world}" +
+                                       (" by position (quantiles of v and x)" if world > 1 else "")) +
                        (("; distributed FFT: " + ("reduce-scatter + 2 all-to-all + all-gather"
                                                    if args.dense_exchange else
                                                    "4 all-to-alls (grid / h rows exchanged "
                                                    "sparsely)")
                          if dist_fft is not None else ", NCCL all-reduce of the K-grid")
-                        if world > 1 else "")},
+                        if world > 1 and not col_shard else "")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "alg_bytes_per_launch": alg[dom],
