@@ -189,31 +189,66 @@ def run_sinc_b200(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     sh = C.c_void_p(stream.cuda_stream)
     rng = np.random.default_rng(0)
-    a = rng.uniform(-0.5, 0.5, cfg["M1"])
-    b = rng.uniform(-0.5, 0.5, cfg["M2"])
-    c = rng.standard_normal(cfg["M1"])
-    # independent replicas per rank (the sinc path's large stages shard the
-    # same way as the NNFFT; here each rank runs the whole transform)
+    a_all = rng.uniform(-0.5, 0.5, cfg["M1"])
+    b_all = rng.uniform(-0.5, 0.5, cfg["M2"])
+    c_all = rng.standard_normal(cfg["M1"])
+    # N > 1: sources and targets partitioned by position (quantile ranges);
+    # stage 1 is linear in c, so the ranks' partial alphas at the n+1
+    # Clenshaw-Curtis nodes are summed with ONE all-reduce of (n+1) complex,
+    # then every rank evaluates its own targets (sincfft_sinc_stage1/3)
+    si = np.argsort(a_all, kind="stable")[rank * cfg["M1"] // world:(rank + 1) * cfg["M1"] // world]
+    ti = np.argsort(b_all, kind="stable")[rank * cfg["M2"] // world:(rank + 1) * cfg["M2"] // world]
+    if world == 1:
+        si = ti = slice(None)
+    a, b, c = a_all[si], b_all[ti], np.ascontiguousarray(c_all[si])
     tp = time.perf_counter()
     plan = sf.sinc_plan(cfg["N"], a, b, m1=cfg["m"], m2=cfg["m"], device=local)
     torch.cuda.synchronize()
     plan_ms = (time.perf_counter() - tp) * 1e3
     d_c = torch.from_numpy(c).to(dev)
-    d_out = torch.empty(cfg["M2"], dtype=torch.complex128, device=dev)
+    d_out = torch.empty(b.size, dtype=torch.complex128, device=dev)
+    d_alpha = torch.empty(plan.n + 1, dtype=torch.complex128, device=dev)
     L = _lib.lib
 
     def step():
-        _lib.check(L.sincfft_sinc_execute(plan.handle, d_c.data_ptr(), 1, d_out.data_ptr(),
-                                          _lib.PTR_DEVICE, sh))
+        if world == 1:
+            _lib.check(L.sincfft_sinc_execute(plan.handle, d_c.data_ptr(), 1, d_out.data_ptr(),
+                                              _lib.PTR_DEVICE, sh))
+            return
+        _lib.check(L.sincfft_sinc_stage1(plan.handle, d_c.data_ptr(), 1, d_alpha.data_ptr(), sh))
+        if args.dist_backend != "nccl":
+            torch.cuda.synchronize()
+        dist.all_reduce(torch.view_as_real(d_alpha))
+        if args.dist_backend != "nccl":
+            torch.cuda.synchronize()
+        _lib.check(L.sincfft_sinc_stage3(plan.handle, d_alpha.data_ptr(), d_out.data_ptr(), sh))
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
@@ -221,21 +256,35 @@ def run_sinc_b200(args, cfg):
             step()
         ev1.record(stream)
         ev1.synchronize()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist:
+        dist.barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     units = cfg["M1"] + cfg["M2"]
+    shard_dev = None
+    if world > 1 and args.check_shards:
+        full = sf.sinc_plan(cfg["N"], a_all, b_all, m1=cfg["m"], m2=cfg["m"], device=local)
+        ref = sf.fast_sinc_transform(full, c_all)[ti]
+        shard_dev = float(np.max(np.abs(d_out.cpu().numpy() - ref)) / np.abs(c_all).sum())
+        del full
     # end to end from pinned host buffers, pipelined like the NNFFT configs:
     # successive steps rotate over --e2e-streams streams (SINCFFT_PTR_HOST_ASYNC)
     # so the H2D of step k+1, the kernels of step k and the D2H of step k-1
     # overlap on the full-duplex PCIe link
-    nbuf = args.e2e_streams
+    nbuf = args.e2e_streams if world == 1 else 1
     h_c = [torch.from_numpy(c).pin_memory() for _ in range(nbuf)]
-    h_out = [torch.empty(cfg["M2"], dtype=torch.complex128).pin_memory() for _ in range(nbuf)]
-    streams = [torch.cuda.Stream(dev) for _ in range(nbuf)]
+    h_out = [torch.empty(b.size, dtype=torch.complex128).pin_memory() for _ in range(nbuf)]
+    streams = [torch.cuda.Stream(dev) for _ in range(nbuf)] if world == 1 else [stream]
 
     def e2e_step(k):
         st = C.c_void_p(streams[k % nbuf].cuda_stream)
-        _lib.check(L.sincfft_sinc_execute(plan.handle, h_c[k % nbuf].data_ptr(), 1,
-                                          h_out[k % nbuf].data_ptr(), _lib.PTR_HOST_ASYNC, st))
+        if world == 1:
+            _lib.check(L.sincfft_sinc_execute(plan.handle, h_c[k % nbuf].data_ptr(), 1,
+                                              h_out[k % nbuf].data_ptr(), _lib.PTR_HOST_ASYNC,
+                                              st))
+            return
+        d_c.copy_(h_c[0], non_blocking=True)  # sharded: H2D, stage 1, all-reduce, stage 3, D2H
+        step()
+        h_out[0].copy_(d_out, non_blocking=True)
 
     for k in range(max(3 * nbuf, args.warmup)):
         e2e_step(k)
@@ -251,7 +300,7 @@ def run_sinc_b200(args, cfg):
         stream.wait_event(e)
     ev1.record(stream)
     ev1.synchronize()
-    e2e_ms = ev0.elapsed_time(ev1) / args.steps
+    e2e_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     e2e_dev = float(np.max(np.abs(h_out[(args.steps - 1) % nbuf].numpy() - d_out.cpu().numpy()))
                     / np.abs(c).sum())
     if e2e_dev > 1e-13:
@@ -264,21 +313,27 @@ def run_sinc_b200(args, cfg):
     achieved = alg / (ms * 1e-3) / 1e9
     line = {"metric": "fast sinc transform (L1+L2) nodes/sec fp64", "value": units / (ms * 1e-3),
             "unit": "nodes/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["desc"], "n_star": plan.n_star, "K": g1["K"],
-                       "N2": g1["N2"], "fft_length_L": g1["L"]},
+                       "N2": g1["N2"], "fft_length_L": g1["L"],
+                       "parallelism": f"sources+targets sharded x{world} by position"
+                                      + ("; one all-reduce of the n+1 stage-1 values"
+                                         if world > 1 else "")},
             "roofline": {"bound": "hbm", "kernel": "whole transform", "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "alg_bytes_per_launch": alg},
             "plan_ms": plan_ms,
             "e2e": {"value": units / (e2e_ms * 1e-3), "unit": "nodes/s",
-                    "h2d_bytes_per_step": 8 * cfg["M1"], "d2h_bytes_per_step": 16 * cfg["M2"],
+                    "h2d_bytes_per_step": 8 * c.size, "d2h_bytes_per_step": 16 * b.size,
                     "ms_per_step": e2e_ms,
-                    "mode": f"sincfft_sinc_execute(host pinned, PTR_HOST_ASYNC), {nbuf} streams "
-                            "round-robin"},
+                    "mode": (f"sincfft_sinc_execute(host pinned, PTR_HOST_ASYNC), {nbuf} "
+                             "streams round-robin" if world == 1 else
+                             "H2D, stage 1, all-reduce, stage 3, D2H on one stream")},
             "e2e_vs_device_rel_err": e2e_dev,
             "gpu_launches": 2 * 5 * args.steps, "clocks": clk.summary()}
+    if shard_dev is not None:
+        line["shard_check_rel_err"] = shard_dev
     if rank == 0:
         print(json.dumps(line), flush=True)
 

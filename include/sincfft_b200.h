@@ -247,6 +247,16 @@ SINCFFT_API int sincfft_sinc_plan_geometry(sincfft_sinc_plan plan, sincfft_geome
 SINCFFT_API int sincfft_sinc_execute(sincfft_sinc_plan plan, const double *c, int32_t c_is_real,
                          double *out, int32_t ptr_kind, void *stream);
 
+/* The two stages of sincfft_sinc_execute, for source/target-sharded runs
+ * (additive): stage1 writes alpha = w .* (stage-1 transform of c) at the n+1
+ * Clenshaw-Curtis nodes into a caller device buffer (linear in c, so partial
+ * alphas of source shards sum -- one all-reduce of (n+1) complex); stage3
+ * evaluates this plan's targets from alpha.  Device pointers, stream-ordered. */
+SINCFFT_API int sincfft_sinc_stage1(sincfft_sinc_plan plan, const double *c, int32_t c_is_real,
+                                    double *alpha_dev, void *stream);
+SINCFFT_API int sincfft_sinc_stage3(sincfft_sinc_plan plan, const double *alpha_dev,
+                                    double *out_dev, void *stream);
+
 /* --- classical NFFT ---------------------------------
  * Replaces sincfft.nfft (nfft.py:53-123), sinh window: nfft_plan(N, x,
  * sigma, m) -> sincfft_nfft_plan_create (N even, sigma N an even integer,

@@ -87,6 +87,8 @@ SIGNATURES = {
     "sincfft_sinc_plan_destroy": (C.c_int, [_vp]),
     "sincfft_sinc_plan_geometry": (C.c_int, [_vp, C.POINTER(Geometry), C.POINTER(Geometry)]),
     "sincfft_sinc_execute": (C.c_int, [_vp, _vp, C.c_int32, _vp, C.c_int32, _vp]),
+    "sincfft_sinc_stage1": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp]),
+    "sincfft_sinc_stage3": (C.c_int, [_vp, _vp, _vp, _vp]),
     "sincfft_nnfft_adjoint": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, _vp]),
     "sincfft_nfft_plan_create": (C.c_int, [C.POINTER(_vp), C.c_int64, C.c_int64, C.c_double,
                                            C.c_int32, _vp, C.c_int32, C.c_int32, _vp]),

@@ -798,6 +798,51 @@ int sincfft_sinc_plan_geometry(sincfft_sinc_plan plan, sincfft_geometry* stage1,
   });
 }
 
+// stage 1 (NNFFT or NFFT trafo of c at the Chebyshev nodes, times the
+// Clenshaw-Curtis weights folded into its gather scale) and stage 3 (from the
+// weighted alpha to the targets) of the fast sinc transform
+static void sinc_stage1(sincfft_sinc_plan plan, const void* cdev, int c_is_real, double2* alpha,
+                        cudaStream_t s) {
+  if (plan->nf1) {
+    // stage 1 = NFFT trafo of c (complex; real input promoted like the reference)
+    const double2* cc = (const double2*)cdev;
+    sfb::Scratch cz(c_is_real ? sizeof(double2) * (size_t)plan->L1 : 1, s);
+    if (c_is_real) {
+      k_real_to_complex<<<(unsigned)sfb::ceil_div(plan->L1, 256), 256, 0, s>>>(
+          (const double*)cdev, cz.as<double2>(), plan->L1);
+      SF_LAUNCH_CHECK();
+      cc = cz.as<double2>();
+    }
+    sfb::run_nfft_trafo(*plan->nf1, cc, alpha, s);
+  } else {
+    const sfb::NnfftPlanImpl& p1 = plan->st1;
+    sfb::Scratch g1(sizeof(double2) * (size_t)p1.g.K, s);
+    sfb::Scratch w1(sizeof(double2) * (size_t)p1.fft.work_elems(), s);
+    sfb::Scratch h1(sizeof(double2) * (size_t)p1.fft.Kout, s);
+    if (c_is_real) sfb::run_spread_real(p1, (const double*)cdev, g1.as<double2>(), s);
+    else sfb::run_spread(p1, (const double2*)cdev, g1.as<double2>(), 1, s);
+    sfb::run_fft(p1, g1.as<double2>(), h1.as<double2>(), w1.as<double2>(), 1, s);
+    sfb::run_gather(p1, h1.as<double2>(), alpha, 1, s);
+  }
+}
+
+static void sinc_stage3(sincfft_sinc_plan plan, const double2* alpha, double* out,
+                        int32_t ptr_kind, cudaStream_t s) {
+  const size_t ob = sizeof(double2) * (size_t)plan->L2;
+  auto stage3 = [&](double2* dst) {
+    if (plan->nf3) sfb::run_nfft_adjoint(*plan->nf3, alpha, dst, s);
+    else sfb::run_execute(plan->st3, alpha, dst, 1, s);
+  };
+  if (ptr_kind == SINCFFT_PTR_DEVICE) {
+    stage3((double2*)out);
+  } else {
+    sfb::Scratch o(ob, s);
+    stage3(o.as<double2>());
+    SF_CUDA(cudaMemcpyAsync(out, o.p, ob, cudaMemcpyDeviceToHost, s));
+    if (ptr_kind == SINCFFT_PTR_HOST) SF_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
 int sincfft_sinc_execute(sincfft_sinc_plan plan, const double* c, int32_t c_is_real, double* out,
                          int32_t ptr_kind, void* stream) {
   return guarded([&] {
@@ -807,42 +852,27 @@ int sincfft_sinc_execute(sincfft_sinc_plan plan, const double* c, int32_t c_is_r
     cudaStream_t s = as_stream(stream);
     const size_t cb = (c_is_real ? sizeof(double) : sizeof(double2)) * (size_t)plan->L1;
     InBuf cin(c, cb, ptr_kind, s);
-    const int64_t nz = plan->n + 1;
-    sfb::Scratch alpha(sizeof(double2) * (size_t)nz, s);
-    if (plan->nf1) {
-      // stage 1 = NFFT trafo of c (complex; real input promoted like the reference)
-      const double2* cc = (const double2*)cin.ptr;
-      sfb::Scratch cz(c_is_real ? sizeof(double2) * (size_t)plan->L1 : 1, s);
-      if (c_is_real) {
-        k_real_to_complex<<<(unsigned)sfb::ceil_div(plan->L1, 256), 256, 0, s>>>(
-            (const double*)cin.ptr, cz.as<double2>(), plan->L1);
-        SF_LAUNCH_CHECK();
-        cc = cz.as<double2>();
-      }
-      sfb::run_nfft_trafo(*plan->nf1, cc, alpha.as<double2>(), s);
-    } else {
-      const sfb::NnfftPlanImpl& p1 = plan->st1;
-      sfb::Scratch g1(sizeof(double2) * (size_t)p1.g.K, s);
-      sfb::Scratch w1(sizeof(double2) * (size_t)p1.fft.work_elems(), s);
-      sfb::Scratch h1(sizeof(double2) * (size_t)p1.fft.Kout, s);
-      if (c_is_real) sfb::run_spread_real(p1, (const double*)cin.ptr, g1.as<double2>(), s);
-      else sfb::run_spread(p1, (const double2*)cin.ptr, g1.as<double2>(), 1, s);
-      sfb::run_fft(p1, g1.as<double2>(), h1.as<double2>(), w1.as<double2>(), 1, s);
-      sfb::run_gather(p1, h1.as<double2>(), alpha.as<double2>(), 1, s);
-    }
-    const size_t ob = sizeof(double2) * (size_t)plan->L2;
-    auto stage3 = [&](double2* dst) {
-      if (plan->nf3) sfb::run_nfft_adjoint(*plan->nf3, alpha.as<double2>(), dst, s);
-      else sfb::run_execute(plan->st3, alpha.as<double2>(), dst, 1, s);
-    };
-    if (ptr_kind == SINCFFT_PTR_DEVICE) {
-      stage3((double2*)out);
-    } else {
-      sfb::Scratch o(ob, s);
-      stage3(o.as<double2>());
-      SF_CUDA(cudaMemcpyAsync(out, o.p, ob, cudaMemcpyDeviceToHost, s));
-      if (ptr_kind == SINCFFT_PTR_HOST) SF_CUDA(cudaStreamSynchronize(s));
-    }
+    sfb::Scratch alpha(sizeof(double2) * (size_t)(plan->n + 1), s);
+    sinc_stage1(plan, cin.ptr, c_is_real, alpha.as<double2>(), s);
+    sinc_stage3(plan, alpha.as<double2>(), out, ptr_kind, s);
+  });
+}
+
+int sincfft_sinc_stage1(sincfft_sinc_plan plan, const double* c, int32_t c_is_real,
+                        double* alpha_dev, void* stream) {
+  return guarded([&] {
+    if (!plan || !c || !alpha_dev) sfb::fail(1, "NULL argument");
+    set_device(plan->device);
+    sinc_stage1(plan, c, c_is_real, (double2*)alpha_dev, as_stream(stream));
+  });
+}
+
+int sincfft_sinc_stage3(sincfft_sinc_plan plan, const double* alpha_dev, double* out_dev,
+                        void* stream) {
+  return guarded([&] {
+    if (!plan || !alpha_dev || !out_dev) sfb::fail(1, "NULL argument");
+    set_device(plan->device);
+    sinc_stage3(plan, (const double2*)alpha_dev, out_dev, SINCFFT_PTR_DEVICE, as_stream(stream));
   });
 }
 
