@@ -41,7 +41,10 @@ struct Geometry {
 constexpr int kTile = SFB_SPREAD_TILE;
 constexpr int kChunk = 4;
 constexpr int kBlockChunks = 32;  // chunks per block = lanes per warp
-constexpr int kSpreadWarps = 8;   // warps per spread CTA (independent workers)
+#ifndef SFB_SPREAD_WARPS
+#define SFB_SPREAD_WARPS 8
+#endif
+constexpr int kSpreadWarps = SFB_SPREAD_WARPS;  // warps per spread CTA (independent workers)
 
 struct SpreadPlan {
   DevArray<double> pos;    // fl(N1 * v) in chunk-slot order    [n_blocks * 32 * kChunk]

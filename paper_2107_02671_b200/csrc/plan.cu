@@ -12,6 +12,10 @@
 
 #include "nnfft_impl.cuh"
 
+#ifndef SFB_SPREAD_CTAS
+#define SFB_SPREAD_CTAS 2  // persistent spread CTAs per SM (matches SFB_SPREAD_MINB)
+#endif
+
 namespace sfb {
 
 // --------------------------------------------------------------- geometry
@@ -474,7 +478,7 @@ void build_sources(NnfftPlanImpl& p, const double* v, int64_t M1, double N1, int
       const int64_t nblk = p.sp.n_blocks;
       const char* e1 = getenv("SFB_SPREAD_CTAS_PER_SM");
       const char* e2 = getenv("SFB_SPREAD_BLOCKS_PER_WARP");
-      const int cps = e1 ? std::max(1, atoi(e1)) : 2;
+      const int cps = e1 ? std::max(1, atoi(e1)) : SFB_SPREAD_CTAS;
       const int bpw = e2 ? std::max(1, atoi(e2)) : 1;  // 1 measured best (configs 1-3, 5)
       p.sp.n_ctas = (int)std::max<int64_t>(
           1, std::min<int64_t>(cps * (int64_t)p.sp.n_sms, ceil_div(nblk, bpw * kSpreadWarps)));

@@ -118,7 +118,11 @@ __device__ __forceinline__ void flush_tile(const SpreadArgs& a, W& S, int tile, 
 }
 
 template <int M, bool REAL>
-__global__ void __launch_bounds__(kSpreadWarps * 32, 2) k_spread(SpreadArgs a, WinCoef C) {
+#ifndef SFB_SPREAD_MINB
+#define SFB_SPREAD_MINB 2  // resident CTAs per SM (registers <= 65536 / (32 warps * MINB))
+#endif
+__global__ void __launch_bounds__(kSpreadWarps * 32, SFB_SPREAD_MINB) k_spread(SpreadArgs a,
+                                                                             WinCoef C) {
   using W = WarpSmem<M, REAL>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
