@@ -23,7 +23,10 @@
 namespace sfb {
 
 constexpr int kTileB = 128;   // cells per spread CTA
-constexpr int kSub = 4;       // F rows per pipelined sub-block
+#ifndef SFB_SPREADB_SUB
+#define SFB_SPREADB_SUB 4
+#endif
+constexpr int kSub = SFB_SPREADB_SUB;  // F rows per pipelined sub-block
 constexpr int kThreadsB = 128;  // 4 warps = 128 columns per CTA
 
 // ------------------------------------------------------------------ spread
