@@ -47,6 +47,46 @@ struct WinCoef {
   double o[kMaxM][kMaxNO];
 };
 
+// Polynomial in v = u^2 with compile-time coefficient offsets: Horner, or
+// Estrin's scheme (SFB_ESTRIN=1: the same number of FMAs with a dependency
+// depth of ~log2(N), the powers v^2, v^4, v^8 formed once per node).  Estrin
+// measured slower in both spread and gather (the extra live powers push the
+// spread past 124 registers into spills: 0.373 -> 0.385 ms, gather 0.297 ->
+// 0.321 ms), so Horner is the default.
+#ifndef SFB_ESTRIN
+#define SFB_ESTRIN 0  // Horner: Estrin measured slower (spills; gather 0.297 -> 0.321 ms)
+#endif
+struct VPow {
+  double p[4];  // v, v^2, v^4, v^8
+};
+__host__ __device__ __forceinline__ VPow vpowers(double v) {
+  VPow w;
+  w.p[0] = v;
+  w.p[1] = v * v;
+  w.p[2] = w.p[1] * w.p[1];
+  w.p[3] = w.p[2] * w.p[2];
+  return w;
+}
+template <int N, int OFF = 0>
+__host__ __device__ __forceinline__ double poly(const double* c, const VPow& w) {
+#if SFB_ESTRIN
+  if constexpr (N == 1) {
+    return c[OFF];
+  } else if constexpr (N == 2) {
+    return fma(c[OFF + 1], w.p[0], c[OFF]);
+  } else {
+    constexpr int H = N > 8 ? 8 : N > 4 ? 4 : 2;  // largest power of two below N
+    constexpr int L = H == 8 ? 3 : H == 4 ? 2 : 1;
+    return fma(poly<N - H, OFF + H>(c, w), w.p[L], poly<H, OFF>(c, w));
+  }
+#else
+  double r = c[OFF + N - 1];
+#pragma unroll
+  for (int k = N - 2; k >= 0; --k) r = fma(r, w.p[0], c[OFF + k]);
+  return r;
+#endif
+}
+
 // All 2M tap values w[i] = g_{i+1-M}(d) for one node.  Host and device use
 // the same instruction sequence (host validation emulates the kernel).
 template <int M>
@@ -55,15 +95,11 @@ __host__ __device__ __forceinline__ void window_taps(const WinCoef& C, double d,
   constexpr int NE = P / 2 + 1;
   constexpr int NO = (P + 1) / 2;
   const double u = 2.0 * d - 1.0;
-  const double u2 = u * u;
+  const VPow vw = vpowers(u * u);
 #pragma unroll
   for (int q = 0; q < M; ++q) {
-    double E = C.e[q][NE - 1];
-#pragma unroll
-    for (int k = NE - 2; k >= 0; --k) E = fma(E, u2, C.e[q][k]);
-    double O = C.o[q][NO - 1];
-#pragma unroll
-    for (int k = NO - 2; k >= 0; --k) O = fma(O, u2, C.o[q][k]);
+    const double E = poly<NE>(C.e[q], vw);
+    const double O = poly<NO>(C.o[q], vw);
     const double hi = fma(u, O, E);
     const double lo = fma(-u, O, E);
     if (q < M - 1) {
@@ -85,16 +121,12 @@ __device__ __forceinline__ void window_accumulate(const WinCoef& C, double d, do
   constexpr int NE = P / 2 + 1;
   constexpr int NO = (P + 1) / 2;
   const double u = 2.0 * d - 1.0;
-  const double u2 = u * u;
+  const VPow vw = vpowers(u * u);
   const double sq_hi = sqrt(d), sq_lo = sqrt(1.0 - d);
 #pragma unroll
   for (int q = 0; q < M; ++q) {
-    double E = C.e[q][NE - 1];
-#pragma unroll
-    for (int k = NE - 2; k >= 0; --k) E = fma(E, u2, C.e[q][k]);
-    double O = C.o[q][NO - 1];
-#pragma unroll
-    for (int k = NO - 2; k >= 0; --k) O = fma(O, u2, C.o[q][k]);
+    const double E = poly<NE>(C.e[q], vw);
+    const double O = poly<NO>(C.o[q], vw);
     double hi = fma(u, O, E);
     double lo = fma(-u, O, E);
     const int ih = (q < M - 1) ? M + q : 2 * M - 1;
@@ -120,23 +152,11 @@ __device__ __forceinline__ void window_taps2(const WinCoef& C, double d0, double
   constexpr int NE = P / 2 + 1;
   constexpr int NO = (P + 1) / 2;
   const double u0 = 2.0 * d0 - 1.0, u1 = 2.0 * d1 - 1.0;
-  const double v0 = u0 * u0, v1 = u1 * u1;
+  const VPow vw0 = vpowers(u0 * u0), vw1 = vpowers(u1 * u1);
 #pragma unroll
   for (int q = 0; q < M; ++q) {
-    double E0 = C.e[q][NE - 1], E1 = E0;
-#pragma unroll
-    for (int k = NE - 2; k >= 0; --k) {
-      const double c = C.e[q][k];
-      E0 = fma(E0, v0, c);
-      E1 = fma(E1, v1, c);
-    }
-    double O0 = C.o[q][NO - 1], O1 = O0;
-#pragma unroll
-    for (int k = NO - 2; k >= 0; --k) {
-      const double c = C.o[q][k];
-      O0 = fma(O0, v0, c);
-      O1 = fma(O1, v1, c);
-    }
+    const double E0 = poly<NE>(C.e[q], vw0), E1 = poly<NE>(C.e[q], vw1);
+    const double O0 = poly<NO>(C.o[q], vw0), O1 = poly<NO>(C.o[q], vw1);
     const double hi0 = fma(u0, O0, E0), lo0 = fma(-u0, O0, E0);
     const double hi1 = fma(u1, O1, E1), lo1 = fma(-u1, O1, E1);
     if (q < M - 1) {
@@ -159,24 +179,12 @@ __device__ __forceinline__ void window_accumulate2(const WinCoef& C, double d0, 
   constexpr int NE = P / 2 + 1;
   constexpr int NO = (P + 1) / 2;
   const double u0 = 2.0 * d0 - 1.0, u1 = 2.0 * d1 - 1.0;
-  const double v0 = u0 * u0, v1 = u1 * u1;
+  const VPow vw0 = vpowers(u0 * u0), vw1 = vpowers(u1 * u1);
   const double sh0 = sqrt(d0), sl0 = sqrt(1.0 - d0), sh1 = sqrt(d1), sl1 = sqrt(1.0 - d1);
 #pragma unroll
   for (int q = 0; q < M; ++q) {
-    double E0 = C.e[q][NE - 1], E1 = E0;
-#pragma unroll
-    for (int k = NE - 2; k >= 0; --k) {
-      const double c = C.e[q][k];
-      E0 = fma(E0, v0, c);
-      E1 = fma(E1, v1, c);
-    }
-    double O0 = C.o[q][NO - 1], O1 = O0;
-#pragma unroll
-    for (int k = NO - 2; k >= 0; --k) {
-      const double c = C.o[q][k];
-      O0 = fma(O0, v0, c);
-      O1 = fma(O1, v1, c);
-    }
+    const double E0 = poly<NE>(C.e[q], vw0), E1 = poly<NE>(C.e[q], vw1);
+    const double O0 = poly<NO>(C.o[q], vw0), O1 = poly<NO>(C.o[q], vw1);
     double hi0 = fma(u0, O0, E0), lo0 = fma(-u0, O0, E0);
     double hi1 = fma(u1, O1, E1), lo1 = fma(-u1, O1, E1);
     const int ih = (q < M - 1) ? M + q : 2 * M - 1;
@@ -204,24 +212,12 @@ __device__ __forceinline__ void window_dot2(const WinCoef& C, double d0, double 
   constexpr int NE = P / 2 + 1;
   constexpr int NO = (P + 1) / 2;
   const double u0 = 2.0 * d0 - 1.0, u1 = 2.0 * d1 - 1.0;
-  const double v0 = u0 * u0, v1 = u1 * u1;
+  const VPow vw0 = vpowers(u0 * u0), vw1 = vpowers(u1 * u1);
   const double sh0 = sqrt(d0), sl0 = sqrt(1.0 - d0), sh1 = sqrt(d1), sl1 = sqrt(1.0 - d1);
 #pragma unroll
   for (int q = 0; q < M; ++q) {
-    double E0 = C.e[q][NE - 1], E1 = E0;
-#pragma unroll
-    for (int k = NE - 2; k >= 0; --k) {
-      const double c = C.e[q][k];
-      E0 = fma(E0, v0, c);
-      E1 = fma(E1, v1, c);
-    }
-    double O0 = C.o[q][NO - 1], O1 = O0;
-#pragma unroll
-    for (int k = NO - 2; k >= 0; --k) {
-      const double c = C.o[q][k];
-      O0 = fma(O0, v0, c);
-      O1 = fma(O1, v1, c);
-    }
+    const double E0 = poly<NE>(C.e[q], vw0), E1 = poly<NE>(C.e[q], vw1);
+    const double O0 = poly<NO>(C.o[q], vw0), O1 = poly<NO>(C.o[q], vw1);
     double hi0 = fma(u0, O0, E0), lo0 = fma(-u0, O0, E0);
     double hi1 = fma(u1, O1, E1), lo1 = fma(-u1, O1, E1);
     const int ih = (q < M - 1) ? M + q : 2 * M - 1;
