@@ -396,8 +396,15 @@ def run_b200(args, cfg):
             # position partitions: exchange only the grid / h rows each rank
             # touches (sparse) unless --dense-exchange asks for the
             # reduce-scatter / all-gather form
-            dist_fft = (DistributedFftNnfft(plan) if args.dense_exchange
-                        else SparseDistributedFftNnfft(plan))
+            # default: the two transposes fused into the column / row passes
+            # over peer memory (CUDA IPC, NVLink P2P between the node's GPUs)
+            if args.dense_exchange:
+                dist_fft = DistributedFftNnfft(plan)
+            elif args.no_peer_transposes:
+                dist_fft = SparseDistributedFftNnfft(plan)
+            else:
+                from paper_2107_02671_b200.sharding import PeerDistributedFftNnfft
+                dist_fft = PeerDistributedFftNnfft(plan)
     torch.cuda.synchronize()
     plan_ms = (time.perf_counter() - tp) * 1e3
     geo = plan.backend_geometry
@@ -656,7 +663,10 @@ def run_b200(args, cfg):
                        (("; distributed FFT: " + ("reduce-scatter + 2 all-to-all + all-gather"
                                                    if args.dense_exchange else
                                                    "4 all-to-alls (grid / h rows exchanged "
-                                                   "sparsely)")
+                                                   "sparsely)" if args.no_peer_transposes else
+                                                   "grid / h rows all-to-all (sparse), the two "
+                                                   "transposes fused into the passes over peer "
+                                                   "memory (CUDA IPC)")
                          if dist_fft is not None else ", NCCL all-reduce of the K-grid")
                         if world > 1 and not col_shard else "")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
@@ -712,6 +722,9 @@ def main():
     ap.add_argument("--dense-exchange", action="store_true",
                     help="N > 1 distributed FFT: reduce-scatter / all-gather the whole "
                          "K-grid and h instead of all-to-alls of the rows each rank touches")
+    ap.add_argument("--no-peer-transposes", action="store_true",
+                    help="N > 1 distributed FFT: NCCL all-to-alls for the two transposes "
+                         "instead of the column / row passes storing into peer memory")
     ap.add_argument("--check-shards", action="store_true",
                     help="N > 1: compare this rank's output shard with a single-rank "
                          "transform of the same inputs and report the max deviation")

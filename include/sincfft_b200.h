@@ -190,6 +190,28 @@ SINCFFT_API int sincfft_nnfft_dist_gather_rows(sincfft_nnfft_plan plan, int32_t 
                                                const double *recv_dev, int64_t k2lo, int64_t cnt,
                                                double *out_dev, void *stream);
 
+/* Fused transposes over peer memory (additive): the two middle all-to-alls
+ * of the distributed FFT replaced by stores into the owners' receive buffers.
+ * Every rank allocates its rows buffer (L2 * Bc complex) and cols2 buffer
+ * with sincfft_ipc_alloc, exchanges sincfft_ipc_handle()s (64 bytes) through
+ * the process group and maps the peers' buffers with sincfft_ipc_open (NVLink
+ * P2P between the GPUs of a node).  Per transform:
+ *   dist_colfwd_peer(block, peers = rows buffers of all ranks)  ; barrier
+ *   dist_rowmul_peer(own rows, peers = cols2 buffers of all ranks) ; barrier
+ *   dist_colinv(own cols2, ...) as before.
+ * peers[q] is rank q's buffer as mapped in this process (its own for q == rank). */
+SINCFFT_API int sincfft_ipc_alloc(int32_t device, int64_t bytes, void **ptr);
+SINCFFT_API int sincfft_ipc_free(void *ptr);
+SINCFFT_API int sincfft_ipc_handle(void *ptr, uint8_t *handle64);
+SINCFFT_API int sincfft_ipc_open(int32_t device, const uint8_t *handle64, void **ptr);
+SINCFFT_API int sincfft_ipc_close(void *ptr);
+SINCFFT_API int sincfft_nnfft_dist_colfwd_peer(sincfft_nnfft_plan plan, int32_t world,
+                                               int32_t rank, const double *block_dev,
+                                               const uint64_t *peers, void *stream);
+SINCFFT_API int sincfft_nnfft_dist_rowmul_peer(sincfft_nnfft_plan plan, int32_t world,
+                                               int32_t rank, double *rows_dev,
+                                               const uint64_t *peers, void *stream);
+
 /* Observability: one execute with DEVICE pointers and CUDA events recorded
  * on `stream` between the stages; returns after synchronizing the stream
  * with stage_ms[0..3] = spread (incl. grid zeroing), FFT (deconvolution +

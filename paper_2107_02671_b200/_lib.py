@@ -66,6 +66,15 @@ SIGNATURES = {
     "sincfft_nnfft_dist_colinv": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]),
     "sincfft_nnfft_dist_gather": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp]),
     "sincfft_nnfft_dist_support": (C.c_int, [_vp, _i64p, _vp]),
+    "sincfft_ipc_alloc": (C.c_int, [C.c_int32, C.c_int64, C.POINTER(_vp)]),
+    "sincfft_ipc_free": (C.c_int, [_vp]),
+    "sincfft_ipc_handle": (C.c_int, [_vp, C.POINTER(C.c_uint8)]),
+    "sincfft_ipc_open": (C.c_int, [C.c_int32, C.POINTER(C.c_uint8), C.POINTER(_vp)]),
+    "sincfft_ipc_close": (C.c_int, [_vp]),
+    "sincfft_nnfft_dist_colfwd_peer": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp,
+                                                 C.POINTER(C.c_uint64), _vp]),
+    "sincfft_nnfft_dist_rowmul_peer": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp,
+                                                 C.POINTER(C.c_uint64), _vp]),
     "sincfft_nnfft_dist_pack_rows": (C.c_int, [_vp, C.c_int32, _vp, C.c_int64, C.c_int64, _vp,
                                                _vp]),
     "sincfft_nnfft_dist_unpack_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _i64p, _i64p,

@@ -540,6 +540,64 @@ int sincfft_nnfft_dist_gather(sincfft_nnfft_plan plan, int32_t world, const doub
   });
 }
 
+// ---- peer-memory buffers (CUDA IPC; NVLink P2P between the GPUs of a node)
+int sincfft_ipc_alloc(int32_t device, int64_t bytes, void** ptr) {
+  return guarded([&] {
+    if (!ptr || bytes <= 0) sfb::fail(1, "ipc_alloc: bad arguments");
+    set_device(device);
+    SF_CUDA(cudaMalloc(ptr, (size_t)bytes));  // its own allocation: the handle covers it exactly
+  });
+}
+
+int sincfft_ipc_free(void* ptr) {
+  return guarded([&] { SF_CUDA(cudaFree(ptr)); });
+}
+
+int sincfft_ipc_handle(void* ptr, uint8_t* handle64) {
+  return guarded([&] {
+    if (!ptr || !handle64) sfb::fail(1, "NULL argument");
+    cudaIpcMemHandle_t h;
+    SF_CUDA(cudaIpcGetMemHandle(&h, ptr));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    std::memcpy(handle64, &h, sizeof(h));
+  });
+}
+
+int sincfft_ipc_open(int32_t device, const uint8_t* handle64, void** ptr) {
+  return guarded([&] {
+    if (!handle64 || !ptr) sfb::fail(1, "NULL argument");
+    set_device(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    SF_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int sincfft_ipc_close(void* ptr) {
+  return guarded([&] { SF_CUDA(cudaIpcCloseMemHandle(ptr)); });
+}
+
+int sincfft_nnfft_dist_colfwd_peer(sincfft_nnfft_plan plan, int32_t world, int32_t rank,
+                                   const double* block_dev, const uint64_t* peers,
+                                   void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!block_dev || !peers);
+    double2* pp[sfb::kDistMaxRanks] = {};
+    for (int q = 0; q < world && q < sfb::kDistMaxRanks; ++q) pp[q] = (double2*)peers[q];
+    sfb::run_dist_colfwd_peer(p, world, rank, (const double2*)block_dev, pp, s);
+  });
+}
+
+int sincfft_nnfft_dist_rowmul_peer(sincfft_nnfft_plan plan, int32_t world, int32_t rank,
+                                   double* rows_dev, const uint64_t* peers, void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!rows_dev || !peers);
+    double2* pp[sfb::kDistMaxRanks] = {};
+    for (int q = 0; q < world && q < sfb::kDistMaxRanks; ++q) pp[q] = (double2*)peers[q];
+    sfb::run_dist_rowmul_peer(p, world, rank, (double2*)rows_dev, pp, s);
+  });
+}
+
 int sincfft_nnfft_dist_support(sincfft_nnfft_plan plan, int64_t* out4, void* stream) {
   return guarded([&] {
     SF_DIST_PROLOGUE(!out4);

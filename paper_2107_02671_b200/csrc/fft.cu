@@ -835,7 +835,13 @@ struct DistArgs {
   FftArgs a;
   int rank, world;
   int64_t Bc, Br, I, K2, Sb;
-  int bc_log2;
+  int bc_log2, br_log2;
+  // fused transposes over peer memory (NVLink P2P / CUDA IPC): when set, the
+  // column pass and the row pass store every element straight into the
+  // receive buffer of the rank that owns it (the layout the all-to-all would
+  // have delivered), so no collective runs between the passes
+  int use_peers;
+  double2* peer[kDistMaxRanks];
 };
 
 __global__ void k_dpack(const double2* __restrict__ g, double2* __restrict__ S, DistArgs d) {
@@ -880,8 +886,11 @@ __global__ void __launch_bounds__(T, MINB) k_dcolfwd(DistArgs d, const double2* 
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int p = R * u + r;
-      Yc[((int64_t)p << d.bc_log2) + c] =
-          cmul(f.x[k][r], wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(p)));
+      const double2 v = cmul(f.x[k][r], wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(p)));
+      if (d.use_peers)  // row p belongs to rank p / Br: its block from this rank
+        d.peer[p >> d.br_log2][((((int64_t)d.rank << d.br_log2) + (p & (d.Br - 1))) << d.bc_log2) + c] = v;
+      else
+        Yc[((int64_t)p << d.bc_log2) + c] = v;
     }
   }
 }
@@ -917,7 +926,14 @@ __global__ void __launch_bounds__(T, MINB) k_drowmul(DistArgs d, double2* __rest
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
 #pragma unroll
-    for (int r = 0; r < R; ++r) Rr[at(F::template pos<S0>(u, r))] = cconj(f.x[k][r]);
+    for (int r = 0; r < R; ++r) {
+      const int n1 = F::template pos<S0>(u, r);
+      if (d.use_peers)  // column n1 belongs to rank n1 / Bc: block [this rank][pl][c]
+        d.peer[n1 >> d.bc_log2][((((int64_t)d.rank << d.br_log2) + pl) << d.bc_log2) +
+                                (n1 & (d.Bc - 1))] = cconj(f.x[k][r]);
+      else
+        Rr[at(n1)] = cconj(f.x[k][r]);
+    }
   }
 }
 
@@ -1894,6 +1910,8 @@ static DistArgs dist_args(const NnfftPlanImpl& p, int world, int rank) {
   d.K2 = l.K2;
   d.Sb = l.Sb;
   d.bc_log2 = log2i((int)l.Bc);
+  d.br_log2 = log2i((int)l.Br);
+  d.use_peers = 0;
   return d;
 }
 
@@ -2013,6 +2031,31 @@ void run_dist_unpack_hrows(const NnfftPlanImpl& p, int world, const double2* rec
   const DistArgs d = dist_args(p, world, 0);
   const int64_t n = world * cnt * d.Bc;
   k_dunpack_hrows<<<(unsigned)ceil_div(n, (int64_t)256), 256, 0, s>>>(recv, h, d, k2lo, cnt);
+  SF_LAUNCH_CHECK();
+}
+
+
+void run_dist_colfwd_peer(const NnfftPlanImpl& p, int world, int rank, const double2* R,
+                          double2* const* peers, cudaStream_t s) {
+  DistArgs d = dist_args(p, world, rank);
+  if (world > kDistMaxRanks) fail(1, "peer transposes: at most 16 ranks");
+  d.use_peers = 1;
+  for (int q = 0; q < world; ++q) d.peer[q] = peers[q];
+  if (col16(p.fft))
+    k_dcolfwd<1024, 1, 128, 4, 16><<<(unsigned)(d.Bc / 2), 128, sizeof(double2) * 2048, s>>>(d, R, nullptr);
+  else
+    k_dcolfwd<1024, 1, 256, 4><<<(unsigned)(d.Bc / 2), 256, sizeof(double2) * 2048, s>>>(d, R, nullptr);
+  SF_LAUNCH_CHECK();
+}
+
+void run_dist_rowmul_peer(const NnfftPlanImpl& p, int world, int rank, double2* Rr,
+                          double2* const* peers, cudaStream_t s) {
+  DistArgs d = dist_args(p, world, rank);
+  if (world > kDistMaxRanks) fail(1, "peer transposes: at most 16 ranks");
+  d.use_peers = 1;
+  for (int q = 0; q < world; ++q) d.peer[q] = peers[q];
+  if (row16(p.fft)) k_drowmul<4096, 256, 2, 16><<<(unsigned)d.Br, 256, sizeof(double2) * 4096, s>>>(d, Rr);
+  else k_drowmul<4096, 256, 2><<<(unsigned)d.Br, 256, sizeof(double2) * 4096, s>>>(d, Rr);
   SF_LAUNCH_CHECK();
 }
 

@@ -227,6 +227,12 @@ void run_dist_pack(const NnfftPlanImpl& p, int world, const double2* grid, doubl
 void run_dist_colfwd(const NnfftPlanImpl& p, int world, int rank, const double2* R, double2* Yc,
                      cudaStream_t s);
 void run_dist_rowmul(const NnfftPlanImpl& p, int world, int rank, double2* Rr, cudaStream_t s);
+// the same two passes storing straight into the owners' receive buffers
+// (peers[q]: rank q's buffer, this process's view; the all-to-all layouts)
+void run_dist_colfwd_peer(const NnfftPlanImpl& p, int world, int rank, const double2* R,
+                          double2* const* peers, cudaStream_t s);
+void run_dist_rowmul_peer(const NnfftPlanImpl& p, int world, int rank, double2* Rr,
+                          double2* const* peers, cudaStream_t s);
 void run_dist_colinv(const NnfftPlanImpl& p, int world, int rank, const double2* Y2,
                      const double2* R, double2* H, cudaStream_t s);
 void run_dist_unpack(const NnfftPlanImpl& p, int world, const double2* Hall, double2* h,

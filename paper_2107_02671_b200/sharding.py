@@ -445,3 +445,157 @@ def run_sparse_ranks_in_process(ranks, f_shards):
     hblks = [r.colinv(x) for r, x in zip(ranks, a2a(rws))]
     recv2 = a2av([r.pack_hrows(h) for r, h in zip(ranks, hblks)], rows.h_send_splits)
     return [r.gather_rows(x) for r, x in zip(ranks, recv2)]
+
+
+# --------------------------------------- fused transposes over peer memory
+def _u64(ptrs):
+    import ctypes as C
+    return (C.c_uint64 * len(ptrs))(*[int(p) for p in ptrs])
+
+
+class PeerDistFftRank(SparseDistFftRank):
+    """SparseDistFftRank whose two middle all-to-alls are fused into the passes:
+    the column pass stores each element into the row-owner's receive buffer,
+    the row pass into the column-owner's (``sincfft_nnfft_dist_colfwd_peer`` /
+    ``_rowmul_peer``; the buffers are mapped over NVLink with CUDA IPC)."""
+
+    def colfwd_peer(self, block, rows_ptrs):
+        from . import _lib
+        self.block = block
+        _lib.check(_lib.lib.sincfft_nnfft_dist_colfwd_peer(
+            self.plan.handle, self.world, self.rank, block.data_ptr(), _u64(rows_ptrs),
+            self._s()))
+
+    def rowmul_peer(self, rows_ptr, cols2_ptrs):
+        from . import _lib
+        _lib.check(_lib.lib.sincfft_nnfft_dist_rowmul_peer(
+            self.plan.handle, self.world, self.rank, rows_ptr, _u64(cols2_ptrs), self._s()))
+
+    def colinv_ptr(self, cols2_ptr):
+        from . import _lib
+        hblk = self._empty(self.layout["hblk"])
+        _lib.check(_lib.lib.sincfft_nnfft_dist_colinv(self.plan.handle, self.world, self.rank,
+                                                      cols2_ptr, self.block.data_ptr(),
+                                                      hblk.data_ptr(), self._s()))
+        return hblk
+
+
+class IpcBuffer:
+    """A device buffer of this rank mapped into every other rank (CUDA IPC):
+    ``ptrs[q]`` is rank q's buffer as seen from this process."""
+
+    def __init__(self, device, nbytes, coll):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+        self.device = device
+        p = C.c_void_p()
+        _lib.check(_lib.lib.sincfft_ipc_alloc(device, int(nbytes), C.byref(p)))
+        self.own = p.value
+        h = (C.c_uint8 * 64)()
+        _lib.check(_lib.lib.sincfft_ipc_handle(C.c_void_p(self.own), h))
+        mine = torch.tensor(list(bytes(h)), dtype=torch.uint8,
+                            device=torch.device("cuda", device) if coll.nccl else "cpu")
+        allh = [torch.zeros_like(mine) for _ in range(coll.world)]
+        dist.all_gather(allh, mine, group=coll.group)
+        self.ptrs, self._opened = [], []
+        for q, t in enumerate(allh):
+            if q == coll.rank:
+                self.ptrs.append(self.own)
+                continue
+            hq = (C.c_uint8 * 64)(*t.cpu().tolist())
+            pq = C.c_void_p()
+            _lib.check(_lib.lib.sincfft_ipc_open(device, hq, C.byref(pq)))
+            self.ptrs.append(pq.value)
+            self._opened.append(pq.value)
+
+    def close(self):
+        import ctypes as C
+
+        from . import _lib
+        for p in self._opened:
+            _lib.lib.sincfft_ipc_close(C.c_void_p(p))
+        self._opened = []
+        if self.own:
+            _lib.lib.sincfft_ipc_free(C.c_void_p(self.own))
+            self.own = None
+
+
+class PeerDistributedFftNnfft:
+    """The sparse-exchange distributed FFT with the two transposes fused into
+    the column and row passes over peer memory: per transform two all-to-alls
+    (grid rows in, h rows out) and two stream-ordered barriers instead of four
+    collectives."""
+
+    def __init__(self, plan, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.coll = TorchCollectives(group)
+        self.r = PeerDistFftRank(plan, self.coll.world, self.coll.rank)
+        mine = torch.tensor(self.r.support(), dtype=torch.int64,
+                            device=self.r.dev if self.coll.nccl else "cpu")
+        allsup = [torch.zeros_like(mine) for _ in range(self.coll.world)]
+        dist.all_gather(allsup, mine, group=group)
+        self.r.set_rows(sparse_rows_for([a.tolist() for a in allsup], self.r))
+        nbytes = 16 * self.r.layout["cols"]
+        self.rows = IpcBuffer(plan.device, nbytes, self.coll)
+        self.cols2 = IpcBuffer(plan.device, nbytes, self.coll)
+        self._flag = torch.zeros(1, dtype=torch.float64, device=self.r.dev)
+
+    def _barrier(self):
+        """Every rank's peer stores have landed: a stream-ordered all-reduce
+        (NCCL) or a host barrier (other backends)."""
+        import torch
+        import torch.distributed as dist
+        if self.coll.nccl:
+            dist.all_reduce(self._flag, group=self.coll.group)
+        else:
+            torch.cuda.synchronize(self.r.dev)
+            dist.barrier(group=self.coll.group)
+
+    def __call__(self, f_shard):
+        r, c, rw, k = self.r, self.coll, self.r.rows, self.coll.rank
+        recv = _all_to_all_v(c, r.pack_rows(f_shard), rw.grid_send_splits(k),
+                             rw.grid_recv_splits(k))
+        r.colfwd_peer(r.unpack_rows(recv), self.rows.ptrs)
+        self._barrier()
+        r.rowmul_peer(self.rows.own, self.cols2.ptrs)
+        self._barrier()
+        hblk = r.colinv_ptr(self.cols2.own)
+        recv2 = _all_to_all_v(c, r.pack_hrows(hblk), rw.h_send_splits(k), rw.h_recv_splits(k))
+        return r.gather_rows(recv2)
+
+    def close(self):
+        self.rows.close()
+        self.cols2.close()
+
+
+def run_peer_ranks_in_process(ranks, f_shards):
+    """run_sparse_ranks_in_process with the fused peer transposes: all ranks in
+    one process, so a rank's 'peer' buffers are simply the others' tensors."""
+    import torch
+
+    world = len(ranks)
+    rows = sparse_rows_for([r.support() for r in ranks], ranks[0])
+    for r in ranks:
+        r.set_rows(rows)
+
+    def a2av(sends, send_splits):
+        chunks = [list(torch.split(s, send_splits(i))) for i, s in enumerate(sends)]
+        return [torch.cat([chunks[src][dst] for src in range(world)]) for dst in range(world)]
+
+    recv = a2av([r.pack_rows(f) for r, f in zip(ranks, f_shards)], rows.grid_send_splits)
+    blocks = [r.unpack_rows(x) for r, x in zip(ranks, recv)]
+    rbuf = [r._empty(r.layout["cols"]) for r in ranks]
+    cbuf = [r._empty(r.layout["cols"]) for r in ranks]
+    for r, b in zip(ranks, blocks):
+        r.colfwd_peer(b, [x.data_ptr() for x in rbuf])
+    for r, x in zip(ranks, rbuf):
+        r.rowmul_peer(x.data_ptr(), [y.data_ptr() for y in cbuf])
+    hblks = [r.colinv_ptr(y.data_ptr()) for r, y in zip(ranks, cbuf)]
+    recv2 = a2av([r.pack_hrows(h) for r, h in zip(ranks, hblks)], rows.h_send_splits)
+    return [r.gather_rows(x) for r, x in zip(ranks, recv2)]
