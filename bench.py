@@ -630,8 +630,11 @@ def run_b200(args, cfg):
     launches = L.sincfft_nnfft_launches_per_execute(ph, B) * args.steps
     if dist_fft is not None:  # grid memset + spread, pack (+ tail fix), 3 passes
         fix = 1 if geo["L"] < geo["K"] + geo["Kout"] - 1 else 0  # (+ rank-0 fix add), unpack, gather
-        launches = (2 + 1 + fix + 3 + (fix if rank == 0 else 0) + 1 + 1
-                    + (0 if args.dense_exchange else 2)) * args.steps  # + unpack_rows, pack_hrows
+        if args.dense_exchange or args.no_peer_transposes:
+            launches = (2 + 1 + fix + 3 + (fix if rank == 0 else 0) + 1 + 1
+                        + (0 if args.dense_exchange else 2)) * args.steps
+        else:  # memset, spread, pack (+fix) to peers, unpack, 3 passes, unpack h, gather
+            launches = (2 + 1 + fix + 1 + 3 + 1 + 1) * args.steps
     fp64_peak, fp64_note = 148 * 64 * 2 * (clk.max_mhz or 1965) * 1e6 / 1e12, \
         "derived: 148 SMs x 64 DFMA/clk x 2 flops x max SM clock"
     pf = os.path.join(ROOT, "profiles", "fp64_peak.json")
@@ -664,9 +667,9 @@ def run_b200(args, cfg):
                                                    if args.dense_exchange else
                                                    "4 all-to-alls (grid / h rows exchanged "
                                                    "sparsely)" if args.no_peer_transposes else
-                                                   "grid / h rows all-to-all (sparse), the two "
-                                                   "transposes fused into the passes over peer "
-                                                   "memory (CUDA IPC)")
+                                                   "every exchange fused into the kernels as "
+                                                   "stores into the owners' buffers over peer "
+                                                   "memory (CUDA IPC), 4 barriers")
                          if dist_fft is not None else ", NCCL all-reduce of the K-grid")
                         if world > 1 and not col_shard else "")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,

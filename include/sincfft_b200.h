@@ -211,6 +211,22 @@ SINCFFT_API int sincfft_nnfft_dist_colfwd_peer(sincfft_nnfft_plan plan, int32_t 
 SINCFFT_API int sincfft_nnfft_dist_rowmul_peer(sincfft_nnfft_plan plan, int32_t world,
                                                int32_t rank, double *rows_dev,
                                                const uint64_t *peers, void *stream);
+/* The first and last exchanges fused the same way: pack_rows_peer writes
+ * chunk q straight into receiver q's grid-row buffer at poff[q] (this
+ * sender's offset there; chunks to rank 0 carry the tail fix), and
+ * colinv_peer stores each h row into every rank r whose targets read it
+ * (rows [k2lo[r], k2lo[r] + cnt[r]), receiver layout [sender][row][c]);
+ * rank 0 adds the summed tail fix from its block.  Barrier after each. */
+SINCFFT_API int sincfft_nnfft_dist_pack_rows_peer(sincfft_nnfft_plan plan, int32_t world,
+                                                  int32_t rank, const double *grid_dev,
+                                                  int64_t ilo, int64_t nrow,
+                                                  const uint64_t *peers, const int64_t *poff,
+                                                  void *stream);
+SINCFFT_API int sincfft_nnfft_dist_colinv_peer(sincfft_nnfft_plan plan, int32_t world,
+                                               int32_t rank, const double *cols_dev,
+                                               const double *block_dev, const uint64_t *peers,
+                                               const int64_t *k2lo, const int64_t *cnt,
+                                               void *stream);
 
 /* Observability: one execute with DEVICE pointers and CUDA events recorded
  * on `stream` between the stages; returns after synchronizing the stream

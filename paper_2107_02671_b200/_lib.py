@@ -75,6 +75,11 @@ SIGNATURES = {
                                                  C.POINTER(C.c_uint64), _vp]),
     "sincfft_nnfft_dist_rowmul_peer": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp,
                                                  C.POINTER(C.c_uint64), _vp]),
+    "sincfft_nnfft_dist_pack_rows_peer": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int64,
+                                                    C.c_int64, C.POINTER(C.c_uint64), _i64p,
+                                                    _vp]),
+    "sincfft_nnfft_dist_colinv_peer": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp,
+                                                 C.POINTER(C.c_uint64), _i64p, _i64p, _vp]),
     "sincfft_nnfft_dist_pack_rows": (C.c_int, [_vp, C.c_int32, _vp, C.c_int64, C.c_int64, _vp,
                                                _vp]),
     "sincfft_nnfft_dist_unpack_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _i64p, _i64p,

@@ -598,6 +598,30 @@ int sincfft_nnfft_dist_rowmul_peer(sincfft_nnfft_plan plan, int32_t world, int32
   });
 }
 
+int sincfft_nnfft_dist_pack_rows_peer(sincfft_nnfft_plan plan, int32_t world, int32_t rank,
+                                      const double* grid_dev, int64_t ilo, int64_t nrow,
+                                      const uint64_t* peers, const int64_t* poff, void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!grid_dev || !peers || !poff);
+    double2* pp[sfb::kDistMaxRanks] = {};
+    for (int q = 0; q < world && q < sfb::kDistMaxRanks; ++q) pp[q] = (double2*)peers[q];
+    sfb::run_dist_pack_rows_peer(p, world, rank, (const double2*)grid_dev, ilo, nrow, pp, poff, s);
+  });
+}
+
+int sincfft_nnfft_dist_colinv_peer(sincfft_nnfft_plan plan, int32_t world, int32_t rank,
+                                   const double* cols_dev, const double* block_dev,
+                                   const uint64_t* peers, const int64_t* k2lo,
+                                   const int64_t* cnt, void* stream) {
+  return guarded([&] {
+    SF_DIST_PROLOGUE(!cols_dev || !block_dev || !peers || !k2lo || !cnt);
+    double2* pp[sfb::kDistMaxRanks] = {};
+    for (int q = 0; q < world && q < sfb::kDistMaxRanks; ++q) pp[q] = (double2*)peers[q];
+    sfb::run_dist_colinv_peer(p, world, rank, (const double2*)cols_dev,
+                              (const double2*)block_dev, pp, k2lo, cnt, s);
+  });
+}
+
 int sincfft_nnfft_dist_support(sincfft_nnfft_plan plan, int64_t* out4, void* stream) {
   return guarded([&] {
     SF_DIST_PROLOGUE(!out4);

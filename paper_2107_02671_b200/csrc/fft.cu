@@ -842,6 +842,12 @@ struct DistArgs {
   // have delivered), so no collective runs between the passes
   int use_peers;
   double2* peer[kDistMaxRanks];
+  // fused first / last exchanges: this sender's chunk offset in each
+  // receiver's grid-row buffer; every receiver's h-row range; rank 0's fix
+  int64_t poff[kDistMaxRanks];
+  int64_t hlo[kDistMaxRanks], hcnt[kDistMaxRanks];
+  const double2* fixp;
+  int64_t fixD;
 };
 
 __global__ void k_dpack(const double2* __restrict__ g, double2* __restrict__ S, DistArgs d) {
@@ -967,7 +973,17 @@ __global__ void __launch_bounds__(T, MINB) k_dcolinv(DistArgs d, const double2* 
       const int64_t k2 = F::template pos<S0>(u, r);
       const int64_t kk = n1 + a.L1 * k2;
       if (k2 < d.K2 && kk < a.Kout) {
-        H[(k2 << d.bc_log2) + c] = cmul(cconj(f.x[k][r]), __ldg(a.Q + kk));
+        double2 v = cmul(cconj(f.x[k][r]), __ldg(a.Q + kk));
+        if (d.use_peers) {  // straight into every rank whose targets read h row k2
+          if (d.fixp && kk < d.fixD) v = cadd(v, d.fixp[kk]);  // rank 0: the Bluestein tail fix
+          for (int q = 0; q < d.world; ++q) {
+            const int64_t lk = k2 - d.hlo[q];
+            if (lk >= 0 && lk < d.hcnt[q])
+              d.peer[q][((d.rank * d.hcnt[q] + lk) << d.bc_log2) + c] = v;
+          }
+        } else {
+          H[(k2 << d.bc_log2) + c] = v;
+        }
       }
     }
   }
@@ -1014,7 +1030,8 @@ __global__ void k_dpack_rows(const double2* __restrict__ g, double2* __restrict_
     const int64_t n = q * d.Bc + c + d.a.L1 * i;
     if (n < d.a.K) v = g[n];
   }
-  S[o] = v;
+  if (d.use_peers) d.peer[q][d.poff[q] + e] = v;  // straight into receiver q's buffer
+  else S[o] = v;
 }
 
 __global__ void k_dunpack_rows(const double2* __restrict__ recv, double2* __restrict__ R,
@@ -1912,6 +1929,8 @@ static DistArgs dist_args(const NnfftPlanImpl& p, int world, int rank) {
   d.bc_log2 = log2i((int)l.Bc);
   d.br_log2 = log2i((int)l.Br);
   d.use_peers = 0;
+  d.fixp = nullptr;
+  d.fixD = p.fft.fixD;
   return d;
 }
 
@@ -2056,6 +2075,43 @@ void run_dist_rowmul_peer(const NnfftPlanImpl& p, int world, int rank, double2* 
   for (int q = 0; q < world; ++q) d.peer[q] = peers[q];
   if (row16(p.fft)) k_drowmul<4096, 256, 2, 16><<<(unsigned)d.Br, 256, sizeof(double2) * 4096, s>>>(d, Rr);
   else k_drowmul<4096, 256, 2><<<(unsigned)d.Br, 256, sizeof(double2) * 4096, s>>>(d, Rr);
+  SF_LAUNCH_CHECK();
+}
+
+
+void run_dist_pack_rows_peer(const NnfftPlanImpl& p, int world, int rank, const double2* grid,
+                             int64_t ilo, int64_t nrow, double2* const* peers,
+                             const int64_t* poff, cudaStream_t s) {
+  DistArgs d = dist_args(p, world, rank);
+  if (world > kDistMaxRanks) fail(1, "peer exchange: at most 16 ranks");
+  d.use_peers = 1;
+  for (int q = 0; q < world; ++q) d.peer[q] = peers[q], d.poff[q] = poff[q];
+  const int64_t dpad = dist_dpad(p);
+  const int64_t total = world * nrow * d.Bc + dpad;
+  k_dpack_rows<<<(unsigned)ceil_div(total, (int64_t)256), 256, 0, s>>>(grid, nullptr, d, ilo,
+                                                                    nrow, dpad);
+  SF_LAUNCH_CHECK();
+  const FftPlan& f = p.fft;
+  if (f.fixD > 0) {  // this rank's tail-fix partial, into rank 0's buffer after its rows
+    k_bluestein_fix<<<dim3((unsigned)ceil_div(f.fixD * 32, 256), 1), 256, 0, s>>>(
+        grid, f.P.p, f.fixc.p, f.Q.p, peers[0] + poff[0] + nrow * d.Bc, p.g.K, f.fixD, f.Kout, 0,
+        1, 0);
+    SF_LAUNCH_CHECK();
+  }
+}
+
+void run_dist_colinv_peer(const NnfftPlanImpl& p, int world, int rank, const double2* Y2,
+                          const double2* R, double2* const* peers, const int64_t* k2lo,
+                          const int64_t* cnt, cudaStream_t s) {
+  DistArgs d = dist_args(p, world, rank);
+  if (world > kDistMaxRanks) fail(1, "peer exchange: at most 16 ranks");
+  d.use_peers = 1;
+  for (int q = 0; q < world; ++q) d.peer[q] = peers[q], d.hlo[q] = k2lo[q], d.hcnt[q] = cnt[q];
+  d.fixp = (rank == 0 && p.fft.fixD > 0) ? R + d.I * d.Bc : nullptr;
+  if (col16(p.fft))
+    k_dcolinv<1024, 1, 128, 4, 16><<<(unsigned)(d.Bc / 2), 128, sizeof(double2) * 2048, s>>>(d, Y2, nullptr);
+  else
+    k_dcolinv<1024, 1, 256, 4><<<(unsigned)(d.Bc / 2), 256, sizeof(double2) * 2048, s>>>(d, Y2, nullptr);
   SF_LAUNCH_CHECK();
 }
 

@@ -233,6 +233,15 @@ void run_dist_colfwd_peer(const NnfftPlanImpl& p, int world, int rank, const dou
                           double2* const* peers, cudaStream_t s);
 void run_dist_rowmul_peer(const NnfftPlanImpl& p, int world, int rank, double2* Rr,
                           double2* const* peers, cudaStream_t s);
+// fused first / last exchanges: pack the grid rows into every receiver's
+// buffer at this sender's offsets; the inverse column pass stores h rows into
+// every rank whose targets read them (rank 0 adds the summed tail fix)
+void run_dist_pack_rows_peer(const NnfftPlanImpl& p, int world, int rank, const double2* grid,
+                             int64_t ilo, int64_t nrow, double2* const* peers,
+                             const int64_t* poff, cudaStream_t s);
+void run_dist_colinv_peer(const NnfftPlanImpl& p, int world, int rank, const double2* Y2,
+                          const double2* R, double2* const* peers, const int64_t* k2lo,
+                          const int64_t* cnt, cudaStream_t s);
 void run_dist_colinv(const NnfftPlanImpl& p, int world, int rank, const double2* Y2,
                      const double2* R, double2* H, cudaStream_t s);
 void run_dist_unpack(const NnfftPlanImpl& p, int world, const double2* Hall, double2* h,

@@ -471,6 +471,56 @@ class PeerDistFftRank(SparseDistFftRank):
         _lib.check(_lib.lib.sincfft_nnfft_dist_rowmul_peer(
             self.plan.handle, self.world, self.rank, rows_ptr, _u64(cols2_ptrs), self._s()))
 
+    def grid_offsets(self):
+        """poff[q]: this rank's chunk offset in receiver q's grid-row buffer."""
+        rw, out = self.rows, []
+        for q in range(self.world):
+            extra = rw.Dpad if q == 0 else 0
+            out.append(sum(rw.nrow[s] * rw.Bc + extra for s in range(self.rank)))
+        return out
+
+    def grid_recv_elems(self):
+        return sum(self.rows.grid_recv_splits(self.rank))
+
+    def h_recv_elems(self):
+        return sum(self.rows.h_recv_splits(self.rank))
+
+    def pack_rows_peer(self, f, grid_ptrs):
+        from . import _lib
+        grid = self._empty(self.geo["K"])
+        _lib.check(_lib.lib.sincfft_nnfft_spread(self.plan.handle, f.data_ptr(), grid.data_ptr(),
+                                                 1, _lib.PTR_DEVICE, self._s()))
+        rw, r = self.rows, self.rank
+        _lib.check(_lib.lib.sincfft_nnfft_dist_pack_rows_peer(
+            self.plan.handle, self.world, r, grid.data_ptr(), rw.ilo[r], rw.nrow[r],
+            _u64(grid_ptrs), _i64(self.grid_offsets()), self._s()))
+        self._grid_keep = grid  # alive until the stream passes the barrier
+
+    def unpack_rows_ptr(self, recv_ptr):
+        from . import _lib
+        rw = self.rows
+        block = self._empty(self.layout["Sb"])
+        _lib.check(_lib.lib.sincfft_nnfft_dist_unpack_rows(
+            self.plan.handle, self.world, self.rank, recv_ptr, _i64(rw.ilo), _i64(rw.nrow),
+            block.data_ptr(), self._s()))
+        return block
+
+    def colinv_peer(self, cols2_ptr, h_ptrs):
+        from . import _lib
+        rw = self.rows
+        _lib.check(_lib.lib.sincfft_nnfft_dist_colinv_peer(
+            self.plan.handle, self.world, self.rank, cols2_ptr, self.block.data_ptr(),
+            _u64(h_ptrs), _i64(rw.k2lo), _i64(rw.cnt), self._s()))
+
+    def gather_rows_ptr(self, recv_ptr):
+        from . import _lib
+        rw, r = self.rows, self.rank
+        out = self._empty(self.geo["M2"])
+        _lib.check(_lib.lib.sincfft_nnfft_dist_gather_rows(
+            self.plan.handle, self.world, recv_ptr, rw.k2lo[r], rw.cnt[r], out.data_ptr(),
+            self._s()))
+        return out
+
     def colinv_ptr(self, cols2_ptr):
         from . import _lib
         hblk = self._empty(self.layout["hblk"])
@@ -525,10 +575,11 @@ class IpcBuffer:
 
 
 class PeerDistributedFftNnfft:
-    """The sparse-exchange distributed FFT with the two transposes fused into
-    the column and row passes over peer memory: per transform two all-to-alls
-    (grid rows in, h rows out) and two stream-ordered barriers instead of four
-    collectives."""
+    """The distributed FFT with every exchange fused into a kernel over peer
+    memory: the grid rows are packed straight into their owners' buffers, the
+    two transposes are the column / row passes' stores, and the inverse column
+    pass stores each h row into every rank whose targets read it.  Per
+    transform: four stream-ordered barriers and no data collective."""
 
     def __init__(self, plan, group=None):
         import torch
@@ -541,9 +592,11 @@ class PeerDistributedFftNnfft:
         allsup = [torch.zeros_like(mine) for _ in range(self.coll.world)]
         dist.all_gather(allsup, mine, group=group)
         self.r.set_rows(sparse_rows_for([a.tolist() for a in allsup], self.r))
-        nbytes = 16 * self.r.layout["cols"]
-        self.rows = IpcBuffer(plan.device, nbytes, self.coll)
-        self.cols2 = IpcBuffer(plan.device, nbytes, self.coll)
+        cols = 16 * self.r.layout["cols"]
+        self.gridrecv = IpcBuffer(plan.device, 16 * self.r.grid_recv_elems(), self.coll)
+        self.rows = IpcBuffer(plan.device, cols, self.coll)
+        self.cols2 = IpcBuffer(plan.device, cols, self.coll)
+        self.hrecv = IpcBuffer(plan.device, 16 * self.r.h_recv_elems(), self.coll)
         self._flag = torch.zeros(1, dtype=torch.float64, device=self.r.dev)
 
     def _barrier(self):
@@ -558,44 +611,41 @@ class PeerDistributedFftNnfft:
             dist.barrier(group=self.coll.group)
 
     def __call__(self, f_shard):
-        r, c, rw, k = self.r, self.coll, self.r.rows, self.coll.rank
-        recv = _all_to_all_v(c, r.pack_rows(f_shard), rw.grid_send_splits(k),
-                             rw.grid_recv_splits(k))
-        r.colfwd_peer(r.unpack_rows(recv), self.rows.ptrs)
+        r = self.r
+        r.pack_rows_peer(f_shard, self.gridrecv.ptrs)
+        self._barrier()
+        r.colfwd_peer(r.unpack_rows_ptr(self.gridrecv.own), self.rows.ptrs)
         self._barrier()
         r.rowmul_peer(self.rows.own, self.cols2.ptrs)
         self._barrier()
-        hblk = r.colinv_ptr(self.cols2.own)
-        recv2 = _all_to_all_v(c, r.pack_hrows(hblk), rw.h_send_splits(k), rw.h_recv_splits(k))
-        return r.gather_rows(recv2)
+        r.colinv_peer(self.cols2.own, self.hrecv.ptrs)
+        self._barrier()
+        return r.gather_rows_ptr(self.hrecv.own)
 
     def close(self):
-        self.rows.close()
-        self.cols2.close()
+        for b in (self.gridrecv, self.rows, self.cols2, self.hrecv):
+            b.close()
 
 
 def run_peer_ranks_in_process(ranks, f_shards):
-    """run_sparse_ranks_in_process with the fused peer transposes: all ranks in
-    one process, so a rank's 'peer' buffers are simply the others' tensors."""
-    import torch
-
+    """PeerDistributedFftNnfft with all ranks in one process (one GPU): a
+    rank's 'peer' buffers are simply the other ranks' tensors."""
     world = len(ranks)
     rows = sparse_rows_for([r.support() for r in ranks], ranks[0])
     for r in ranks:
         r.set_rows(rows)
-
-    def a2av(sends, send_splits):
-        chunks = [list(torch.split(s, send_splits(i))) for i, s in enumerate(sends)]
-        return [torch.cat([chunks[src][dst] for src in range(world)]) for dst in range(world)]
-
-    recv = a2av([r.pack_rows(f) for r, f in zip(ranks, f_shards)], rows.grid_send_splits)
-    blocks = [r.unpack_rows(x) for r, x in zip(ranks, recv)]
+    gbuf = [r._empty(r.grid_recv_elems()) for r in ranks]
     rbuf = [r._empty(r.layout["cols"]) for r in ranks]
     cbuf = [r._empty(r.layout["cols"]) for r in ranks]
-    for r, b in zip(ranks, blocks):
-        r.colfwd_peer(b, [x.data_ptr() for x in rbuf])
+    hbuf = [r._empty(r.h_recv_elems()) for r in ranks]
+    ptrs = lambda bufs: [x.data_ptr() for x in bufs]  # noqa: E731
+    for r, f in zip(ranks, f_shards):
+        r.pack_rows_peer(f, ptrs(gbuf))
+    for r, g in zip(ranks, gbuf):
+        r.colfwd_peer(r.unpack_rows_ptr(g.data_ptr()), ptrs(rbuf))
     for r, x in zip(ranks, rbuf):
-        r.rowmul_peer(x.data_ptr(), [y.data_ptr() for y in cbuf])
-    hblks = [r.colinv_ptr(y.data_ptr()) for r, y in zip(ranks, cbuf)]
-    recv2 = a2av([r.pack_hrows(h) for r, h in zip(ranks, hblks)], rows.h_send_splits)
-    return [r.gather_rows(x) for r, x in zip(ranks, recv2)]
+        r.rowmul_peer(x.data_ptr(), ptrs(cbuf))
+    for r, y in zip(ranks, cbuf):
+        r.colinv_peer(y.data_ptr(), ptrs(hbuf))
+    assert world == len(hbuf)
+    return [r.gather_rows_ptr(h.data_ptr()) for r, h in zip(ranks, hbuf)]
