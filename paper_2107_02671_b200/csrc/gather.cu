@@ -127,6 +127,9 @@ __device__ __forceinline__ double2 gather_one(const GatherArgs& a, const double2
   return s;
 }
 
+#ifndef SFB_GATHER_TMA
+#define SFB_GATHER_TMA 1  // the h span staged by one TMA bulk copy
+#endif
 #ifndef SFB_GATHER2_MINB
 #define SFB_GATHER2_MINB (8 * 128 / SFB_GATHER_THREADS)  // 64 registers (0.381 -> 0.299 ms at config 3)
 #endif
@@ -163,6 +166,19 @@ __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(Ga
     }
   }
   pdl_wait();  // h is the previous kernel's output
+#if SFB_GATHER_TMA
+  // the span is one contiguous range: one bulk copy on the TMA engine,
+  // completing on an mbarrier (no per-thread copy instructions)
+  __shared__ __align__(8) unsigned long long mbar;
+  if (staged && threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    bulk_g2s(hs, h + klo, (unsigned)((khi - klo + 1) * sizeof(double2)), &mbar);
+  }
+  if (staged) {
+    __syncthreads();  // the barrier is initialised before anyone polls it
+    mbar_wait(&mbar, 0);
+  }
+#else
   if (staged) {
     for (int64_t i = threadIdx.x; i <= khi - klo; i += kGatherThreads)
       cp_async16(hs + i, h + klo + i);
@@ -172,6 +188,7 @@ __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(Ga
     cp_async_wait<0>();
     __syncthreads();
   }
+#endif
   if (dst[0] < 0) return;
   const double sg = a.conj_out ? -1.0 : 1.0;
 #pragma unroll
