@@ -33,6 +33,11 @@
 #include "nnfft_impl.cuh"
 #include "fft_reg.cuh"
 
+#ifndef SFB_FFT_ROW_TMA
+#define SFB_FFT_ROW_TMA 0  // 1: the config-3 row staged by one TMA bulk copy (measured
+                           // 0.174 -> 0.176 ms: the extra barrier; kept off)
+#endif
+
 namespace sfb {
 
 constexpr int kSingleMax = 8192;      // largest L done by one CTA
@@ -752,12 +757,32 @@ __global__ void __launch_bounds__(T, MINB) k_rowmul_r1(FftArgs a) {
   const int64_t p = blockIdx.x;
   double2* row = a.Y + (int64_t)col * a.L + p * a.L1;
   F f;
+#if SFB_FFT_ROW_TMA
+  // the row is one contiguous 64 KB range: one TMA bulk copy into the
+  // exchange buffer (linear layout), stage-0 legs read from it, one barrier
+  // before the first (swizzled) exchange reuses the buffer
+  __shared__ __align__(8) unsigned long long mbar;
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    bulk_g2s(sm, row, (unsigned)(sizeof(double2) * N), &mbar);
+  }
+  __syncthreads();
+  mbar_wait(&mbar, 0);
+#pragma unroll
+  for (int k = 0; k < F::BPT; ++k) {
+    const int u = F::but(k);
+#pragma unroll
+    for (int r = 0; r < R; ++r) f.x[k][r] = sm[F::template pos<S0>(u, r)];
+  }
+  __syncthreads();
+#else
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
 #pragma unroll
     for (int r = 0; r < R; ++r) f.x[k][r] = row[F::template pos<S0>(u, r)];
   }
+#endif
   f.dif(sm, R == 16 ? a.st1x : a.st1, R == 16 ? a.tw1x : a.tw1);
   const double2* Bh = (R == 16 ? a.Bhatx : a.Bhat) + p * a.L1;
 #pragma unroll
