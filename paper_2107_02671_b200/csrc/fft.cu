@@ -1131,6 +1131,10 @@ struct DirectArgs {
   int p_smooth;
   int conj_in;
   FftStages stA, stP;
+  // Rader rows (P prime, P - 1 smooth): input gather g^q, output scatter g^-q
+  int rader;
+  const int* rin;
+  const int* rout;
 };
 
 __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_dstep1(DirectArgs a) {
@@ -1194,6 +1198,7 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_dstep1(DirectArgs a) {
 
 __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_dstep2(DirectArgs a) {
   extern __shared__ double2 sm[];
+  __shared__ double2 y0s[64], a0s[64];  // Rader: y[0] and sum_{n>0} y[n] per row
   const int col = blockIdx.y;
   const int R = 1 << a.R_log2;
   const int64_t r0 = (int64_t)blockIdx.x * R;
@@ -1201,7 +1206,8 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_dstep2(DirectArgs a) {
   const int n_el = n << a.R_log2;
   const int T = blockDim.x;
   const double2* Y = a.Y + (int64_t)col * a.A * a.P;
-  // load rows r0.. (element (n2, row b) at e = n2 * R + b), Bluestein pre-chirp
+  // load rows r0.. (element (n2, row b) at e = n2 * R + b): Bluestein
+  // pre-chirp, or the Rader gather a_q = y[g^q mod P], q < P - 1
   for (int e0 = threadIdx.x; e0 < n_el; e0 += kU * T) {
     double2 v[kU];
 #pragma unroll
@@ -1210,7 +1216,9 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_dstep2(DirectArgs a) {
       const int64_t k1 = r0 + (e & (R - 1));
       const int n2 = e >> a.R_log2;
       v[u] = make_double2(0.0, 0.0);
-      if (e < n_el && k1 < a.A && n2 < a.P) {
+      if (a.rader) {
+        if (e < n_el && k1 < a.A) v[u] = Y[k1 * a.P + __ldg(a.rin + n2)];
+      } else if (e < n_el && k1 < a.A && n2 < a.P) {
         v[u] = Y[k1 * a.P + n2];
         if (!a.p_smooth) v[u] = cmul(v[u], __ldg(a.cp + n2));
       }
@@ -1219,23 +1227,33 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_dstep2(DirectArgs a) {
     for (int u = 0; u < kU; ++u)
       if (e0 + u * T < n_el) sm[spad(e0 + u * T)] = v[u];
   }
+  if (a.rader && threadIdx.x < R) {
+    const int64_t k1 = r0 + threadIdx.x;
+    y0s[threadIdx.x] = k1 < a.A ? Y[k1 * a.P] : make_double2(0.0, 0.0);
+  }
   __syncthreads();
   fft_dif(sm, a.R_log2, a.stP, a.twP);
   if (!a.p_smooth) {
+    if (a.rader && threadIdx.x < R) a0s[threadIdx.x] = sm[spad(threadIdx.x)];  // DFT bin 0
+    __syncthreads();
     for (int e = threadIdx.x; e < n_el; e += T)
       sm[spad(e)] = cconj(cmul(sm[spad(e)], __ldg(a.bhat + (e >> a.R_log2))));
     __syncthreads();
     fft_dit(sm, a.R_log2, a.stP, a.twP);
   }
   double2* h = a.h + (int64_t)col * a.Kout;
-  const int nout = (int)a.P << a.R_log2;  // positions 0..P-1 of each row
+  const int nout = (int)(a.rader ? a.P - 1 : a.P) << a.R_log2;  // positions of each row
   for (int e = threadIdx.x; e < nout; e += T) {
-    const int64_t k1 = r0 + (e & (R - 1));
+    const int b = e & (R - 1);
+    const int64_t k1 = r0 + b;
     if (k1 >= a.A) continue;
     const int q = e >> a.R_log2;
     int64_t k2;
     double2 X;
-    if (a.p_smooth) {
+    if (a.rader) {  // X[g^-q] = y[0] + (a conv w)[q]
+      k2 = __ldg(a.rout + q);
+      X = cadd(y0s[b], cconj(sm[spad(e)]));
+    } else if (a.p_smooth) {
       k2 = __ldg(a.revP + q);
       X = sm[spad(e)];
     } else {
@@ -1245,6 +1263,11 @@ __global__ void __launch_bounds__(256, SFB_FFT_MINB) k_dstep2(DirectArgs a) {
     int64_t kk = (k1 + a.A * k2 - a.s_lo) % a.N2;
     if (kk < 0) kk += a.N2;
     if (kk < a.Kout) h[kk] = X;
+  }
+  if (a.rader && threadIdx.x < R && r0 + threadIdx.x < a.A) {  // X[0] = y[0] + sum_{n>0} y[n]
+    int64_t kk = (r0 + threadIdx.x - a.s_lo) % a.N2;
+    if (kk < 0) kk += a.N2;
+    if (kk < a.Kout) h[kk] = cadd(y0s[threadIdx.x], a0s[threadIdx.x]);
   }
 }
 
@@ -1452,6 +1475,43 @@ namespace {
 constexpr int kDirectSmem = 4096;   // elements per CTA in step 1 (and step 2 target)
 constexpr int kDirectSmem2 = 8192;  // hard cap for one step-2 row (R = 1)
 
+bool is_prime(int64_t n) {
+  if (n < 2) return false;
+  for (int64_t q = 2; q * q <= n; ++q)
+    if (n % q == 0) return false;
+  return true;
+}
+
+int64_t powmod(int64_t b, int64_t e, int64_t m) {
+  int64_t r = 1;
+  b %= m;
+  while (e) {
+    if (e & 1) r = r * b % m;
+    b = b * b % m;
+    e >>= 1;
+  }
+  return r;
+}
+
+// smallest generator of the multiplicative group mod the prime P
+int64_t primitive_root(int64_t P) {
+  std::vector<int64_t> fac;
+  int64_t m = P - 1;
+  for (int64_t q = 2; q * q <= m; ++q)
+    if (m % q == 0) {
+      fac.push_back(q);
+      while (m % q == 0) m /= q;
+    }
+  if (m > 1) fac.push_back(m);
+  for (int64_t g = 2; g < P; ++g) {
+    bool ok = true;
+    for (int64_t q : fac) ok = ok && powmod(g, (P - 1) / q, P) != 1;
+    if (ok) return g;
+  }
+  fail(3, "internal: no primitive root");
+  return 0;
+}
+
 // pick N2 = A * P for the direct path; false if no split fits.  best_out is
 // the model cost per point (stage costs + ~1 unit per byte of HBM traffic)
 bool choose_direct(int64_t N2, DirectFft& d, double* best_out = nullptr) {
@@ -1461,7 +1521,10 @@ bool choose_direct(int64_t N2, DirectFft& d, double* best_out = nullptr) {
     if (N2 % A || !smooth7(A)) continue;
     const int64_t P = N2 / A;
     const bool ps = smooth7(P);
-    const int64_t LP = ps ? P : next_smooth(2 * P - 1);
+    // a prime P with P - 1 smooth takes Rader's cyclic convolution of length
+    // P - 1 instead of Bluestein's of length >= 2P - 1
+    const bool rader = !ps && P > 2 && is_prime(P) && smooth7(P - 1) && !getenv("SFB_NO_RADER");
+    const int64_t LP = ps ? P : rader ? P - 1 : next_smooth(2 * P - 1);
     if (LP > kDirectSmem2) continue;
     int C = 8;
     while (C > 1 && C * A > kDirectSmem) C >>= 1;
@@ -1472,7 +1535,7 @@ bool choose_direct(int64_t N2, DirectFft& d, double* best_out = nullptr) {
                        (C < 4 ? 1.15 : 1.0);
     if (cst < best) {
       best = cst, found = true;
-      d.A = A, d.P = P, d.LP = LP, d.p_smooth = ps, d.C = C;
+      d.A = A, d.P = P, d.LP = LP, d.p_smooth = ps, d.C = C, d.rader = rader;
     }
   }
   if (best_out) *best_out = best;
@@ -1516,7 +1579,38 @@ void build_direct(NnfftPlanImpl& p, cudaStream_t s) {
   d.D.alloc(g.K);
   k_deconv<<<(unsigned)ceil_div(g.K, 256), 256, 0, s>>>(d.D.p, p.hat2.p, g.K, p.fft.in_scale);
   SF_LAUNCH_CHECK();
-  if (!d.p_smooth) {
+  if (d.rader) {
+    // Rader: X[g^-q] - y[0] = sum_p y[g^p] W^(g^(p-q)), a cyclic convolution
+    // of a_p = y[g^p] with w_m = W^(g^-m), m, p, q < P - 1
+    const int64_t g0 = primitive_root(d.P), LR = d.P - 1;
+    std::vector<int> rin(LR), rout(LR);
+    const int64_t ginv = powmod(g0, d.P - 2, d.P);
+    int64_t x = 1, y = 1;
+    for (int64_t q = 0; q < LR; ++q, x = x * g0 % d.P, y = y * ginv % d.P) {
+      rin[q] = (int)x;
+      rout[q] = (int)y;
+    }
+    upload(d.rin, rin);
+    upload(d.rout, rout);
+    std::vector<double2> w(LR);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int64_t m = 0; m < LR; ++m) {
+      const long double ang = -2.0L * pi * (long double)rout[m] / (long double)d.P;
+      w[m] = make_double2((double)cosl(ang), (double)sinl(ang));
+    }
+    DevArray<double2> b(LR);
+    SF_CUDA(cudaMemcpyAsync(b.p, w.data(), sizeof(double2) * LR, cudaMemcpyHostToDevice, s));
+    d.bhat.alloc(LR);
+    FftArgs fa{};
+    fa.g = b.p;
+    fa.Y = d.bhat.p;
+    fa.L = LR;
+    fa.st1 = d.stP;
+    fa.tw1 = d.twP.p;
+    k_single<IN_PLAIN><<<dim3(1, 1), 512, smem_bytes(LR), s>>>(fa, 1);
+    SF_LAUNCH_CHECK();
+    SF_CUDA(cudaStreamSynchronize(s));
+  } else if (!d.p_smooth) {
     d.cp.alloc(d.P);
     k_chirp_p<<<(unsigned)ceil_div(d.P, 256), 256, 0, s>>>(d.cp.p, d.P);
     SF_LAUNCH_CHECK();
@@ -1558,6 +1652,9 @@ DirectArgs make_direct_args(const NnfftPlanImpl& p) {
   a.C_log2 = d.C_log2;
   a.R_log2 = d.R_log2;
   a.p_smooth = d.p_smooth ? 1 : 0;
+  a.rader = d.rader ? 1 : 0;
+  a.rin = d.rin.p;
+  a.rout = d.rout.p;
   a.conj_in = p.fft.conj_in ? 1 : 0;
   a.stA = d.stA;
   a.stP = d.stP;

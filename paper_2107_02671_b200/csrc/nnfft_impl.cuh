@@ -110,9 +110,10 @@ struct DirectFft {
   int C = 1, C_log2 = 0;  // step-1 columns per CTA
   int R = 1, R_log2 = 0;  // step-2 rows per CTA
   bool p_smooth = false;
-  FftStages stA{}, stP{};  // stP: P (smooth) or LP (Bluestein)
+  bool rader = false;      // P prime, P - 1 smooth: Rader rows of length LP = P - 1
+  FftStages stA{}, stP{};  // stP: P (smooth), LP (Bluestein) or P - 1 (Rader)
   DevArray<double2> twA, twP, w_lo, w_hi, cp, bhat;
-  DevArray<int> revA, revP;
+  DevArray<int> revA, revP, rin, rout;
   DevArray<double> D;      // 1 / (N1 N2 phi_hat_2(l - K/2)), l in [0, K)
 };
 
