@@ -240,21 +240,39 @@ template <int M, bool REAL>
 __global__ void __launch_bounds__(256) k_spread_small(SpreadArgs a, WinCoef C) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // slot
   const int col = blockIdx.y;
+  // whole warps only (the slot count is a multiple of 128): the 4 slots of a
+  // chunk are 4 consecutive lanes and take part in the shuffles below
   if (s >= a.n_blocks * kBlockChunks * kChunk) return;
   const int64_t ci = s / kChunk;
   const int info = __ldg(a.info + ci);
-  if ((int)(s % kChunk) >= (info & 255)) return;
-  const int lcell = info >> 8;
-  const int tile = __ldg(a.blk_tile + ci / kBlockChunks);
-  const double pos = __ldg(a.pos + s);
-  const int src = __ldg(a.perm + s);
-  double2 fv;
-  if (REAL) fv = make_double2(__ldg(static_cast<const double*>(a.f) + src), 0.0);
-  else fv = __ldg(static_cast<const double2*>(a.f) + (int64_t)src * a.batch + col);
+  const int cnt = info & 255;
+  const bool act = (int)(s % kChunk) < cnt;
   double2 r[2 * M];
 #pragma unroll
   for (int k = 0; k < 2 * M; ++k) r[k] = make_double2(0.0, 0.0);
-  window_accumulate<M, REAL>(C, pos - floor(pos), fv, r);
+  if (act) {
+    const double pos = __ldg(a.pos + s);
+    const int src = __ldg(a.perm + s);
+    double2 fv;
+    if (REAL) fv = make_double2(__ldg(static_cast<const double*>(a.f) + src), 0.0);
+    else fv = __ldg(static_cast<const double2*>(a.f) + (int64_t)src * a.batch + col);
+    window_accumulate<M, REAL>(C, pos - floor(pos), fv, r);
+  }
+  // a chunk's sources share one cell: sum its 4 lanes' taps first, so only
+  // one lane per chunk issues the fp64 REDs (the Chebyshev sources of
+  // fast-sinc stage 3 pile hundreds into the end cells)
+#pragma unroll
+  for (int k = 0; k < 2 * M; ++k) {
+    r[k].x += __shfl_xor_sync(0xffffffffu, r[k].x, 1);
+    r[k].x += __shfl_xor_sync(0xffffffffu, r[k].x, 2);
+    if (!REAL) {
+      r[k].y += __shfl_xor_sync(0xffffffffu, r[k].y, 1);
+      r[k].y += __shfl_xor_sync(0xffffffffu, r[k].y, 2);
+    }
+  }
+  if ((s % kChunk) != 0 || cnt == 0) return;
+  const int lcell = info >> 8;
+  const int tile = __ldg(a.blk_tile + ci / kBlockChunks);
   double2* grid = a.grid + (int64_t)col * a.K;
   const int64_t base = (int64_t)tile * kTile - (M - 1) + lcell;  // as flush_tile
 #pragma unroll
