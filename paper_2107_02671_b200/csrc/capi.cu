@@ -324,8 +324,9 @@ void launch_graph(sincfft_nnfft_plan plan, const double2* f, double2* out, int64
       }
       gc.entries.push_back({f, out, batch, exec});
     }
+    // launched under the lock: another thread's eviction may destroy exec
+    SF_CUDA(cudaGraphLaunch(exec, s));
   }
-  SF_CUDA(cudaGraphLaunch(exec, s));
 }
 
 }  // namespace

@@ -111,6 +111,41 @@ def test_concurrent_streams_one_plan():
         assert relerr(o.cpu().numpy(), ref, f) <= 1e-15
 
 
+def test_concurrent_host_threads_one_plan():
+    """Plans are read-only during execute: host threads on
+    their own streams share one plan, with more distinct (f, out) pairs than
+    the plan's graph cache holds, so captures and evictions interleave."""
+    import threading
+
+    torch = pytest.importorskip("torch")
+    v, x, f = nodes_and_coeffs(14, 3000, 2500)
+    N, vs = sf.rescale_frequencies(512, v, 2.0, 6)
+    plan = sf.nnfft_plan(N, vs, x, m1=6, m2=6)
+    ref = sf.nnfft_trafo(plan, f)
+    df = torch.from_numpy(f).cuda()
+    errors, results = [], []
+
+    def worker():
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                outs = [sf.nnfft_trafo(plan, df) for _ in range(12)]
+            st.synchronize()
+            results.extend(o.cpu().numpy() for o in outs)
+        except Exception as e:  # noqa: BLE001 -- surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker) for _ in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert len(results) == 48
+    for o in results:
+        assert relerr(o, ref, f) <= 1e-15
+
+
 def test_shape_and_domain_errors():
     plan = sf.nnfft_plan(64, np.zeros(5), np.zeros(3))
     with pytest.raises(sf.ParameterError):
