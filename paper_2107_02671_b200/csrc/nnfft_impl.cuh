@@ -59,7 +59,18 @@ struct SpreadPlan {
   DevArray<double> bpos;
   DevArray<int> bperm;
   DevArray<int> btile;
+  // dense sources (>= kDenseMin per cell on average, e.g. fast-sinc stage 1):
+  // per-cell window moments instead of per-source windows (spread.cu)
+  DevArray<int4> units;    // {cell, first, end, 0}: <= kDenseUnit sources of one cell
+  int64_t n_units = 0;
+  bool dense = false;
 };
+
+constexpr int64_t kDenseMin = 64;   // average sources per cell from which the moment spread is used
+#ifndef SFB_DENSE_UNIT
+#define SFB_DENSE_UNIT 128
+#endif
+constexpr int kDenseUnit = SFB_DENSE_UNIT;  // sources per moment-spread unit (heavy cells are split)
 
 constexpr int kBatchedMin = 16;  // columns from which the column-vectorised path is used
 

@@ -129,6 +129,23 @@ __global__ void k_chunk_counts(const int* start, int64_t ncell, int* nch) {
   nch[c] = (start[c + 1] - start[c] + kChunk - 1) / kChunk;
 }
 
+// moment-spread work units: cells cut into runs of <= kDenseUnit sources
+__global__ void k_dense_counts(const int* start, int64_t ncell, int* nu) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= ncell) return;
+  nu[c] = (start[c + 1] - start[c] + kDenseUnit - 1) / kDenseUnit;
+}
+
+__global__ void k_dense_emit(const int* start, const int* nu, const int* off, int64_t ncell,
+                             int4* units) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= ncell) return;
+  for (int r = 0; r < nu[c]; ++r) {
+    const int s0 = start[c] + r * kDenseUnit;
+    units[off[c] + r] = make_int4((int)c, s0, min(s0 + kDenseUnit, start[c + 1]), 0);
+  }
+}
+
 // chunk sort key: (tile, rank within cell, local cell)
 constexpr int kLcBits = 12;                   // local cell < kTile <= 4096
 constexpr int kTileKeyShift = kLcBits + 30;  // rank < 2^30
@@ -452,6 +469,22 @@ void build_sources(NnfftPlanImpl& p, const double* v, int64_t M1, double N1, int
                                                p.sp.blk_tile.p);
     SF_LAUNCH_CHECK();
     SF_CUDA(cudaDeviceGetAttribute(&p.sp.n_sms, cudaDevAttrMultiProcessorCount, p.device));
+    // dense sources: keep the per-cell starts for the moment spread
+    // (SFB_SPREAD_DENSE: 0 never, 1 always, default by average cell load)
+    {
+      const char* e = getenv("SFB_SPREAD_DENSE");
+      p.sp.dense = e ? atoi(e) != 0 : M1 >= kDenseMin * K;
+      if (p.sp.dense) {
+        Scratch nu(sizeof(int) * K, s), uoff(sizeof(int) * (K + 1), s);
+        k_dense_counts<<<blocks(K), 256, 0, s>>>(cstart.as<int>(), K, nu.as<int>());
+        SF_LAUNCH_CHECK();
+        p.sp.n_units = exclusive_scan(nu.as<int>(), uoff.as<int>(), K, s);
+        p.sp.units.alloc(std::max<int64_t>(p.sp.n_units, 1));
+        k_dense_emit<<<blocks(K), 256, 0, s>>>(cstart.as<int>(), nu.as<int>(), uoff.as<int>(), K,
+                                              p.sp.units.p);
+        SF_LAUNCH_CHECK();
+      }
+    }
     // batched path: keep the cell-sorted arrays and the 128-cell tile starts
     {
       const int64_t ntb = ceil_div(K, 128);

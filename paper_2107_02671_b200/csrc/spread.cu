@@ -285,6 +285,157 @@ __global__ void __launch_bounds__(256) k_spread_small(SpreadArgs a, WinCoef C) {
   }
 }
 
+// Dense sources (hundreds per cell: fast-sinc stage 1 puts 2^22 sources on
+// 8,224 cells).  Every tap is a polynomial in u = 2d - 1 (window.cuh), so the
+// sum over a cell's sources of f * g_t(d) is a fixed combination of the
+// cell's moments  S_j = sum f u^j,  S'_j = sum f sqrt(d) u^j,
+// S''_j = sum f sqrt(1-d) u^j  (j <= P; the primed sets feed the two edge
+// taps): 1 multiply + 3 FMAs per power and source instead of ~160 fp64 ops
+// per source for the 2m tap polynomials.  Cells are cut into plan-time units
+// of <= kDenseUnit sources (heavy cells of clustered inputs spread over many
+// units); a group of kDenseLanes lanes owns a unit, sums its moments over the
+// group by shuffles, forms the 2m taps from the uniform coefficients and adds
+// them to the grid with one fp64 RED per tap.  Complex f runs the moments
+// once per component.  Fast-sinc stage 1 (config 5, ~510 sources per cell):
+// 82 us for the per-source spread, 79 us for a warp per cell (the 42-moment
+// butterflies cost as much as the sources), 50 us with 2 lanes x 64 sources
+// per unit and the next batch's loads in flight (measured over lanes 1-16 and
+// units 16-512).
+struct DenseArgs {
+  const double* pos;   // fl(N1 v), cell-sorted
+  const int* perm;     // cell-sorted
+  const int4* units;   // {cell, first, end, 0}
+  const void* f;
+  double2* grid;
+  int64_t K, n_units;
+  int batch;
+};
+
+#ifndef SFB_DENSE_LANES
+#define SFB_DENSE_LANES 2
+#endif
+constexpr int kDenseLanes = SFB_DENSE_LANES;  // lanes per unit
+
+template <int M, bool REAL>
+__global__ void __launch_bounds__(256, 2) k_spread_dense(DenseArgs a, WinCoef C) {
+  constexpr int P = window_degree(M);
+  constexpr int NE = P / 2 + 1;
+  constexpr int NO = (P + 1) / 2;
+  constexpr int L = kDenseLanes, G = 2;  // G sources per lane per load batch
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % L;
+  const int64_t un_i = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * (32 / L) + lane / L;
+  const int col = blockIdx.y;
+  if (((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * (32 / L) >= a.n_units) return;
+  int4 un = make_int4(0, 0, 0, 0);  // inactive groups: empty unit
+  if (un_i < a.n_units) un = __ldg(a.units + un_i);
+  const int64_t cell = un.x;
+  const int s0 = un.y, s1 = un.z;
+  double2* grid = a.grid + (int64_t)col * a.K;
+#pragma unroll 1
+  for (int comp = 0; comp < (REAL ? 1 : 2); ++comp) {
+    double m0[P + 1], m1[P + 1], m2[P + 1];
+#pragma unroll
+    for (int j = 0; j <= P; ++j) m0[j] = m1[j] = m2[j] = 0.0;
+    // G sources per lane at a time, software-pipelined: the f loads of batch
+    // g and the position / permutation loads of batch g + 1 are in flight
+    // together, then batch g's arithmetic
+    double pv[G];
+    int src[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int s = s0 + gl + L * i;
+      pv[i] = s < s1 ? __ldg(a.pos + s) : 0.5;
+      src[i] = s < s1 ? __ldg(a.perm + s) : -1;
+    }
+#pragma unroll 1
+    for (int g = 0;; g += G) {
+      if (__all_sync(0xffffffffu, s0 + L * g >= s1)) break;
+      double fr[G];
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        fr[i] = 0.0;
+        if (src[i] >= 0) {
+          if (REAL) {
+            fr[i] = __ldg(static_cast<const double*>(a.f) + src[i]);
+          } else {
+            const double* fp = reinterpret_cast<const double*>(static_cast<const double2*>(a.f) +
+                                                               (int64_t)src[i] * a.batch + col);
+            fr[i] = __ldg(fp + comp);
+          }
+        }
+      }
+      double pn[G];
+      int sn[G];
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        const int s = s0 + gl + L * (g + G + i);
+        pn[i] = s < s1 ? __ldg(a.pos + s) : 0.5;
+        sn[i] = s < s1 ? __ldg(a.perm + s) : -1;
+      }
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        const double pos = pv[i], fv = fr[i];
+        const double d = pos - floor(pos);
+        const double u = 2.0 * d - 1.0;
+        const double fb = fv * sqrt(d), fc = fv * sqrt(1.0 - d);
+        double pw = 1.0;
+#pragma unroll
+        for (int j = 0; j <= P; ++j) {
+          m0[j] = fma(fv, pw, m0[j]);
+          m1[j] = fma(fb, pw, m1[j]);
+          m2[j] = fma(fc, pw, m2[j]);
+          pw *= u;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        pv[i] = pn[i];
+        src[i] = sn[i];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j <= P; ++j) {
+#pragma unroll
+      for (int o = 1; o < L; o <<= 1) {
+        m0[j] += __shfl_xor_sync(0xffffffffu, m0[j], o);
+        m1[j] += __shfl_xor_sync(0xffffffffu, m1[j], o);
+        m2[j] += __shfl_xor_sync(0xffffffffu, m2[j], o);
+      }
+    }
+    // tap pair q: g_{q+1} = E + uO and g_{-q} = E - uO (edge pair: times
+    // sqrt(d), sqrt(1-d)), so sum f g = sum_k e_k S_2k +- o_k S_2k+1; lane gl
+    // of the group adds taps gl, gl + L, ...
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+      const double* ma = q < M - 1 ? m0 : m1;
+      const double* mb = q < M - 1 ? m0 : m2;
+      double ea = 0.0, oa = 0.0, eb = 0.0, ob = 0.0;
+#pragma unroll
+      for (int k = 0; k < NE; ++k) {
+        ea = fma(C.e[q][k], ma[2 * k], ea);
+        eb = fma(C.e[q][k], mb[2 * k], eb);
+      }
+#pragma unroll
+      for (int k = 0; k < NO; ++k) {
+        oa = fma(C.o[q][k], ma[2 * k + 1], oa);
+        ob = fma(C.o[q][k], mb[2 * k + 1], ob);
+      }
+      const int ih = (q < M - 1) ? M + q : 2 * M - 1;
+      const int il = (q < M - 1) ? M - 1 - q : 0;
+      const double th = ea + oa, tl = eb - ob;
+      if (s0 < s1 && (ih % L) == gl) {
+        const int64_t gi = cell - (M - 1) + ih;
+        if (gi >= 0 && gi < a.K && th != 0.0) atomicAdd(reinterpret_cast<double*>(grid + gi) + comp, th);
+      }
+      if (s0 < s1 && (il % L) == gl) {
+        const int64_t gi = cell - (M - 1) + il;
+        if (gi >= 0 && gi < a.K && tl != 0.0) atomicAdd(reinterpret_cast<double*>(grid + gi) + comp, tl);
+      }
+    }
+  }
+}
+
 static int64_t small_spread_blocks() {
   static const int64_t v = [] {
     const char* e = getenv("SFB_SPREAD_SMALL_MAX");
@@ -304,6 +455,17 @@ static void launch_spread_m(const NnfftPlanImpl& p, const void* f, double2* grid
     SF_CUDA(cudaFuncSetAttribute(k_spread<M, REAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     attr_set.fetch_or(bit);
+  }
+  if (p.sp.dense) {
+    DenseArgs d{p.sp.bpos.p, p.sp.bperm.p, p.sp.units.p, f, grid, p.g.K, p.sp.n_units, batch};
+    if (p.sp.n_units == 0) return;
+    k_spread_dense<M, REAL>
+        <<<dim3((unsigned)ceil_div(ceil_div(p.sp.n_units, (int64_t)(32 / kDenseLanes)) * 32,
+                                   (int64_t)256),
+                batch),
+           256, 0, s>>>(d, p.c1);
+    SF_LAUNCH_CHECK();
+    return;
   }
   SpreadArgs a{p.sp.pos.p, p.sp.perm.p, p.sp.info.p, p.sp.blk_tile.p, p.sp.wstart.p, f, grid,
                p.g.K, p.sp.n_blocks, batch};

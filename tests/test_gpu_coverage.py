@@ -207,6 +207,40 @@ def test_config3_full_size_properties():
     assert err <= 1e-12  # the reference measured ~3.5e-15 at m = 8
 
 
+@pytest.mark.parametrize("m,clustered,batch", [(2, False, 1), (4, True, 1), (8, False, 1),
+                                               (8, True, 3), (11, False, 1), (16, True, 1)])
+def test_dense_moment_spread(monkeypatch, m, clustered, batch):
+    """The moment spread (spread.cu k_spread_dense; chosen by plan when cells
+    hold >= 64 sources on average) forced on ordinary inputs: same transform
+    as the per-source spread and the oracle, complex and batched."""
+    v, x, f = nodes_and_coeffs(300 + m, 6000, 2500, clustered=clustered)
+    if batch > 1:
+        f = np.stack([f * (k + 1) for k in range(batch)], axis=1)
+    N, vs = sf.rescale_frequencies(256, v, 2.0, m)
+    monkeypatch.setenv("SFB_SPREAD_DENSE", "1")
+    dense = sf.nnfft_trafo(sf.nnfft_plan(N, vs, x, m1=m, m2=m), f)
+    monkeypatch.setenv("SFB_SPREAD_DENSE", "0")
+    plain = sf.nnfft_trafo(sf.nnfft_plan(N, vs, x, m1=m, m2=m), f)
+    assert relerr(dense, plain, f) <= 1e-14
+    ref = O.trafo(O.plan(N, vs, x, 2.0, 2.0, m, m), f[:, 0] if batch > 1 else f)
+    assert relerr(dense[:, 0] if batch > 1 else dense, ref, f[:, 0] if batch > 1 else f) <= TOL
+
+
+def test_dense_spread_chosen_for_fast_sinc_stage1():
+    """Config-5 shape at a quarter of the sources: stage 1 (~128 sources per
+    cell) takes the moment spread by default; real and complex c agree with
+    the oracle."""
+    rng = np.random.default_rng(55)
+    a = rng.uniform(-0.5, 0.5, 1 << 20)
+    b = rng.uniform(-0.5, 0.5, 4096)
+    plan = sf.sinc_plan(4096, a, b, m1=8, m2=8)
+    oplan = O.sinc_plan(4096, a, b, m1=8, m2=8)
+    c = rng.standard_normal(1 << 20)
+    assert relerr(sf.fast_sinc_transform(plan, c), O.sinc_transform(oplan, c), c) <= TOL
+    cz = c + 1j * rng.standard_normal(1 << 20)
+    assert relerr(sf.fast_sinc_transform(plan, cz), O.sinc_transform(oplan, cz), cz) <= TOL
+
+
 @pytest.mark.slow
 def test_config5_full_size_vs_oracle():
     """BASELINE config 5 (fast sinc, L1 = L2 = 2^22) against the CPU oracle."""
