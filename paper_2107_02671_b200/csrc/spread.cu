@@ -315,13 +315,19 @@ struct DenseArgs {
 #define SFB_DENSE_LANES 2
 #endif
 constexpr int kDenseLanes = SFB_DENSE_LANES;  // lanes per unit
+#ifndef SFB_DENSE_G
+#define SFB_DENSE_G 2
+#endif
 
 template <int M, bool REAL>
-__global__ void __launch_bounds__(256, 2) k_spread_dense(DenseArgs a, WinCoef C) {
+#ifndef SFB_DENSE_MINB
+#define SFB_DENSE_MINB 2
+#endif
+__global__ void __launch_bounds__(256, SFB_DENSE_MINB) k_spread_dense(DenseArgs a, WinCoef C) {
   constexpr int P = window_degree(M);
   constexpr int NE = P / 2 + 1;
   constexpr int NO = (P + 1) / 2;
-  constexpr int L = kDenseLanes, G = 2;  // G sources per lane per load batch
+  constexpr int L = kDenseLanes, G = SFB_DENSE_G;  // G sources per lane per load batch
   const int lane = threadIdx.x & 31;
   const int gl = lane % L;
   const int64_t un_i = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * (32 / L) + lane / L;

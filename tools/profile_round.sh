@@ -19,4 +19,7 @@ ncu --set full --import-source on --clock-control none -k regex:"k_spread|_r1|k_
 ncu --set full --import-source on --clock-control none -k regex:"k_spread_b|_rb|k_gather_b" \
     --launch-count 5 -o $P/c4 python bench.py --config 4 --no-cpu --steps 1 --warmup 3 \
     > $P/ncu_c4.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"k_spread_dense|k_spread_small|k_gather2|_d?step" \
+    --launch-count 8 -o $P/c5 python bench.py --config 5 --no-cpu --steps 1 --warmup 3 \
+    > $P/ncu_c5.log 2>&1
 ls -la $P
