@@ -333,6 +333,22 @@ SINCFFT_API int sincfft_sinc_direct(const double *c, const double *a, int64_t L1
                                     int64_t L2, int64_t N, double *out, int32_t ptr_kind,
                                     int32_t device, void *stream);
 
+/* ---- public window functions (sinh kind) ------------------------------------
+ * Replaces windows.py:106-125 (omega_eval), :135-160 (omega_hat_eval),
+ * :212-214 (phi_eval), :217-220 (phi_hat_eval) of the reference for
+ * kind = "sinh": out[i] = F(x[i]) with the reference's closed forms, evaluated
+ * on the device.  func: SINCFFT_WIN_OMEGA, _OMEGA_HAT, _PHI, _PHI_HAT; beta is
+ * the window shape 2 pi m (1 - 1/(2 sigma)); m and n_grid dilate phi / phi_hat
+ * (phi(t) = omega(t n_grid/m), phi_hat(v) = (m/n_grid) omega_hat(v m/n_grid)).
+ * n == 0 is a no-op. */
+#define SINCFFT_WIN_OMEGA 0
+#define SINCFFT_WIN_OMEGA_HAT 1
+#define SINCFFT_WIN_PHI 2
+#define SINCFFT_WIN_PHI_HAT 3
+SINCFFT_API int sincfft_window_eval(int32_t func, double beta, int32_t m, int64_t n_grid,
+                                    const double *x, int64_t n, double *out, int32_t ptr_kind,
+                                    int32_t device, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

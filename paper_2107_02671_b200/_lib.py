@@ -118,6 +118,8 @@ SIGNATURES = {
                                       C.c_int32, _vp]),
     "sincfft_sinc_direct": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int64, C.c_int64, _vp,
                                       C.c_int32, C.c_int32, _vp]),
+    "sincfft_window_eval": (C.c_int, [C.c_int32, C.c_double, C.c_int32, C.c_int64, _vp,
+                                      C.c_int64, _vp, C.c_int32, C.c_int32, _vp]),
 }
 
 

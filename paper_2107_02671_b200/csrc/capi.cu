@@ -1107,4 +1107,25 @@ int sincfft_sinc_direct(const double* c, const double* a, int64_t L1, const doub
   });
 }
 
+
+int sincfft_window_eval(int32_t func, double beta, int32_t m, int64_t n_grid, const double* x,
+                        int64_t n, double* out, int32_t ptr_kind, int32_t device, void* stream) {
+  return guarded([&] {
+    if (func < SINCFFT_WIN_OMEGA || func > SINCFFT_WIN_PHI_HAT)
+      sfb::fail(1, "window_eval: unknown window function");
+    if (n < 0) sfb::fail(1, "window_eval: negative length");
+    if (n == 0) return;
+    if (!x || !out) sfb::fail(1, "NULL argument");
+    if ((func == SINCFFT_WIN_PHI || func == SINCFFT_WIN_PHI_HAT) && (m <= 0 || n_grid <= 0))
+      sfb::fail(1, "window_eval: m and n_grid must be positive");
+    check_ptr_kind(ptr_kind);
+    set_device(device);
+    cudaStream_t s = as_stream(stream);
+    InBuf xb(x, sizeof(double) * n, ptr_kind, s);
+    OutBuf ob(out, sizeof(double) * n, ptr_kind, s);
+    sfb::run_window_eval(func, beta, m, n_grid, (const double*)xb.ptr, n, (double*)ob.ptr, s);
+    ob.finish(s);
+  });
+}
+
 }  // extern "C"

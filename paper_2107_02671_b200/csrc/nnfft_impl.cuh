@@ -281,6 +281,9 @@ void run_nndft_direct(const double2* f, const double* v, int64_t M1, const doubl
                       int64_t M2, double N, double2* out, cudaStream_t stream);
 void run_ndft_direct(const double2* c, int64_t Nc, const double* x, int64_t M, double2* out,
                      cudaStream_t stream);
+// public window evaluation (window.cu): func 0 omega, 1 omega_hat, 2 phi, 3 phi_hat
+void run_window_eval(int func, double beta, int m, int64_t n_grid, const double* x, int64_t n,
+                     double* out, cudaStream_t s);
 void run_sinc_direct(const double2* c, const double* a, int64_t L1, const double* b, int64_t L2,
                      double N, double2* out, cudaStream_t stream);
 // ----- batched.cu: batch >= kBatchedMin columns, columns across lanes

@@ -158,3 +158,45 @@ WinCoef fit_window_uncached(int m, double beta_d, double* max_err_out) {
 }  // namespace
 
 }  // namespace sfb
+
+// ---------------------------------------------------------------------------
+// Public window evaluation (drop-in for windows.py's omega_eval, omega_hat_eval,
+// phi_eval, phi_hat_eval, sinh kind): the reference's closed forms evaluated
+// elementwise on the device -- not the per-tap polynomials of the hot path.
+namespace sfb {
+
+// omega(x) = e^{beta(s-1)} (1 - e^{-2 beta s}) / (1 - e^{-2 beta}),
+// s = sqrt(max(0, 1 - x^2)), zero unless |x| < 1   (windows.py:106-125)
+__device__ inline double omega_sinh(double beta, double x) {
+  if (!(fabs(x) < 1.0)) return 0.0;
+  const double s = sqrt(fmax(0.0, 1.0 - x * x));
+  return exp(beta * (s - 1.0)) * (-expm1(-2.0 * beta * s)) / (-expm1(-2.0 * beta));
+}
+
+__global__ void k_window_eval(int func, double beta, double scale, const double* __restrict__ x,
+                              int64_t n, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double xi = x[i];
+  double r;
+  switch (func) {
+    case 0: r = omega_sinh(beta, xi); break;               // omega_eval
+    case 1: r = omega_hat_sinh(beta, xi); break;           // omega_hat_eval
+    case 2: r = omega_sinh(beta, xi * scale); break;       // phi_eval: scale = n_grid/m
+    default: r = scale * omega_hat_sinh(beta, xi * scale); // phi_hat_eval: scale = m/n_grid
+  }
+  out[i] = r;
+}
+
+void run_window_eval(int func, double beta, int m, int64_t n_grid, const double* x, int64_t n,
+                     double* out, cudaStream_t s) {
+  // the quotients are formed first, as in windows.py:212-220
+  const double scale = func == 2 ? (double)n_grid / (double)m
+                     : func == 3 ? (double)m / (double)n_grid : 1.0;
+  if (n <= 0) return;
+  const int T = 256;
+  k_window_eval<<<(unsigned)((n + T - 1) / T), T, 0, s>>>(func, beta, scale, x, n, out);
+  SF_LAUNCH_CHECK();
+}
+
+}  // namespace sfb

@@ -69,3 +69,14 @@ def cc_quadrature(n):
         raise ParameterError("cc_quadrature: n must be an integer >= 2")
     w = cc_weights_fast(n) if (n >= 4 and (n & (n - 1)) == 0) else cc_weights_direct(n)
     return CcQuadrature(int(n), chebyshev_points(n), np.asarray(w, dtype=float))
+
+
+def cc_export_csv(quad, path):
+    """Write the quadrature to ``path`` as CSV with columns k, z_k, w_k
+    (sinc_approx.py:157-165: a ``# schema=1`` line, the header, then one row
+    per node with both floats printed to 17 significant digits)."""
+    with open(path, "w", encoding="utf-8", newline="") as fh:
+        fh.write("# schema=1\nk,z_k,w_k\n")
+        fh.writelines(f"{k},{format(z, '.17g')},{format(w, '.17g')}\n"
+                      for k, (z, w) in enumerate(zip(quad.points[:quad.n + 1],
+                                                     quad.weights[:quad.n + 1])))
