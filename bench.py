@@ -133,14 +133,42 @@ def make_inputs(cfg, seed=0):
                             batch=cfg["batch"])
 
 
+def cpu_info():
+    """The host the CPU leg ran on: core count, model, and the core this
+    process is pinned to (os.sched_setaffinity, i.e. taskset -c)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    aff = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None
+    return {"nproc": os.cpu_count(), "cpu_model": model, "affinity": aff}
+
+
+def pin_one_core():
+    """taskset -c <core>: the reference is single-threaded numpy/scipy
+    (SURVEY.md 8d), so it is timed on one pinned core; the first core of the
+    inherited affinity set is used."""
+    if hasattr(os, "sched_setaffinity"):
+        core = min(os.sched_getaffinity(0))
+        os.sched_setaffinity(0, {core})
+
+
 def cpu_sample_rate(cfg, steps=1, warmup=0, sample_nodes=1 << 22):
     """Time the CPU oracle's trafo (single-threaded numpy/scipy, like the
-    reference) on a bounded sample: the workload's geometry (N, m) with
-    sample_nodes sources and targets drawn the same way."""
+    reference) pinned to one core: the workload's geometry (N, m) with
+    sample_nodes sources and targets drawn the same way (the full workload
+    when sample_nodes >= M1, with the workload's own seed)."""
     from oracle import sincfft_oracle as O
+    pin_one_core()
     M = min(sample_nodes, cfg["M1"])
+    full = M == cfg["M1"]
     sub = dict(cfg, M1=M, M2=M, batch=0)
-    v, x, f = make_inputs(sub, seed=1)
+    v, x, f = make_inputs(sub, seed=0 if full else 1)
     n_star, vs = O.rescale_frequencies(cfg["N"], v, 2.0, cfg["m"])
     t0 = time.perf_counter()
     tab = O.plan(n_star, vs, x, m1=cfg["m"], m2=cfg["m"])
@@ -153,10 +181,14 @@ def cpu_sample_rate(cfg, steps=1, warmup=0, sample_nodes=1 << 22):
         O.trafo(tab, f)
         ts.append(time.perf_counter() - t0)
     t = statistics.median(ts)
+    info = cpu_info()
     return {"value": 2 * M / t, "unit": "nodes/s", "cores": 1, "kind": "port",
-            "sample": f"oracle trafo, N={cfg['N']}, m={cfg['m']}, M1=M2={M} "
-                      f"({'clustered' if cfg['clustered'] else 'uniform'}), median of {steps}, "
-                      f"plan {t_plan:.1f}s untimed",
+            "sample": (f"oracle trafo (restatement of the reference's nnfft_trafo, pinned to "
+                       f"core {info['affinity']}), N={cfg['N']}, m={cfg['m']}, M1=M2={M} "
+                       f"({'clustered' if cfg['clustered'] else 'uniform'}"
+                       f"{', the full workload, seed 0' if full else ', a bounded sample'}), "
+                       f"median of {steps} after {warmup} warm-up, plan {t_plan:.1f}s untimed"),
+            "same_config": full, "plan_s": t_plan, **info,
             "seconds_per_step": t}
 
 
@@ -164,19 +196,17 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    # bound the whole K+W run to ~2.5 min of single-core work: per-step cost of
-    # the oracle trafo is ~0.85 s (FFT at N=2^20) + ~0.5 us per node
-    budget = 150.0 / (args.steps + args.warmup)
-    M = 1 << 22
-    while M > 1 << 14 and 0.85 + 2 * M * 0.5e-6 > budget:
-        M >>= 1
-    base = cpu_sample_rate(cfg, steps=args.steps, warmup=args.warmup, sample_nodes=M)
+    # the reference's own CPU path on the same workload as the B200 arm: the
+    # full configuration (config 3: ~45 s of plan, ~17 s per trafo on one core)
+    base = cpu_sample_rate(cfg, steps=args.steps, warmup=args.warmup, sample_nodes=cfg["M1"])
     line = {"metric": METRIC, "value": base["value"], "unit": "nodes/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": base["seconds_per_step"] * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "sample": base["sample"]},
-            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": {"workload": cfg["desc"], "sample": base["sample"],
+                       "same_config": base["same_config"]},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                  "nproc", "cpu_model", "affinity")},
             "e2e": {"value": base["value"], "unit": "nodes/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -403,13 +433,16 @@ def run_b200(args, cfg):
             # reduce-scatter / all-gather form
             # default: the two transposes fused into the column / row passes
             # over peer memory (CUDA IPC, NVLink P2P between the node's GPUs)
+            # default: NCCL all-to-alls of the rows each rank touches; the
+            # kernels-store-into-peer-memory form (CUDA IPC) only on request
+            # (--peer-transposes) until it has run across >= 2 GPUs
             if args.dense_exchange:
                 dist_fft = DistributedFftNnfft(plan)
-            elif args.no_peer_transposes:
-                dist_fft = SparseDistributedFftNnfft(plan)
-            else:
+            elif args.peer_transposes:
                 from paper_2107_02671_b200.sharding import PeerDistributedFftNnfft
                 dist_fft = PeerDistributedFftNnfft(plan)
+            else:
+                dist_fft = SparseDistributedFftNnfft(plan)
     torch.cuda.synchronize()
     plan_ms = (time.perf_counter() - tp) * 1e3
     geo = plan.backend_geometry
@@ -506,9 +539,12 @@ def run_b200(args, cfg):
     P = 16 if m <= 2 else 15 if m <= 3 else 14 if m <= 6 else 13 if m <= 9 else 12
     dfma_node = m * (P + 1) + 16 + 4 * m * B
     flops = {"spread": 2 * dfma_node * Ms, "gather": 2 * dfma_node * Mt, "fft": None}
+    # DRAM bytes per launch of that kernel from the committed ncu capture --
+    # single-GPU only (a shard's kernels were not captured: null, not the
+    # whole-problem figure)
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tf):
+    if world == 1 and os.path.exists(tf):
         with open(tf) as fh:
             traffic = json.load(fh).get(f"config{args.config}", {}).get(dom)
 
@@ -517,7 +553,9 @@ def run_b200(args, cfg):
     # successive steps rotate over --e2e-streams streams so the H2D of step
     # k+1, the kernels of step k and the D2H of step k-1 overlap (full-duplex
     # PCIe; 4 streams measured 5.95 ms vs 6.42 with 2 at config 3)
-    nbuf = args.e2e_streams
+    # (N > 1 with a distributed FFT: one stream -- its exchange buffers are
+    # shared by every call, so calls could not overlap anyway)
+    nbuf = 1 if dist_fft is not None else args.e2e_streams
     h_f = [torch.from_numpy(fshard).pin_memory() for _ in range(nbuf)]
     h_out = [torch.empty(tuple(d_out.shape), dtype=torch.complex128).pin_memory()
              for _ in range(nbuf)]
@@ -641,7 +679,7 @@ def run_b200(args, cfg):
     launches = L.sincfft_nnfft_launches_per_execute(ph, B) * args.steps
     if dist_fft is not None:  # grid memset + spread, pack (+ tail fix), 3 passes
         fix = 1 if geo["L"] < geo["K"] + geo["Kout"] - 1 else 0  # (+ rank-0 fix add), unpack, gather
-        if args.dense_exchange or args.no_peer_transposes:
+        if not args.peer_transposes:
             launches = (2 + 1 + fix + 3 + (fix if rank == 0 else 0) + 1 + 1
                         + (0 if args.dense_exchange else 2)) * args.steps
         else:  # memset, spread, pack (+fix) to peers, unpack, 3 passes, unpack h, gather
@@ -657,7 +695,8 @@ def run_b200(args, cfg):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample_rate(cfg)
-        cpu.pop("seconds_per_step", None)
+        for k in ("seconds_per_step", "plan_s"):
+            cpu.pop(k, None)
 
     if rank == 0:
         line = {
@@ -676,11 +715,12 @@ def run_b200(args, cfg):
                                        (" by position (quantiles of v and x)" if world > 1 else "")) +
                        (("; distributed FFT: " + ("reduce-scatter + 2 all-to-all + all-gather"
                                                    if args.dense_exchange else
-                                                   "4 all-to-alls (grid / h rows exchanged "
-                                                   "sparsely)" if args.no_peer_transposes else
                                                    "every exchange fused into the kernels as "
                                                    "stores into the owners' buffers over peer "
-                                                   "memory (CUDA IPC), 4 barriers")
+                                                   "memory (CUDA IPC), 4 barriers"
+                                                   if args.peer_transposes else
+                                                   "4 NCCL all-to-alls (grid / h rows "
+                                                   "exchanged sparsely)")
                          if dist_fft is not None else ", NCCL all-reduce of the K-grid")
                         if world > 1 and not col_shard else "")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
@@ -716,6 +756,28 @@ def run_b200(args, cfg):
         dist.destroy_process_group()
 
 
+def spawn_ranks(n, same_device=False):
+    """Re-launch this command under torch.distributed.run with n ranks on this
+    node (rendezvous on 127.0.0.1, a free port); returns its exit code."""
+    import socket
+    import subprocess
+    if not same_device:
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}",
+                  file=sys.stderr)
+            return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -737,15 +799,24 @@ def main():
     ap.add_argument("--dense-exchange", action="store_true",
                     help="N > 1 distributed FFT: reduce-scatter / all-gather the whole "
                          "K-grid and h instead of all-to-alls of the rows each rank touches")
-    ap.add_argument("--no-peer-transposes", action="store_true",
-                    help="N > 1 distributed FFT: NCCL all-to-alls for the two transposes "
-                         "instead of the column / row passes storing into peer memory")
+    ap.add_argument("--peer-transposes", action="store_true",
+                    help="N > 1 distributed FFT: every exchange fused into the kernels as "
+                         "stores into the owners' buffers over peer memory (CUDA IPC) "
+                         "instead of NCCL all-to-alls")
     ap.add_argument("--check-shards", action="store_true",
                     help="N > 1: compare this rank's output shard with a single-rank "
                          "transform of the same inputs and report the max deviation")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.impl != "reference":
+        if args.gpus > 1 and world == 0:
+            # `python bench.py --gpus N` without a launcher: start the N ranks
+            # ourselves, one process per GPU, exactly as the driver's torchrun
+            sys.exit(spawn_ranks(args.gpus, args.same_device))
+        if max(world, 1) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world or 1}")
     if args.impl == "reference":
         run_reference(args, cfg)
     elif cfg.get("sinc"):

@@ -25,8 +25,14 @@ struct GraphCache {
     int64_t batch;
     cudaGraphExec_t exec;
   };
+  struct Key {
+    const void* f;
+    void* out;
+    int64_t batch;
+  };
   std::mutex mu;
-  std::vector<Entry> entries;  // most recent last, at most kMax
+  std::vector<Entry> entries;  // least recently used first, at most kMax
+  std::vector<Key> seen;       // keys executed once without a graph, at most kMax
   static constexpr size_t kMax = 8;
   ~GraphCache() {
     for (auto& e : entries) cudaGraphExecDestroy(e.exec);
@@ -289,44 +295,72 @@ bool use_graph(const sfb::NnfftPlanImpl& p, int64_t batch) {
   return !off && (batch == 1 || (p.g.M1 + p.g.M2) * batch <= lim);
 }
 
-void launch_graph(sincfft_nnfft_plan plan, const double2* f, double2* out, int64_t batch,
+// Replays the spread/FFT/gather sequence of (f, out, batch) as a CUDA graph.
+// A key is captured on its SECOND execute (a caller that allocates a fresh
+// output every call never pays capture + instantiate); hits move to the back
+// (LRU); a new key reuses the least recently used exec through
+// cudaGraphExecUpdate (same topology, new pointers) instead of instantiating.
+// Returns false when the caller should launch directly (first sighting).
+bool launch_graph(sincfft_nnfft_plan plan, const double2* f, double2* out, int64_t batch,
                   cudaStream_t s) {
   GraphCache& gc = plan->graphs;
+  std::lock_guard<std::mutex> lk(gc.mu);
   cudaGraphExec_t exec = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(gc.mu);
-    for (size_t i = 0; i < gc.entries.size(); ++i) {
-      if (gc.entries[i].f == f && gc.entries[i].out == out && gc.entries[i].batch == batch) {
-        exec = gc.entries[i].exec;
+  for (size_t i = 0; i < gc.entries.size(); ++i) {
+    const GraphCache::Entry e = gc.entries[i];
+    if (e.f == f && e.out == out && e.batch == batch) {
+      gc.entries.erase(gc.entries.begin() + i);
+      gc.entries.push_back(e);
+      exec = e.exec;
+      break;
+    }
+  }
+  if (!exec) {
+    bool seen = false;
+    for (size_t i = 0; i < gc.seen.size(); ++i) {
+      if (gc.seen[i].f == f && gc.seen[i].out == out && gc.seen[i].batch == batch) {
+        gc.seen.erase(gc.seen.begin() + i);
+        seen = true;
         break;
       }
     }
-    if (!exec) {
-      cudaStream_t cs;
-      SF_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-      cudaGraph_t graph = nullptr;
-      try {
-        SF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        sfb::run_execute(plan->impl, f, out, (int)batch, cs);
-        SF_CUDA(cudaStreamEndCapture(cs, &graph));
-        SF_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-      } catch (...) {
-        cudaStreamEndCapture(cs, &graph);
-        if (graph) cudaGraphDestroy(graph);
-        cudaStreamDestroy(cs);
-        throw;
-      }
-      cudaGraphDestroy(graph);
-      cudaStreamDestroy(cs);
-      if (gc.entries.size() == GraphCache::kMax) {
-        cudaGraphExecDestroy(gc.entries.front().exec);
-        gc.entries.erase(gc.entries.begin());
-      }
-      gc.entries.push_back({f, out, batch, exec});
+    if (!seen) {
+      if (gc.seen.size() == GraphCache::kMax) gc.seen.erase(gc.seen.begin());
+      gc.seen.push_back({f, out, batch});
+      return false;
     }
-    // launched under the lock: another thread's eviction may destroy exec
-    SF_CUDA(cudaGraphLaunch(exec, s));
+    cudaStream_t cs;
+    SF_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    try {
+      SF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      sfb::run_execute(plan->impl, f, out, (int)batch, cs);
+      SF_CUDA(cudaStreamEndCapture(cs, &graph));
+      if (gc.entries.size() == GraphCache::kMax) {
+        cudaGraphExec_t lru = gc.entries.front().exec;
+        gc.entries.erase(gc.entries.begin());
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(lru, graph, &info) == cudaSuccess) {
+          exec = lru;
+        } else {
+          cudaGetLastError();  // clear the update failure
+          cudaGraphExecDestroy(lru);
+        }
+      }
+      if (!exec) SF_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    } catch (...) {
+      cudaStreamEndCapture(cs, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      cudaStreamDestroy(cs);
+      throw;
+    }
+    cudaGraphDestroy(graph);
+    cudaStreamDestroy(cs);
+    gc.entries.push_back({f, out, batch, exec});
   }
+  // launched under the lock: another thread's eviction may update or destroy exec
+  SF_CUDA(cudaGraphLaunch(exec, s));
+  return true;
 }
 
 }  // namespace
@@ -425,8 +459,8 @@ int sincfft_nnfft_execute(sincfft_nnfft_plan plan, const double* f, double* out,
     const size_t fb = sizeof(double2) * (size_t)p.g.M1 * batch;
     const size_t ob = sizeof(double2) * (size_t)p.g.M2 * batch;
     InBuf fin(f, fb, ptr_kind, s);
-    if (ptr_kind == SINCFFT_PTR_DEVICE && use_graph(p, batch)) {
-      launch_graph(plan, (const double2*)f, (double2*)out, batch, s);
+    if (ptr_kind == SINCFFT_PTR_DEVICE && use_graph(p, batch) &&
+        launch_graph(plan, (const double2*)f, (double2*)out, batch, s)) {
     } else if (ptr_kind == SINCFFT_PTR_DEVICE) {
       sfb::run_execute(p, (const double2*)fin.ptr, (double2*)out, (int)batch, s);
     } else {

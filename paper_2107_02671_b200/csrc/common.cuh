@@ -152,6 +152,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(mbar))
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned phase) {
   asm volatile(
       "{\n"
@@ -177,6 +180,11 @@ __device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, int sr
 __device__ __forceinline__ void cp_async8z(void* smem, const void* gmem, int src_bytes) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async4z(void* smem, const void* gmem, int src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem),
                "r"(src_bytes));
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {

@@ -1559,8 +1559,14 @@ void build_direct(NnfftPlanImpl& p, cudaStream_t s) {
   const int64_t want = 2 * (int64_t)p.sp.n_sms;
   while (d.R > 1 && ceil_div(d.A, (int64_t)d.R) < want) d.R >>= 1;
   while (d.C > 2 && ceil_div(d.P, (int64_t)d.C) < want) d.C >>= 1;
-  if (const char* e = getenv("SFB_DIRECT_R")) d.R = std::max(1, atoi(e));
-  if (const char* e = getenv("SFB_DIRECT_C")) d.C = std::max(2, atoi(e));
+  // tuning overrides, clamped to what the kernels' shared memory holds: R rows
+  // of n2len in step 2 (and the 64-entry Rader row tables), C columns of A in
+  // step 1; both powers of two
+  auto pow2_floor = [](int x) { int r = 1; while (2 * r <= x) r *= 2; return r; };
+  if (const char* e = getenv("SFB_DIRECT_R"))
+    d.R = pow2_floor(std::min(std::max(1, atoi(e)), std::min(64, kDirectSmem2 / n2len)));
+  if (const char* e = getenv("SFB_DIRECT_C"))
+    d.C = pow2_floor(std::min(std::max(2, atoi(e)), std::max(2, kDirectSmem / (int)d.A)));
   d.C_log2 = log2i(d.C);
   d.R_log2 = log2i(d.R);
   d.stA = make_stages(d.A);

@@ -212,16 +212,147 @@ __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(Ga
   }
 }
 
+// Persistent form of k_gather2 (SFB_GATHER_PERSIST): every CTA walks the
+// 256-target groups g = blockIdx.x, blockIdx.x + gridDim.x, ... -- round-robin,
+// so at any moment all CTAs work on one band of consecutive groups (one index
+// slice: the scattered output stores still merge in L2) -- and the next
+// group's h span is on its way (TMA bulk copy into the other half of a
+// double buffer) and its plan records in registers while the current group is
+// interpolated: no CTA-start latency after the first group.
+#ifndef SFB_GATHER3_MINB
+#define SFB_GATHER3_MINB 4
+#endif
+#ifndef SFB_GATHER_PERSIST_DEFAULT
+#define SFB_GATHER_PERSIST_DEFAULT 0
+#endif
+__device__ __forceinline__ bool span_fits(const GatherArgs& a, int2 sp) {
+  return sp.x >= 0 && sp.y < a.Kout && sp.y - sp.x + 1 <= kGatherSpan;
+}
+// the plan records (position, scale, destination) of this thread's two
+// targets of group g into stage st of the record buffers (cp.async, no
+// registers held); out-of-range targets are zero-filled
+__device__ __forceinline__ void issue_grec(const GatherArgs& a, int64_t g, double (*rp)[2][kGatherThreads],
+                                          double (*rs)[2][kGatherThreads],
+                                          int (*rd)[2][kGatherThreads], int st) {
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int64_t j = g * kGatherGroup + threadIdx.x + (int64_t)t * kGatherThreads;
+    const bool ok = j < a.M2;
+    const int64_t jj = ok ? j : 0;
+    cp_async8z(&rp[st][t][threadIdx.x], a.pos + jj, ok ? 8 : 0);
+    cp_async8z(&rs[st][t][threadIdx.x], a.scale + jj, ok ? 8 : 0);
+    cp_async4z(&rd[st][t][threadIdx.x], a.perm + jj, ok ? 4 : 0);
+  }
+  cp_async_commit();
+}
+template <int M>
+__global__ void __launch_bounds__(kGatherThreads, SFB_GATHER3_MINB)
+    k_gather3(GatherArgs a, WinCoef C, int64_t n_groups) {
+  static_assert(kGatherTPT == 2, "two targets per thread");
+  __shared__ __align__(16) double2 hs[2][kGatherSpan];
+  __shared__ double rp[2][2][kGatherThreads], rs[2][2][kGatherThreads];
+  __shared__ int rd[2][2][kGatherThreads];
+  __shared__ __align__(8) unsigned long long mbar[2];
+  const int col = blockIdx.y;
+  const double2* h = a.h + (int64_t)col * a.Kout;
+  const int64_t stride = gridDim.x;
+  int64_t g = blockIdx.x;
+  if (g >= n_groups) return;
+  issue_grec(a, g, rp, rs, rd, 0);
+  int2 sp_cur = __ldg(a.span + g);
+  int2 sp_nxt = g + stride < n_groups ? __ldg(a.span + g + stride) : make_int2(-1, -1);
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+  }
+  __syncthreads();
+  pdl_wait();  // h is the previous kernel's output
+  if (threadIdx.x == 0) {
+    if (span_fits(a, sp_cur))
+      bulk_g2s(hs[0], h + sp_cur.x, (unsigned)((sp_cur.y - sp_cur.x + 1) * sizeof(double2)),
+               &mbar[0]);
+    else
+      mbar_arrive(&mbar[0]);
+  }
+  const double sg = a.conj_out ? -1.0 : 1.0;
+  for (int i = 0; g < n_groups; ++i, g += stride) {
+    const int b = i & 1;
+    const int64_t gn = g + stride;
+    // the other buffers were released by the barrier that ended iteration i-1
+    if (gn < n_groups) {
+      if (threadIdx.x == 0) {
+        if (span_fits(a, sp_nxt))
+          bulk_g2s(hs[b ^ 1], h + sp_nxt.x,
+                   (unsigned)((sp_nxt.y - sp_nxt.x + 1) * sizeof(double2)), &mbar[b ^ 1]);
+        else
+          mbar_arrive(&mbar[b ^ 1]);
+      }
+      issue_grec(a, gn, rp, rs, rd, b ^ 1);
+    } else {
+      cp_async_commit();  // keep the group count: wait<1> below covers stage b
+    }
+    const int2 sp = sp_cur;
+    sp_cur = sp_nxt;
+    if (gn + stride < n_groups) sp_nxt = __ldg(a.span + gn + stride);
+    cp_async_wait<1>();  // this thread's records of group g
+    const int64_t j0 = g * kGatherGroup + threadIdx.x;
+    const bool act0 = j0 < a.M2, act1 = j0 + kGatherThreads < a.M2;
+    const double p0 = act0 ? rp[b][0][threadIdx.x] : 0.0;
+    const double p1 = act1 ? rp[b][1][threadIdx.x] : p0;  // inactive: a window in range
+    mbar_wait(&mbar[b], (i >> 1) & 1);
+    if (act0) {
+      double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
+      if (span_fits(a, sp)) {
+        const double c0 = floor(p0), c1 = floor(p1);
+        const int64_t k0 = (int64_t)c0 + (1 - M) - a.s_lo, k1 = (int64_t)c1 + (1 - M) - a.s_lo;
+        window_dot2<M>(C, p0 - c0, p1 - c1, hs[b] + (k0 - sp.x), hs[b] + (k1 - sp.x), s0, s1);
+      } else {
+        s0 = gather_one<M>(a, h, p0, C);
+        if (act1) s1 = gather_one<M>(a, h, p1, C);
+      }
+      const double sc0 = rs[b][0][threadIdx.x];
+      a.out[(int64_t)rd[b][0][threadIdx.x] * a.batch + col] =
+          make_double2(s0.x * sc0, sg * (s0.y * sc0));
+      if (act1) {
+        const double sc1 = rs[b][1][threadIdx.x];
+        a.out[(int64_t)rd[b][1][threadIdx.x] * a.batch + col] =
+            make_double2(s1.x * sc1, sg * (s1.y * sc1));
+      }
+    }
+    __syncthreads();  // every read of hs[b] is done before it is refilled
+  }
+}
+
+bool gather_persistent() {
+  static const int v = [] {
+    const char* e = getenv("SFB_GATHER_PERSIST");
+    return e ? atoi(e) : SFB_GATHER_PERSIST_DEFAULT;
+  }();
+  return v != 0;
+}
+
 void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batch,
                 cudaStream_t s) {
   GatherArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, p.gp.span.p, h, out,
                p.g.M2,     p.fft.Kout,  p.g.N2,        p.fft.s_lo,  batch, p.gp.conj_out ? 1 : 0};
   const dim3 grid((unsigned)ceil_div(p.g.M2, (int64_t)kGatherGroup), batch);
+  const int64_t n_groups = ceil_div(p.g.M2, (int64_t)kGatherGroup);
+  // persistent: resident CTAs x SMs, fewer when there are fewer groups
+  auto pgrid = [&](auto kern) {
+    static int per_sm = -1;
+    if (per_sm < 0) SF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
+                                                                          kGatherThreads, 0));
+    return dim3((unsigned)std::min<int64_t>(n_groups, (int64_t)std::max(per_sm, 1) * p.sp.n_sms),
+                batch);
+  };
   switch (p.g.m2) {
-#define SF_CASE(MM)                                          \
-  case MM:                                                   \
-    if (kGatherTPT >= 2) launch_pdl(k_gather2<MM>, grid, dim3(kGatherThreads), 0, s, a, p.c2); \
-    else k_gather<MM><<<grid, kGatherThreads, 0, s>>>(a, p.c2);              \
+#define SF_CASE(MM)                                                                            \
+  case MM:                                                                                     \
+    if (kGatherTPT == 2 && gather_persistent())                                                \
+      launch_pdl(k_gather3<MM>, pgrid(k_gather3<MM>), dim3(kGatherThreads), 0, s, a, p.c2,     \
+                 n_groups);                                                                    \
+    else if (kGatherTPT >= 2) launch_pdl(k_gather2<MM>, grid, dim3(kGatherThreads), 0, s, a, p.c2); \
+    else k_gather<MM><<<grid, kGatherThreads, 0, s>>>(a, p.c2);                                \
     break;
     SF_CASE(2) SF_CASE(3) SF_CASE(4) SF_CASE(5) SF_CASE(6) SF_CASE(7) SF_CASE(8) SF_CASE(9)
     SF_CASE(10) SF_CASE(11) SF_CASE(12) SF_CASE(13) SF_CASE(14) SF_CASE(15) SF_CASE(16)

@@ -169,7 +169,9 @@ namespace sfb {
 // s = sqrt(max(0, 1 - x^2)), zero unless |x| < 1   (windows.py:106-125)
 __device__ inline double omega_sinh(double beta, double x) {
   if (!(fabs(x) < 1.0)) return 0.0;
-  const double s = sqrt(fmax(0.0, 1.0 - x * x));
+  // x*x rounded on its own (no fused 1 - x*x): the reference's numpy rounding,
+  // which matters near |x| = 1 where 1 - x^2 cancels
+  const double s = sqrt(fmax(0.0, 1.0 - __dmul_rn(x, x)));
   return exp(beta * (s - 1.0)) * (-expm1(-2.0 * beta * s)) / (-expm1(-2.0 * beta));
 }
 

@@ -579,7 +579,12 @@ class PeerDistributedFftNnfft:
     memory: the grid rows are packed straight into their owners' buffers, the
     two transposes are the column / row passes' stores, and the inverse column
     pass stores each h row into every rank whose targets read it.  Per
-    transform: four stream-ordered barriers and no data collective."""
+    transform: four stream-ordered barriers and no data collective.
+
+    The peer receive buffers are persistent and shared by every call, so calls
+    are serialised: each call's stream first waits on an event recorded at the
+    end of the previous call (whatever stream that was on).  Within one call
+    the barriers order every peer store before its reader."""
 
     def __init__(self, plan, group=None):
         import torch
@@ -598,6 +603,7 @@ class PeerDistributedFftNnfft:
         self.cols2 = IpcBuffer(plan.device, cols, self.coll)
         self.hrecv = IpcBuffer(plan.device, 16 * self.r.h_recv_elems(), self.coll)
         self._flag = torch.zeros(1, dtype=torch.float64, device=self.r.dev)
+        self._done = None  # event recorded at the end of the previous call
 
     def _barrier(self):
         """Every rank's peer stores have landed: a stream-ordered all-reduce
@@ -611,7 +617,11 @@ class PeerDistributedFftNnfft:
             dist.barrier(group=self.coll.group)
 
     def __call__(self, f_shard):
+        import torch
         r = self.r
+        cur = torch.cuda.current_stream(r.dev)
+        if self._done is not None:  # the previous call (any stream) has released the buffers
+            cur.wait_event(self._done)
         r.pack_rows_peer(f_shard, self.gridrecv.ptrs)
         self._barrier()
         r.colfwd_peer(r.unpack_rows_ptr(self.gridrecv.own), self.rows.ptrs)
@@ -620,7 +630,10 @@ class PeerDistributedFftNnfft:
         self._barrier()
         r.colinv_peer(self.cols2.own, self.hrecv.ptrs)
         self._barrier()
-        return r.gather_rows_ptr(self.hrecv.own)
+        out = r.gather_rows_ptr(self.hrecv.own)
+        self._done = torch.cuda.Event()
+        self._done.record(cur)
+        return out
 
     def close(self):
         for b in (self.gridrecv, self.rows, self.cols2, self.hrecv):

@@ -137,3 +137,15 @@ def test_oracle_adjoint_is_the_conjugate_transpose(golden):
     lhs = np.vdot(y, O.trafo(t, g["f"]))
     rhs = np.vdot(O.adjoint(t, y), g["f"])
     assert abs(lhs - rhs) <= 1e-14 * np.linalg.norm(g["f"]) * np.linalg.norm(y) * 64
+
+
+def test_chunked_oracle_matches_reference(golden):
+    """trafo_chunked (the bounded-memory oracle the full-size config-3 parity
+    test uses) against the reference's own output; chunks far smaller than
+    the inputs so every chunk boundary path runs."""
+    for name in ("nnfft_config3_small.npz", "nnfft_config1.npz"):
+        g = golden(name)
+        N, m = int(g["N"]), int(g["m"])
+        n_star, vs = O.rescale_frequencies(N, g["v"], 2.0, m)
+        out = O.trafo_chunked(n_star, vs, g["x"], g["f"], m1=m, m2=m, chunk=777)
+        assert rel(out, g["out"], g["f"]) <= 1e-15, name

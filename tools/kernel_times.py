@@ -56,3 +56,14 @@ for e in prof.events():
 for k, t in sorted(tot.items(), key=lambda kv: -kv[1]):
     print(f"{t / steps:9.2f} us/step  x{cnt[k] // steps}  {k[:100]}")
 print(f"{sum(tot.values()) / steps:9.2f} us/step total kernel time")
+# variant runs (tools/run_variants.sh): the first run saves its output, later
+# runs report their max deviation from it (relative to sum|f|)
+ref = os.environ.get("VAR_REF")
+if ref:
+    out = d_out.cpu().numpy()
+    if os.path.exists(ref):
+        base = np.load(ref)
+        fl1 = float(np.abs(np.asarray(d_c.cpu() if cfg.get("sinc") else d_f.cpu())).sum())
+        print(f"max|out - base| / sum|f| = {float(np.max(np.abs(out - base))) / fl1:.3e}")
+    else:
+        np.save(ref, out)
