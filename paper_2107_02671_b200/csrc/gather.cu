@@ -127,6 +127,21 @@ __device__ __forceinline__ double2 gather_one(const GatherArgs& a, const double2
   return s;
 }
 
+#ifndef SFB_GATHER_ABL
+#define SFB_GATHER_ABL 0  // timing ablations (wrong results): 1 sorted stores, 2 no windows
+#endif
+#ifndef SFB_GATHER_RECTMA
+#define SFB_GATHER_RECTMA 0  // plan records by bulk copies (needs group-padded tables)
+#endif
+#ifndef SFB_GATHER_OCTET
+#define SFB_GATHER_OCTET 1  // k_gather2 on the octet-ordered records
+#endif
+#ifndef SFB_GATHER_HINT
+#define SFB_GATHER_HINT 0  // L2 hints: 1 streaming record loads, 2 span copy evict-last
+#endif
+#ifndef SFB_GATHER_PF
+#define SFB_GATHER_PF 0  // L2 prefetch distance in CTAs (0: off)
+#endif
 #ifndef SFB_GATHER_TMA
 #define SFB_GATHER_TMA 1  // the h span staged by one TMA bulk copy
 #endif
@@ -141,11 +156,31 @@ template <int M>
 __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(GatherArgs a,
                                                                             WinCoef C) {
   constexpr int NP = kGatherTPT / 2;
-  __shared__ double2 hs[kGatherSpan];
+  __shared__ __align__(128) double2 hs[kGatherSpan];  // bank group of hs[i] = i mod 8
   const int64_t jb = (int64_t)blockIdx.x * kGatherGroup + threadIdx.x;
   const int col = blockIdx.y;
   const double2* h = a.h + (int64_t)col * a.Kout;
   pdl_trigger();
+#if SFB_GATHER_TMA
+  __shared__ __align__(8) unsigned long long mbar;
+  if (threadIdx.x == 0) mbar_init(&mbar, 1);
+#endif
+#if SFB_GATHER_RECTMA
+  // the group's plan records (positions, scales, destinations: contiguous,
+  // padded to whole groups at plan time) arrive by three bulk copies issued
+  // at once -- no per-thread loads in front of the span copy
+  __shared__ __align__(16) double rpos[kGatherGroup], rsc[kGatherGroup];
+  __shared__ __align__(16) int rdst[kGatherGroup];
+  __shared__ __align__(8) unsigned long long mbar_r;
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar_r, 1);
+    const int64_t j0 = (int64_t)blockIdx.x * kGatherGroup;
+    mbar_expect_tx(&mbar_r, kGatherGroup * (2 * sizeof(double) + sizeof(int)));
+    bulk_g2s_tx(rpos, a.pos + j0, kGatherGroup * sizeof(double), &mbar_r);
+    bulk_g2s_tx(rsc, a.scale + j0, kGatherGroup * sizeof(double), &mbar_r);
+    bulk_g2s_tx(rdst, a.perm + j0, kGatherGroup * sizeof(int), &mbar_r);
+  }
+#endif
   const int2 sp = __ldg(a.span + blockIdx.x);
   const int64_t klo = sp.x, khi = sp.y;
   const bool staged = klo >= 0 && khi < a.Kout && khi - klo + 1 <= kGatherSpan;
@@ -153,6 +188,10 @@ __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(Ga
   // loads are in flight while this CTA waits for h
   double pos[2 * NP], sc[2 * NP];
   int dst[2 * NP];
+#if SFB_GATHER_RECTMA
+  __syncthreads();  // mbar_r initialised before anyone polls it
+  mbar_wait(&mbar_r, 0);
+#endif
 #pragma unroll
   for (int t = 0; t < 2 * NP; ++t) {
     const int64_t j = jb + (int64_t)t * kGatherThreads;
@@ -160,24 +199,64 @@ __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(Ga
     sc[t] = 0.0;
     dst[t] = -1;
     if (j < a.M2) {
+#if SFB_GATHER_ABL & 8  // ablation: no record loads (positions inside the span)
+      pos[t] = (double)(klo + a.s_lo + 8) + 0.001 * (threadIdx.x & 255);
+      sc[t] = 1.0;
+      dst[t] = (int)j;
+#elif SFB_GATHER_RECTMA
+      pos[t] = rpos[threadIdx.x + t * kGatherThreads];
+      sc[t] = rsc[threadIdx.x + t * kGatherThreads];
+      dst[t] = rdst[threadIdx.x + t * kGatherThreads];
+#elif SFB_GATHER_HINT & 1  // streaming record loads (evict-first in L2)
+      pos[t] = __ldcs(a.pos + j);
+      sc[t] = __ldcs(a.scale + j);
+      dst[t] = __ldcs(a.perm + j);
+#else
       pos[t] = __ldg(a.pos + j);
       sc[t] = __ldg(a.scale + j);
       dst[t] = __ldg(a.perm + j);
+#endif
     }
   }
   pdl_wait();  // h is the previous kernel's output
+#if SFB_GATHER_ABL & 4  // ablation: no span copy (smem left as is)
+  if (false) {
+#elif SFB_GATHER_TMA
+  if (true) {
+#endif
 #if SFB_GATHER_TMA
   // the span is one contiguous range: one bulk copy on the TMA engine,
   // completing on an mbarrier (no per-thread copy instructions)
-  __shared__ __align__(8) unsigned long long mbar;
   if (staged && threadIdx.x == 0) {
-    mbar_init(&mbar, 1);
+#if SFB_GATHER_HINT & 2  // the span copy marks h evict-last in L2
+    bulk_g2s_hint<true>(hs, h + klo, (unsigned)((khi - klo + 1) * sizeof(double2)), &mbar);
+#else
     bulk_g2s(hs, h + klo, (unsigned)((khi - klo + 1) * sizeof(double2)), &mbar);
+#endif
   }
+#if SFB_GATHER_PF
+  // L2 prefetch for the group SFB_GATHER_PF CTAs ahead (about one resident
+  // wave: the CTA that will start when this one ends) -- its plan records and
+  // its h span -- so CTA start waits on L2, not DRAM
+  if (threadIdx.x == 32) {
+    const int64_t gf = (int64_t)blockIdx.x + SFB_GATHER_PF;
+    if (gf * kGatherGroup + kGatherGroup <= a.M2) {
+      bulk_prefetch_l2(a.pos + gf * kGatherGroup, kGatherGroup * sizeof(double));
+      bulk_prefetch_l2(a.scale + gf * kGatherGroup, kGatherGroup * sizeof(double));
+      bulk_prefetch_l2(a.perm + gf * kGatherGroup, kGatherGroup * sizeof(int));
+      const int2 spf = __ldg(a.span + gf);
+      if (spf.x >= 0 && spf.y < a.Kout && spf.y - spf.x + 1 <= kGatherSpan)
+        bulk_prefetch_l2(h + spf.x, (unsigned)((spf.y - spf.x + 1) * sizeof(double2)));
+    }
+  }
+#endif
   if (staged) {
     __syncthreads();  // the barrier is initialised before anyone polls it
     mbar_wait(&mbar, 0);
   }
+#if SFB_GATHER_TMA
+  }
+#endif
 #else
   if (staged) {
     for (int64_t i = threadIdx.x; i <= khi - klo; i += kGatherThreads)
@@ -199,158 +278,123 @@ __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(Ga
     if (staged) {
       const double c0 = floor(p0), c1 = floor(p1);
       const int64_t k0 = (int64_t)c0 + (1 - M) - a.s_lo, k1 = (int64_t)c1 + (1 - M) - a.s_lo;
+#if SFB_GATHER_ABL & 2  // ablation (timing only): taps read, no window polynomials
+      const double2* h0 = hs + (k0 - klo);
+      const double2* h1 = hs + (k1 - klo);
+#pragma unroll
+      for (int t = 0; t < 2 * M; ++t) {
+        s0.x += h0[t].x * p0, s0.y += h0[t].y * p0;
+        s1.x += h1[t].x * p1, s1.y += h1[t].y * p1;
+      }
+#else
       window_dot2<M>(C, p0 - c0, p1 - c1, hs + (k0 - klo), hs + (k1 - klo), s0, s1);
+#endif
     } else {
       s0 = gather_one<M>(a, h, p0, C);
       if (dst[2 * q + 1] >= 0) s1 = gather_one<M>(a, h, p1, C);
     }
+#if SFB_GATHER_ABL & 1  // ablation (timing only): sorted-order stores instead of scattered
+    a.out[(jb + 2 * q * kGatherThreads) * a.batch + col] =
+        make_double2(s0.x * sc[2 * q], sg * (s0.y * sc[2 * q]));
+    if (dst[2 * q + 1] >= 0)
+      a.out[(jb + (2 * q + 1) * kGatherThreads) * a.batch + col] =
+          make_double2(s1.x * sc[2 * q + 1], sg * (s1.y * sc[2 * q + 1]));
+#else
     a.out[(int64_t)dst[2 * q] * a.batch + col] =
         make_double2(s0.x * sc[2 * q], sg * (s0.y * sc[2 * q]));
     if (dst[2 * q + 1] >= 0)
       a.out[(int64_t)dst[2 * q + 1] * a.batch + col] =
           make_double2(s1.x * sc[2 * q + 1], sg * (s1.y * sc[2 * q + 1]));
+#endif
   }
 }
 
-// Persistent form of k_gather2 (SFB_GATHER_PERSIST): every CTA walks the
-// 256-target groups g = blockIdx.x, blockIdx.x + gridDim.x, ... -- round-robin,
-// so at any moment all CTAs work on one band of consecutive groups (one index
-// slice: the scattered output stores still merge in L2) -- and the next
-// group's h span is on its way (TMA bulk copy into the other half of a
-// double buffer) and its plan records in registers while the current group is
-// interpolated: no CTA-start latency after the first group.
-#ifndef SFB_GATHER3_MINB
-#define SFB_GATHER3_MINB 4
+// SFB_GATHER_NT = 4: k_gather2 with each thread interpolating 4 targets
+// (j0 + t + i * T, i < 4) through one window_dotn -- every coefficient load
+// feeds 4 Horner chains -- over kGatherThreads / 2 threads per CTA, so a CTA
+// still covers kGatherGroup targets and one staged span.
+#ifndef SFB_GATHER_NT
+#define SFB_GATHER_NT 2
 #endif
-#ifndef SFB_GATHER_PERSIST_DEFAULT
-#define SFB_GATHER_PERSIST_DEFAULT 0
+#ifndef SFB_GATHER4_MINB
+#define SFB_GATHER4_MINB 12
 #endif
-__device__ __forceinline__ bool span_fits(const GatherArgs& a, int2 sp) {
-  return sp.x >= 0 && sp.y < a.Kout && sp.y - sp.x + 1 <= kGatherSpan;
-}
-// the plan records (position, scale, destination) of this thread's two
-// targets of group g into stage st of the record buffers (cp.async, no
-// registers held); out-of-range targets are zero-filled
-__device__ __forceinline__ void issue_grec(const GatherArgs& a, int64_t g, double (*rp)[2][kGatherThreads],
-                                          double (*rs)[2][kGatherThreads],
-                                          int (*rd)[2][kGatherThreads], int st) {
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int64_t j = g * kGatherGroup + threadIdx.x + (int64_t)t * kGatherThreads;
-    const bool ok = j < a.M2;
-    const int64_t jj = ok ? j : 0;
-    cp_async8z(&rp[st][t][threadIdx.x], a.pos + jj, ok ? 8 : 0);
-    cp_async8z(&rs[st][t][threadIdx.x], a.scale + jj, ok ? 8 : 0);
-    cp_async4z(&rd[st][t][threadIdx.x], a.perm + jj, ok ? 4 : 0);
-  }
-  cp_async_commit();
-}
 template <int M>
-__global__ void __launch_bounds__(kGatherThreads, SFB_GATHER3_MINB)
-    k_gather3(GatherArgs a, WinCoef C, int64_t n_groups) {
-  static_assert(kGatherTPT == 2, "two targets per thread");
-  __shared__ __align__(16) double2 hs[2][kGatherSpan];
-  __shared__ double rp[2][2][kGatherThreads], rs[2][2][kGatherThreads];
-  __shared__ int rd[2][2][kGatherThreads];
-  __shared__ __align__(8) unsigned long long mbar[2];
+__global__ void __launch_bounds__(kGatherGroup / 4, SFB_GATHER4_MINB) k_gather4(GatherArgs a,
+                                                                             WinCoef C) {
+  constexpr int T = kGatherGroup / 4, NT = 4;
+  __shared__ __align__(16) double2 hs[kGatherSpan];
+  __shared__ __align__(8) unsigned long long mbar;
+  const int64_t jb = (int64_t)blockIdx.x * kGatherGroup + threadIdx.x;
   const int col = blockIdx.y;
   const double2* h = a.h + (int64_t)col * a.Kout;
-  const int64_t stride = gridDim.x;
-  int64_t g = blockIdx.x;
-  if (g >= n_groups) return;
-  issue_grec(a, g, rp, rs, rd, 0);
-  int2 sp_cur = __ldg(a.span + g);
-  int2 sp_nxt = g + stride < n_groups ? __ldg(a.span + g + stride) : make_int2(-1, -1);
-  if (threadIdx.x == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+  pdl_trigger();
+  const int2 sp = __ldg(a.span + blockIdx.x);
+  const int64_t klo = sp.x, khi = sp.y;
+  const bool staged = klo >= 0 && khi < a.Kout && khi - klo + 1 <= kGatherSpan;
+  double pos[NT], sc[NT];
+  int dst[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const int64_t j = jb + (int64_t)t * T;
+    pos[t] = t > 0 ? pos[0] : 0.0;
+    sc[t] = 0.0;
+    dst[t] = -1;
+    if (j < a.M2) {
+      pos[t] = __ldg(a.pos + j);
+      sc[t] = __ldg(a.scale + j);
+      dst[t] = __ldg(a.perm + j);
+    }
   }
-  __syncthreads();
-  pdl_wait();  // h is the previous kernel's output
-  if (threadIdx.x == 0) {
-    if (span_fits(a, sp_cur))
-      bulk_g2s(hs[0], h + sp_cur.x, (unsigned)((sp_cur.y - sp_cur.x + 1) * sizeof(double2)),
-               &mbar[0]);
-    else
-      mbar_arrive(&mbar[0]);
+  pdl_wait();
+  if (staged && threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    bulk_g2s(hs, h + klo, (unsigned)((khi - klo + 1) * sizeof(double2)), &mbar);
   }
+  if (staged) {
+    __syncthreads();
+    mbar_wait(&mbar, 0);
+  }
+  if (dst[0] < 0) return;
   const double sg = a.conj_out ? -1.0 : 1.0;
-  for (int i = 0; g < n_groups; ++i, g += stride) {
-    const int b = i & 1;
-    const int64_t gn = g + stride;
-    // the other buffers were released by the barrier that ended iteration i-1
-    if (gn < n_groups) {
-      if (threadIdx.x == 0) {
-        if (span_fits(a, sp_nxt))
-          bulk_g2s(hs[b ^ 1], h + sp_nxt.x,
-                   (unsigned)((sp_nxt.y - sp_nxt.x + 1) * sizeof(double2)), &mbar[b ^ 1]);
-        else
-          mbar_arrive(&mbar[b ^ 1]);
-      }
-      issue_grec(a, gn, rp, rs, rd, b ^ 1);
-    } else {
-      cp_async_commit();  // keep the group count: wait<1> below covers stage b
+  double2 s[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) s[t] = make_double2(0.0, 0.0);
+  if (staged) {
+    double d[NT];
+    const double2* hp[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const double c = floor(pos[t]);
+      d[t] = pos[t] - c;
+      hp[t] = hs + ((int64_t)c + (1 - M) - a.s_lo - klo);
     }
-    const int2 sp = sp_cur;
-    sp_cur = sp_nxt;
-    if (gn + stride < n_groups) sp_nxt = __ldg(a.span + gn + stride);
-    cp_async_wait<1>();  // this thread's records of group g
-    const int64_t j0 = g * kGatherGroup + threadIdx.x;
-    const bool act0 = j0 < a.M2, act1 = j0 + kGatherThreads < a.M2;
-    const double p0 = act0 ? rp[b][0][threadIdx.x] : 0.0;
-    const double p1 = act1 ? rp[b][1][threadIdx.x] : p0;  // inactive: a window in range
-    mbar_wait(&mbar[b], (i >> 1) & 1);
-    if (act0) {
-      double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
-      if (span_fits(a, sp)) {
-        const double c0 = floor(p0), c1 = floor(p1);
-        const int64_t k0 = (int64_t)c0 + (1 - M) - a.s_lo, k1 = (int64_t)c1 + (1 - M) - a.s_lo;
-        window_dot2<M>(C, p0 - c0, p1 - c1, hs[b] + (k0 - sp.x), hs[b] + (k1 - sp.x), s0, s1);
-      } else {
-        s0 = gather_one<M>(a, h, p0, C);
-        if (act1) s1 = gather_one<M>(a, h, p1, C);
-      }
-      const double sc0 = rs[b][0][threadIdx.x];
-      a.out[(int64_t)rd[b][0][threadIdx.x] * a.batch + col] =
-          make_double2(s0.x * sc0, sg * (s0.y * sc0));
-      if (act1) {
-        const double sc1 = rs[b][1][threadIdx.x];
-        a.out[(int64_t)rd[b][1][threadIdx.x] * a.batch + col] =
-            make_double2(s1.x * sc1, sg * (s1.y * sc1));
-      }
-    }
-    __syncthreads();  // every read of hs[b] is done before it is refilled
+    window_dotn<M, NT>(C, d, hp, s);
+  } else {
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+      if (dst[t] >= 0) s[t] = gather_one<M>(a, h, pos[t], C);
   }
-}
-
-bool gather_persistent() {
-  static const int v = [] {
-    const char* e = getenv("SFB_GATHER_PERSIST");
-    return e ? atoi(e) : SFB_GATHER_PERSIST_DEFAULT;
-  }();
-  return v != 0;
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+    if (dst[t] >= 0)
+      a.out[(int64_t)dst[t] * a.batch + col] =
+          make_double2(s[t].x * sc[t], sg * (s[t].y * sc[t]));
 }
 
 void run_gather(const NnfftPlanImpl& p, const double2* h, double2* out, int batch,
                 cudaStream_t s) {
-  GatherArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, p.gp.span.p, h, out,
+  // k_gather2 reads the octet-ordered records (bank-conflict-free span loads)
+  const bool oct = kGatherTPT == 2 && p.gp.opos.p != nullptr && SFB_GATHER_OCTET;
+  GatherArgs a{oct ? p.gp.opos.p : p.gp.pos.p, oct ? p.gp.operm.p : p.gp.perm.p,
+               oct ? p.gp.oscale.p : p.gp.scale.p, p.gp.span.p, h, out,
                p.g.M2,     p.fft.Kout,  p.g.N2,        p.fft.s_lo,  batch, p.gp.conj_out ? 1 : 0};
   const dim3 grid((unsigned)ceil_div(p.g.M2, (int64_t)kGatherGroup), batch);
-  const int64_t n_groups = ceil_div(p.g.M2, (int64_t)kGatherGroup);
-  // persistent: resident CTAs x SMs, fewer when there are fewer groups
-  auto pgrid = [&](auto kern) {
-    static int per_sm = -1;
-    if (per_sm < 0) SF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
-                                                                          kGatherThreads, 0));
-    return dim3((unsigned)std::min<int64_t>(n_groups, (int64_t)std::max(per_sm, 1) * p.sp.n_sms),
-                batch);
-  };
   switch (p.g.m2) {
 #define SF_CASE(MM)                                                                            \
   case MM:                                                                                     \
-    if (kGatherTPT == 2 && gather_persistent())                                                \
-      launch_pdl(k_gather3<MM>, pgrid(k_gather3<MM>), dim3(kGatherThreads), 0, s, a, p.c2,     \
-                 n_groups);                                                                    \
+    if (SFB_GATHER_NT == 4 && kGatherTPT == 2)                                                 \
+      launch_pdl(k_gather4<MM>, grid, dim3(kGatherGroup / 4), 0, s, a, p.c2);                  \
     else if (kGatherTPT >= 2) launch_pdl(k_gather2<MM>, grid, dim3(kGatherThreads), 0, s, a, p.c2); \
     else k_gather<MM><<<grid, kGatherThreads, 0, s>>>(a, p.c2);                                \
     break;

@@ -104,6 +104,15 @@ struct GatherPlan {
   DevArray<int> perm;
   DevArray<double> scale;
   DevArray<int2> span;  // per gather CTA: {klo, khi} h range (h index k' = s - s_lo)
+  // the same records in "octet order" for the single-column gather (k_gather2):
+  // inside every full group of kGatherGroup targets, the targets are dealt
+  // to threads so that the 8 lanes of each quarter-warp have pairwise distinct
+  // window starts mod 8 (or equal starts) -- their 16-byte shared-memory loads
+  // of the staged h span are then free of bank conflicts (plan.cu
+  // k_octet_order).  pos / scale / perm above stay position-sorted for the
+  // batched gather's rolling windows.
+  DevArray<double> opos, oscale;
+  DevArray<int> operm;
 };
 
 // Pruned Bluestein: h_{s_lo + k'} = Q[k'] * sum_l (g_l P_l) b_{k'-l},
@@ -202,6 +211,7 @@ void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, 
 void fuse_target_weights(NnfftPlanImpl& p, const double* w_dev, cudaStream_t stream);
 
 // ----- fft.cu
+void octet_order(NnfftPlanImpl& p, int64_t M2, cudaStream_t stream);  // GatherPlan::opos/oscale/operm
 void build_fft(NnfftPlanImpl& p, cudaStream_t stream);
 // grid[batch][K] -> h[batch][Kout] (work: batch*L complex scratch)
 void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work, int batch,

@@ -290,6 +290,50 @@ __global__ void k_tgt_tables(const double* x, const int* perm, int64_t n, double
 
 // h range [klo, khi] (k' = s - s_lo) read by each gather CTA of kGatherGroup
 // sorted targets; {-1, -1} (never staged) if it does not fit in int
+__global__ void k_pad_targets(double* pos, double* scale, int* perm, int64_t n, int64_t npad) {
+  for (int64_t j = n + threadIdx.x; j < npad; j += blockDim.x) {
+    pos[j] = pos[n - 1];
+    scale[j] = 0.0;
+    perm[j] = -1;
+  }
+}
+
+// Octet order of one full gather group (one CTA of kGatherGroup threads per
+// group): the group's targets (position-sorted) are stably sorted by the
+// residue r = (floor(pos) - floor(pos_first)) mod 8 of their window start in
+// the staged span, and the element at rank p of that order goes to lane
+// q = p / 32 of octet o = p % 32, i.e. record n = (o / 16) * T + (o % 16) * 8 + q
+// (thread t of k_gather2 takes records t and t + T; its quarter-warp is the 8
+// consecutive t).  Balanced residues give every octet one target per residue;
+// dense groups (few distinct cells) give octets whose equal residues share a
+// cell, i.e. one broadcast address.  A partial last group is left sorted.
+__global__ void k_octet_order(const double* pos, const double* scale, const int* perm,
+                              int64_t M2, double* opos, double* oscale, int* operm) {
+  constexpr int G = kGatherGroup, T = kGatherThreads;
+  __shared__ int res[G];
+  const int64_t j0 = (int64_t)blockIdx.x * G;
+  const int i = threadIdx.x;
+  const int64_t j = j0 + i;
+  if (j0 + G > M2) {  // partial group: copy
+    if (j < M2) opos[j] = pos[j], oscale[j] = scale[j], operm[j] = perm[j];
+    return;
+  }
+  const double base = floor(pos[j0]);
+  const int r = (int)((int64_t)(floor(pos[j]) - base) & 7);
+  res[i] = r;
+  __syncthreads();
+  int rank = 0;
+  for (int k = 0; k < G; ++k) {
+    const int rk = res[k];
+    rank += (rk < r) || (rk == r && k < i);
+  }
+  const int o = rank % 32, q = rank / 32;
+  const int64_t n = j0 + (o / 16) * T + (o % 16) * 8 + q;
+  opos[n] = pos[j];
+  oscale[n] = scale[j];
+  operm[n] = perm[j];
+}
+
 __global__ void k_gather_spans(const double* pos, int64_t n, int64_t nblk, int m2, int64_t s_lo,
                                int2* span) {
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -552,7 +596,11 @@ void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, 
                    int64_t force_s_lo, int64_t force_kout) {
     Scratch kin(sizeof(unsigned long long) * M2, s), kout(sizeof(unsigned long long) * M2, s);
     Scratch iin(sizeof(int) * M2, s);
-    p.gp.perm.alloc(M2);
+    // pos / scale / perm are padded to whole gather groups (a group's records
+    // are fetched by fixed-size bulk copies): pos repeats the last position,
+    // scale 0, perm -1
+    const int64_t m2pad = ceil_div(M2, (int64_t)kGatherGroup) * kGatherGroup;
+    p.gp.perm.alloc(m2pad);
     const int cbits = key_bits((uint64_t)(2 * N2 + 2));
     const int64_t slice = gather_slice();
     k_tgt_keys<<<blocks(M2), 256, 0, s>>>(x, M2, ratio, pos_scale, N2, cbits, slice,
@@ -569,8 +617,8 @@ void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, 
                                               kout.as<unsigned long long>(), iin.as<int>(),
                                               p.gp.perm.p, (int)M2, 0, bits, s));
     }
-    p.gp.pos.alloc(M2);
-    p.gp.scale.alloc(M2);
+    p.gp.pos.alloc(m2pad);
+    p.gp.scale.alloc(m2pad);
     Scratch bad(sizeof(unsigned long long), s);
     SF_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
     k_tgt_tables<<<blocks(M2), 256, 0, s>>>(x, p.gp.perm.p, M2, ratio, pos_scale, ts.hat1 ? 1 : 0,
@@ -579,6 +627,10 @@ void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, 
     SF_LAUNCH_CHECK();
     if (read1(bad.as<unsigned long long>(), s))
       fail(2, "nnfft_plan: phi_hat_1(N x_j) must be strictly positive at every node");
+    if (m2pad > M2) {
+      k_pad_targets<<<1, 256, 0, s>>>(p.gp.pos.p, p.gp.scale.p, p.gp.perm.p, M2, m2pad);
+      SF_LAUNCH_CHECK();
+    }
     double plo, phi;
     device_minmax(p.gp.pos.p, M2, s, &plo, &phi);
     int64_t s_lo = (int64_t)std::floor(plo) + 1 - m2;
@@ -595,6 +647,32 @@ void build_targets(NnfftPlanImpl& p, const double* x, int64_t M2, double ratio, 
     p.gp.span.alloc(nblk);
     k_gather_spans<<<blocks(nblk), 256, 0, s>>>(p.gp.pos.p, M2, nblk, m2, s_lo, p.gp.span.p);
     SF_LAUNCH_CHECK();
+    octet_order(p, M2, s);
+}
+
+void octet_order(NnfftPlanImpl& p, int64_t M2, cudaStream_t s) {
+  static_assert(kGatherGroup == 2 * kGatherThreads && kGatherThreads % 8 == 0,
+                "octet order assumes two targets per thread");
+  const int64_t m2pad = p.gp.pos.n;
+  if (p.gp.opos.n != m2pad) {
+    p.gp.opos.alloc(m2pad);
+    p.gp.oscale.alloc(m2pad);
+    p.gp.operm.alloc(m2pad);
+  }
+  if (m2pad > M2) {  // padding records as in pos / scale / perm
+    SF_CUDA(cudaMemcpyAsync(p.gp.opos.p + M2, p.gp.pos.p + M2, sizeof(double) * (m2pad - M2),
+                            cudaMemcpyDeviceToDevice, s));
+    SF_CUDA(cudaMemcpyAsync(p.gp.oscale.p + M2, p.gp.scale.p + M2,
+                            sizeof(double) * (m2pad - M2), cudaMemcpyDeviceToDevice, s));
+    SF_CUDA(cudaMemcpyAsync(p.gp.operm.p + M2, p.gp.perm.p + M2, sizeof(int) * (m2pad - M2),
+                            cudaMemcpyDeviceToDevice, s));
+  }
+  const int64_t ngroups = ceil_div(M2, (int64_t)kGatherGroup);
+  if (ngroups > 0)
+    k_octet_order<<<(unsigned)ngroups, kGatherGroup, 0, s>>>(p.gp.pos.p, p.gp.scale.p, p.gp.perm.p,
+                                                            M2, p.gp.opos.p, p.gp.oscale.p,
+                                                            p.gp.operm.p);
+  SF_LAUNCH_CHECK();
 }
 
 void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cudaStream_t s) {
@@ -677,6 +755,8 @@ void dist_support(const NnfftPlanImpl& p, cudaStream_t s, int64_t out[4]) {
 
 void fuse_target_weights(NnfftPlanImpl& p, const double* w_dev, cudaStream_t s) {
   k_mul_scale<<<blocks(p.g.M2), 256, 0, s>>>(p.gp.scale.p, p.gp.perm.p, w_dev, p.g.M2);
+  SF_LAUNCH_CHECK();
+  k_mul_scale<<<blocks(p.g.M2), 256, 0, s>>>(p.gp.oscale.p, p.gp.operm.p, w_dev, p.g.M2);
   SF_LAUNCH_CHECK();
 }
 

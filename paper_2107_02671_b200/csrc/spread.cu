@@ -117,6 +117,100 @@ __device__ __forceinline__ void flush_tile(const SpreadArgs& a, W& S, int tile, 
   __syncwarp();
 }
 
+#ifndef SFB_SPREAD_PM
+#define SFB_SPREAD_PM 0
+#endif
+// Pair-major form of one block (SFB_SPREAD_PM): a lane's NS (2 or 4) sources
+// are evaluated together, tap pair by tap pair -- every coefficient (a
+// uniform constant-bank load) feeds NS Horner chains instead of 2 -- and each
+// pair's two taps are added into the tile accumulator as soon as they are
+// formed, so no 2m-tap register array is held (~40 fewer registers).  Lanes
+// of one cell are serialised by rounds computed once per block (rank among
+// the lanes with that cell); the hi and lo taps of one pair are added in two
+// steps, so lanes of different cells never touch one slot in the same step.
+__device__ __forceinline__ double2 as_c(double2 v) { return v; }
+__device__ __forceinline__ double2 as_c(double v) { return make_double2(v, 0.0); }
+template <int M, bool REAL, int NS, class FT>
+__device__ __forceinline__ void pm_block(const WinCoef& C, const double* pp, const FT* fs,
+                                         int lane, int cnt, int lcell, double2* acc) {
+  constexpr int P = window_degree(M);
+  constexpr int NE = P / 2 + 1;
+  constexpr int NO = (P + 1) / 2;
+  double u[NS];
+  double2 fv[NS];
+  VPow vw[NS];
+#pragma unroll
+  for (int t = 0; t < NS; ++t) {
+    const double d = pp[t] - floor(pp[t]);
+    u[t] = 2.0 * d - 1.0;
+    vw[t] = vpowers(u[t] * u[t]);
+    fv[t] = as_c(fs[32 * t + lane]);
+  }
+  int same = 0;
+  __match_all_sync(0xffffffffu, cnt > 0 ? lcell : -1 - lane, &same);
+  const unsigned peers = __match_any_sync(0xffffffffu, cnt > 0 ? lcell : (0x40000000 | lane));
+  const int myround = cnt > 0 ? __popc(peers & ((1u << lane) - 1u)) : -1;
+  const int nrounds = same ? 1 : __reduce_max_sync(0xffffffffu, (unsigned)(myround + 1));
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    double hr = 0.0, hm = 0.0, lr = 0.0, lm = 0.0;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const double E = poly<NE>(C.e[q], vw[t]);
+      const double O = poly<NO>(C.o[q], vw[t]);
+      double hi = fma(u[t], O, E), lo = fma(-u[t], O, E);
+      if (q == M - 1) {
+        const double d = pp[t] - floor(pp[t]);
+        hi *= sqrt(d);
+        lo *= sqrt(1.0 - d);
+      }
+      hr = fma(fv[t].x, hi, hr);
+      lr = fma(fv[t].x, lo, lr);
+      if (!REAL) {
+        hm = fma(fv[t].y, hi, hm);
+        lm = fma(fv[t].y, lo, lm);
+      }
+    }
+    const int ih = (q < M - 1) ? M + q : 2 * M - 1;
+    const int il = (q < M - 1) ? M - 1 - q : 0;
+    if (same) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        hr += __shfl_xor_sync(0xffffffffu, hr, o);
+        lr += __shfl_xor_sync(0xffffffffu, lr, o);
+        if (!REAL) {
+          hm += __shfl_xor_sync(0xffffffffu, hm, o);
+          lm += __shfl_xor_sync(0xffffffffu, lm, o);
+        }
+      }
+      if (lane == 0) {
+        double2 t = acc[lcell + ih];
+        t.x += hr, t.y += hm;
+        acc[lcell + ih] = t;
+        t = acc[lcell + il];
+        t.x += lr, t.y += lm;
+        acc[lcell + il] = t;
+      }
+      continue;
+    }
+    for (int r = 0; r < nrounds; ++r) {
+      if (myround == r) {
+        double2 t = acc[lcell + ih];
+        t.x += hr, t.y += hm;
+        acc[lcell + ih] = t;
+      }
+      __syncwarp();
+      if (myround == r) {
+        double2 t = acc[lcell + il];
+        t.x += lr, t.y += lm;
+        acc[lcell + il] = t;
+      }
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+}
+
 template <int M, bool REAL>
 #ifndef SFB_SPREAD_MINB
 #define SFB_SPREAD_MINB 2  // resident CTAs per SM (registers <= 65536 / (32 warps * MINB))
@@ -159,6 +253,19 @@ __global__ void __launch_bounds__(kSpreadWarps * 32, SFB_SPREAD_MINB) k_spread(S
     const int cnt = info & 255;
     const int lcell = info >> 8;
     const double2 p01 = S.pos[sd][0][lane], p23 = S.pos[sd][1][lane];
+#if SFB_SPREAD_PM
+    {
+      // padding slots have f = 0 and a harmless position; a block where no
+      // lane holds more than 2 sources runs the 2-source form
+      const double pp[4] = {p01.x, p01.y, p23.x, p23.y};
+      const auto* fs = &S.f[sf][0][0];
+      if (__any_sync(0xffffffffu, cnt > 2))
+        pm_block<M, REAL, 4>(C, pp, fs, lane, cnt, lcell, S.acc);
+      else
+        pm_block<M, REAL, 2>(C, pp, fs, lane, cnt, lcell, S.acc);
+      continue;
+    }
+#endif
     double2 r[2 * M];
 #pragma unroll
     for (int k = 0; k < 2 * M; ++k) r[k] = make_double2(0.0, 0.0);

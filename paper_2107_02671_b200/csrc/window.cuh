@@ -233,6 +233,41 @@ __device__ __forceinline__ void window_dot2(const WinCoef& C, double d0, double 
   }
 }
 
+// window_dot2 for NT targets at once: every coefficient feeds NT Horner
+// chains (the uniform coefficient loads amortised over NT targets).
+template <int M, int NT>
+__device__ __forceinline__ void window_dotn(const WinCoef& C, const double* d,
+                                            const double2* const* h, double2* s) {
+  constexpr int P = window_degree(M);
+  constexpr int NE = P / 2 + 1;
+  constexpr int NO = (P + 1) / 2;
+  double u[NT];
+  VPow vw[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    u[t] = 2.0 * d[t] - 1.0;
+    vw[t] = vpowers(u[t] * u[t]);
+  }
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    const int ih = (q < M - 1) ? M + q : 2 * M - 1;
+    const int il = (q < M - 1) ? M - 1 - q : 0;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const double E = poly<NE>(C.e[q], vw[t]);
+      const double O = poly<NO>(C.o[q], vw[t]);
+      double hi = fma(u[t], O, E), lo = fma(-u[t], O, E);
+      if (q == M - 1) {
+        hi *= sqrt(d[t]);
+        lo *= sqrt(1.0 - d[t]);
+      }
+      const double2 a = h[t][ih], b = h[t][il];
+      s[t].x = fma(a.x, hi, fma(b.x, lo, s[t].x));
+      s[t].y = fma(a.y, hi, fma(b.y, lo, s[t].y));
+    }
+  }
+}
+
 // Fourier transform of the sinh shape function, omega_hat(v)
 // (windows.py:143-160), all three branches; on the NNFFT path only the
 // w > 1e-3 branch is reachable.

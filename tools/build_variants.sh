@@ -6,5 +6,5 @@ cd "$(dirname "$0")/../paper_2107_02671_b200/csrc"
 for spec in "$@"; do
   name=${spec%%|*}; extra=${spec#*|}
   make -s -j8 BUILD=build_var_$name OUT=../lib/var_$name.so EXTRA="$extra" || exit 1
-  echo "built var_$name ($extra)"
+  rm -rf build_var_$name; echo "built var_$name ($extra)"
 done
