@@ -534,11 +534,27 @@ def run_b200(args, cfg):
     peak, peak_kind = peaks()
     achieved = alg[dom] / t_dom / 1e9
     # FP64 side of the same kernel: the window polynomials + tap MACs are the
-    # floor for spread/gather; DFMA per node from the kernel's
-    # structure (window.cuh): m pairs x (P + 1) + 2 sqrt (~8 each) + 4m MACs
+    # floor for spread/gather.  Counts per node from the
+    # committed ncu capture (profiles/ncu_fp64.json, tools/ncu_pipes.sh:
+    # sm__sass_thread_inst_executed_op_dfma / _fp64 per launch; a DFMA is 2
+    # flops, any other fp64 instruction 1); without it, the kernel's structure
+    # (window.cuh): m pairs x (P + 1) + 2 sqrt (~8 each) + 4m MACs
     P = 16 if m <= 2 else 15 if m <= 3 else 14 if m <= 6 else 13 if m <= 9 else 12
     dfma_node = m * (P + 1) + 16 + 4 * m * B
-    flops = {"spread": 2 * dfma_node * Ms, "gather": 2 * dfma_node * Mt, "fft": None}
+    fp64_node = {k: (dfma_node, 0, None, "kernel structure (window.cuh)")
+                 for k in ("spread", "gather")}
+    fj = os.path.join(ROOT, "profiles", "ncu_fp64.json")
+    if world == 1 and os.path.exists(fj):
+        with open(fj) as fh:
+            nc = json.load(fh).get(f"config{args.config}", {})
+        for k, d in nc.items():
+            units = Ms if k == "spread" else Mt
+            if d.get("dfma_thread_inst"):
+                fp64_node[k] = (d["dfma_thread_inst"] / units,
+                                (d["fp64_thread_inst"] - d["dfma_thread_inst"]) / units,
+                                d.get("fp64_pipe_active_pct"), "ncu (profiles/ncu_fp64.json)")
+    flops = {k: (2 * v[0] + v[1]) * (Ms if k == "spread" else Mt) for k, v in fp64_node.items()}
+    flops["fft"] = None
     # DRAM bytes per launch of that kernel from the committed ncu capture --
     # single-GPU only (a shard's kernels were not captured: null, not the
     # whole-problem figure)
@@ -733,7 +749,10 @@ def run_b200(args, cfg):
                              "achieved_tflops": flops[dom] / t_dom / 1e12,
                              "peak_tflops": fp64_peak,
                              "frac": flops[dom] / t_dom / 1e12 / fp64_peak,
-                             "dfma_per_node": dfma_node,
+                             "dfma_per_node": fp64_node[dom][0],
+                             "other_fp64_per_node": fp64_node[dom][1],
+                             "ncu_fp64_pipe_active_pct": fp64_node[dom][2],
+                             "counts_from": fp64_node[dom][3],
                              "peak_note": fp64_note}},
             "stage_ms": {n: float(stage[i]) for i, n in enumerate(names)},
             "plan_ms": plan_ms,

@@ -370,11 +370,14 @@ namespace sfb {
 void run_execute(const NnfftPlanImpl& p, const double2* f, double2* out, int batch,
                  cudaStream_t s) {
   if (batch >= kBatchedMin) return run_execute_batched(p, f, out, batch, s);
-  Scratch grid(sizeof(double2) * (size_t)p.g.K * batch, s);
+  // a single column's grid is padded to whole FFT rows (TMA column pass)
+  const bool pad = batch == 1 && p.fft.L1 > 0 && !p.fft.direct && !p.fft.single;
+  const int64_t kg = pad ? ceil_div(p.g.K, p.fft.L1) * p.fft.L1 : p.g.K;
+  Scratch grid(sizeof(double2) * (size_t)kg * batch, s);
   Scratch work(sizeof(double2) * (size_t)p.fft.work_elems() * batch, s);
   Scratch h(sizeof(double2) * (size_t)p.fft.Kout * batch, s);
   run_spread(p, f, grid.as<double2>(), batch, s);
-  run_fft(p, grid.as<double2>(), h.as<double2>(), work.as<double2>(), batch, s);
+  run_fft(p, grid.as<double2>(), h.as<double2>(), work.as<double2>(), batch, s, pad);
   run_gather(p, h.as<double2>(), out, batch, s);
 }
 

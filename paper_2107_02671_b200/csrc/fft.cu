@@ -30,6 +30,9 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "nnfft_impl.cuh"
 #include "fft_reg.cuh"
 
@@ -48,6 +51,22 @@ constexpr int kRowMax = 8192;         // largest row length L1
 constexpr int kColElems = SFB_FFT_COLELEMS;  // C * L2 per single-column column-kernel CTA
 constexpr int kColElemsB = 4096;             // per point-major (batched) CTA
 constexpr int kTwSplit = 4096;        // two-level W_L table split
+#ifndef SFB_FFT_BATCHLD
+#define SFB_FFT_BATCHLD 0  // register passes: all loads of a phase issued before first use
+#endif
+#ifndef SFB_FFT_ABL
+#define SFB_FFT_ABL 0  // timing ablations of k_colfwd_r1 (wrong results): 1 no loads, 2 no stores
+#endif
+#ifndef SFB_FFT_CPL
+#define SFB_FFT_CPL 0  // register column passes: exchange layout padded every 8 slots
+#endif
+#ifndef SFB_FFT_RPL
+#define SFB_FFT_RPL 0  // register row pass: padded every 16 slots
+#endif
+constexpr int kColPL = SFB_FFT_CPL, kRowPL = SFB_FFT_RPL;
+#ifndef SFB_FFT_CMINB
+#define SFB_FFT_CMINB 2
+#endif
 constexpr int64_t kFixMax = 2048;     // largest shortfall D of a short Bluestein length
 
 enum { IN_GP = 0, IN_PLAIN = 1 };     // input mode: g*P (execute) or plain array (plan)
@@ -705,17 +724,64 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_rb(FftBArgs x) {
 // Single-column (column-major [batch][*]) register-resident passes: the NB
 // vectors of a column CTA are NB consecutive n1 (as k_colfwd's C columns);
 // the row CTA holds one row (NB = 1).
-template <int N, int NBL, int T, int MINB, int R = 8>
+template <int N, int NBL, int T, int MINB, int R = 8, int PL = 0>
 __global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
   pdl_trigger();
   pdl_wait();  // reads the previous kernel's output
-  using F = RegFft<N, NBL, T, R>;
+  using F = RegFft<N, NBL, T, R, PL>;
   constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * F::NB;
   const double2* g = a.g + (int64_t)col * a.K;
   F f;
+#if SFB_FFT_BATCHLD
+  // every load of the pass issued before the first use (no branch around a
+  // load: out-of-range elements read index 0 and are zeroed after), so the
+  // thread's 2R loads are in flight together instead of one pair at a time
+  {
+    int64_t idx[F::BPT][R];
+    bool ok[F::BPT][R];
+#pragma unroll
+    for (int k = 0; k < F::BPT; ++k) {
+      const int u = F::but(k);
+      const int64_t n1 = c0 + F::vec(k);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int64_t n = n1 + a.L1 * (int64_t)F::template pos<S0>(u, r);
+        ok[k][r] = n1 < a.L1 && n < a.K;
+        idx[k][r] = ok[k][r] ? n : 0;
+      }
+    }
+    double2 pv[F::BPT][R];
+#if SFB_FFT_ABL & 1  // timing ablation: no input loads
+#pragma unroll
+    for (int k = 0; k < F::BPT; ++k)
+#pragma unroll
+      for (int r = 0; r < R; ++r) f.x[k][r] = pv[k][r] = make_double2((double)idx[k][r], 1.0);
+    if (false)
+#endif
+#pragma unroll
+    for (int k = 0; k < F::BPT; ++k)
+#pragma unroll
+      for (int r = 0; r < R; ++r) f.x[k][r] = __ldg(g + idx[k][r]);
+#if SFB_FFT_ABL & 1
+    if (false)
+#endif
+#pragma unroll
+    for (int k = 0; k < F::BPT; ++k)
+#pragma unroll
+      for (int r = 0; r < R; ++r) pv[k][r] = __ldg(a.P + idx[k][r]);
+#pragma unroll
+    for (int k = 0; k < F::BPT; ++k)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double2 gv = f.x[k][r];
+        if (a.conj_in) gv.y = -gv.y;
+        f.x[k][r] = ok[k][r] ? cmul(gv, pv[k][r]) : make_double2(0.0, 0.0);
+      }
+  }
+#else
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
@@ -731,8 +797,35 @@ __global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
       }
     }
   }
+#endif
   f.dif(sm, R == 16 ? a.st2x : a.st2, R == 16 ? a.tw2x : a.tw2);
   double2* Y = a.Y + (int64_t)col * a.L;
+#if SFB_FFT_BATCHLD
+  {
+    double2 tw[F::BPT][R];
+#pragma unroll
+    for (int k = 0; k < F::BPT; ++k) {
+      const int u = F::but(k);
+      const int64_t n1 = min(c0 + F::vec(k), a.L1 - 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        tw[k][r] = wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(R * u + r));
+    }
+#pragma unroll
+    for (int k = 0; k < F::BPT; ++k) {
+      const int u = F::but(k);
+      const int64_t n1 = c0 + F::vec(k);
+      if (n1 >= a.L1) continue;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+#if SFB_FFT_ABL & 2  // timing ablation: stores only for a NaN
+        if (f.x[k][r].x != f.x[k][r].x)
+#endif
+        Y[n1 + a.L1 * (int64_t)(R * u + r)] = cmul(f.x[k][r], tw[k][r]);
+      }
+    }
+  }
+#else
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
@@ -744,13 +837,145 @@ __global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
       Y[n1 + a.L1 * (int64_t)p] = cmul(f.x[k][r], wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(p)));
     }
   }
+#endif
 }
 
-template <int N, int T, int MINB, int R = 8>
+// ------------------------------------- TMA-pipelined persistent column pass
+// k_colfwd_r1 as a persistent kernel (one 512-thread CTA per SM, all 148
+// resident) whose tiles (NB = 4 adjacent columns x 1024 rows = 64 KB) move
+// with 2D TMA tensor copies through a 3-stage shared-memory ring: the tile
+// two ahead is loaded (cp.async.bulk.tensor.2d, UTMALDG) and the previous
+// tile is stored (cp.async.bulk.tensor.2d global <- shared, UTMASTG) while
+// the current one is transformed in registers.  The stage buffer that
+// received a tile serves as that tile's exchange buffer and then stages its
+// output.  The prechirp P of the next tile is prefetched into registers.
+// Single column (batch 1) with a grid padded to whole rows of L1.
+struct TmaMaps {
+  CUtensorMap in;   // grid g viewed as [rows][2 * L1] float64
+  CUtensorMap out;  // work Y viewed as [L2][2 * L1] float64
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1,
+                                            unsigned long long* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(mbar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, int c0, int c1,
+                                             const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+          reinterpret_cast<uint64_t>(tm)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+constexpr int kTmaStages = 3;
+constexpr int kTmaBox = 256;  // rows per TMA box (box dims <= 256)
+
+template <int N, int T>
+__global__ void __launch_bounds__(T, 1) k_colfwd_tma(FftArgs a, const __grid_constant__ TmaMaps tm,
+                                                     int ntiles) {
+  using F = RegFft<N, 2, T, 8>;
+  constexpr int R = 8, NB = F::NB, S0 = N / R;
+  constexpr int TILE = N * NB;  // double2 per tile
+  static_assert(F::BPT == 1, "one radix-8 butterfly per thread");
+  extern __shared__ __align__(128) double2 smt[];
+  __shared__ __align__(8) unsigned long long full[kTmaStages];
+  const int tid = threadIdx.x;
+  const int u = F::but(0), b = F::vec(0);
+  pdl_trigger();
+  if (tid == 0) {
+    for (int i = 0; i < kTmaStages; ++i) mbar_init(&full[i], 1);
+  }
+  __syncthreads();
+  pdl_wait();  // the grid is the previous kernel's output
+  // rows of the input that can hold nonzeros: the rest is zero (pruned)
+  const int in_rows = (int)((a.K + a.L1 - 1) / a.L1);
+  const int in_boxes = (in_rows + kTmaBox - 1) / kTmaBox;
+  auto issue_load = [&](int t, int st) {
+    double2* buf = smt + (size_t)st * TILE;
+    const int c0 = 2 * NB * t;  // float64 column of the tile
+    mbar_expect_tx(&full[st], (unsigned)(in_boxes * kTmaBox * NB * sizeof(double2)));
+    for (int q = 0; q < in_boxes; ++q)
+      tma_load_2d(buf + q * kTmaBox * NB, &tm.in, c0, q * kTmaBox, &full[st]);
+  };
+  int t = blockIdx.x;
+  if (tid == 0) {
+    if (t < ntiles) issue_load(t, 0);
+    if (t + (int)gridDim.x < ntiles) issue_load(t + gridDim.x, 1);
+  }
+  // P of this thread's 8 inputs, one tile ahead
+  auto load_p = [&](int tt, double2* pv) {
+    const int64_t n1 = (int64_t)tt * NB + b;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t n = n1 + a.L1 * (int64_t)(u + r * S0);
+      pv[r] = __ldg(a.P + (n < a.K ? n : 0));
+    }
+  };
+  double2 pv[R];
+  if (t < ntiles) load_p(t, pv);
+  F f;
+  for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
+    const int st = i % kTmaStages;
+    double2* buf = smt + (size_t)st * TILE;
+    const int64_t n1 = (int64_t)t * NB + b;
+    mbar_wait(&full[st], (i / kTmaStages) & 1);
+    // rows >= in_boxes * kTmaBox were not loaded: they are zero
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int row = u + r * S0;
+      const int64_t n = n1 + a.L1 * (int64_t)row;
+      double2 gv = row < in_boxes * kTmaBox ? buf[row * NB + b] : make_double2(0.0, 0.0);
+      if (a.conj_in) gv.y = -gv.y;
+      f.x[0][r] = n < a.K ? cmul(gv, pv[r]) : make_double2(0.0, 0.0);
+    }
+    // the output twiddles W_L^{n1 rev(p)} (L2-resident tables) and the next
+    // tile's P are in flight during the transform
+    double2 tw[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) tw[r] = wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(R * u + r));
+    if (t + (int)gridDim.x < ntiles) load_p(t + gridDim.x, pv);
+    __syncthreads();  // every input read: the stage becomes the exchange buffer
+    f.dif(buf, a.st2, a.tw2);
+    __syncthreads();  // exchanges done: the stage now stages the output tile
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[(R * u + r) * NB + b] = cmul(f.x[0][r], tw[r]);
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      const int c0 = 2 * NB * t;
+      for (int q = 0; q < N / kTmaBox; ++q)
+        tma_store_2d(&tm.out, c0, q * kTmaBox, buf + q * kTmaBox * NB);
+      bulk_commit();
+      // the load two tiles ahead reuses the stage of the PREVIOUS tile's
+      // output: its store (one group back) must have finished reading
+      const int t2 = t + 2 * gridDim.x;
+      if (t2 < ntiles) {
+        bulk_wait_read<1>();
+        issue_load(t2, (i + 2) % kTmaStages);
+      }
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // stores complete
+}
+
+template <int N, int T, int MINB, int R = 8, int PL = 0>
 __global__ void __launch_bounds__(T, MINB) k_rowmul_r1(FftArgs a) {
   pdl_trigger();
   pdl_wait();  // reads the previous kernel's output
-  using F = RegFft<N, 0, T, R>;
+  using F = RegFft<N, 0, T, R, PL>;
   constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
@@ -800,17 +1025,39 @@ __global__ void __launch_bounds__(T, MINB) k_rowmul_r1(FftArgs a) {
   }
 }
 
-template <int N, int NBL, int T, int MINB, int R = 8>
+template <int N, int NBL, int T, int MINB, int R = 8, int PL = 0>
 __global__ void __launch_bounds__(T, MINB) k_colinv_r1(FftArgs a) {
   pdl_trigger();
   pdl_wait();  // reads the previous kernel's output
-  using F = RegFft<N, NBL, T, R>;
+  using F = RegFft<N, NBL, T, R, PL>;
   constexpr int S0 = N / R;
   extern __shared__ double2 sm[];
   const int col = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * F::NB;
   const double2* Y = a.Y + (int64_t)col * a.L;
   F f;
+#if SFB_FFT_BATCHLD
+  {
+    double2 tw[F::BPT][R];
+#pragma unroll
+    for (int k = 0; k < F::BPT; ++k) {
+      const int u = F::but(k);
+      const int64_t n1 = min(c0 + F::vec(k), a.L1 - 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        f.x[k][r] = Y[n1 + a.L1 * (int64_t)(R * u + r)];
+        tw[k][r] = wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(R * u + r));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < F::BPT; ++k) {
+      const bool ok = c0 + F::vec(k) < a.L1;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        f.x[k][r] = ok ? cmul(cconj(f.x[k][r]), tw[k][r]) : make_double2(0.0, 0.0);
+    }
+  }
+#else
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
@@ -824,8 +1071,35 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_r1(FftArgs a) {
                          wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(p)));
     }
   }
+#endif
   f.dit(sm, R == 16 ? a.st2x : a.st2, R == 16 ? a.tw2x : a.tw2);
   double2* h = a.h + (int64_t)col * a.Kout;
+#if SFB_FFT_BATCHLD
+  {
+    double2 qv[F::BPT][R];
+#pragma unroll
+    for (int k = 0; k < F::BPT; ++k) {
+      const int u = F::but(k);
+      const int64_t n1 = c0 + F::vec(k);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int64_t kk = n1 + a.L1 * (int64_t)F::template pos<S0>(u, r);
+        qv[k][r] = __ldg(a.Q + ((kk < a.Kout && n1 < a.L1) ? kk : 0));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < F::BPT; ++k) {
+      const int u = F::but(k);
+      const int64_t n1 = c0 + F::vec(k);
+      if (n1 >= a.L1) continue;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int64_t kk = n1 + a.L1 * (int64_t)F::template pos<S0>(u, r);
+        if (kk < a.Kout) h[kk] = cmul(cconj(f.x[k][r]), qv[k][r]);
+      }
+    }
+  }
+#else
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
@@ -837,6 +1111,7 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_r1(FftArgs a) {
       if (kk < a.Kout) h[kk] = cmul(cconj(f.x[k][r]), __ldg(a.Q + kk));
     }
   }
+#endif
 }
 
 // ------------------------------------------- distributed (column-split) FFT
@@ -1699,13 +1974,16 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_rowmul_b<512, 3>, smem_bytes(kColElemsB));
   set_smem(k_colinv_b<512, 3>, smem_bytes(kColElemsB));
   set_reg_smem<2, 256, 4>();
-  set_smem(k_colfwd_r1<1024, 2, 512, 2>, sizeof(double2) * 4096);
-  set_smem(k_colinv_r1<1024, 2, 512, 2>, sizeof(double2) * 4096);
+  set_smem(k_colfwd_r1<1024, 2, 512, SFB_FFT_CMINB, 8, kColPL>,
+           sizeof(double2) * RegFft<1024, 2, 512, 8, kColPL>::SMEM_ELEMS);
+  set_smem(k_colinv_r1<1024, 2, 512, SFB_FFT_CMINB, 8, kColPL>,
+           sizeof(double2) * RegFft<1024, 2, 512, 8, kColPL>::SMEM_ELEMS);
   set_smem(k_colfwd_r1<1024, 2, 256, 2, 16>, sizeof(double2) * 4096);
   set_smem(k_colinv_r1<1024, 2, 256, 2, 16>, sizeof(double2) * 4096);
   set_smem(k_rowmul_r1<4096, 256, 2>, sizeof(double2) * 4096);
   set_smem(k_drowmul<4096, 256, 2>, sizeof(double2) * 4096);
-  set_smem(k_rowmul_r1<4096, 256, 2, 16>, sizeof(double2) * 4096);
+  set_smem(k_rowmul_r1<4096, 256, 2, 16, kRowPL>,
+           sizeof(double2) * RegFft<4096, 0, 256, 16, kRowPL>::SMEM_ELEMS);
   set_smem(k_drowmul<4096, 256, 2, 16>, sizeof(double2) * 4096);
   FftPlan& f = p.fft;
   const Geometry& g = p.g;
@@ -1951,23 +2229,78 @@ static bool reg_single(const FftPlan& f) {
   return !(e && atoi(e) == 0);
 }
 
-static void launch_reg_single(const FftArgs& a, const FftPlan& f, int batch, cudaStream_t s) {
-  constexpr int CBL = 2, CT = 512, CMINB = 2, RT = 256, RMINB = 2;
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) fail(3, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+// [rows][2 * row_len] float64 (rows of row_len complex), boxes of
+// {2 * NB, kTmaBox}; out-of-range rows read as zero
+static void encode_rows(CUtensorMap* m, const void* base, int64_t row_len, int64_t rows, int nb) {
+  const cuuint64_t dims[2] = {(cuuint64_t)(2 * row_len), (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)(2 * row_len * sizeof(double))};
+  const cuuint32_t box[2] = {(cuuint32_t)(2 * nb), (cuuint32_t)kTmaBox};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(
+      m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(3, "cuTensorMapEncodeTiled failed");
+}
+#ifndef SFB_FFT_TMA
+#define SFB_FFT_TMA 0  // TMA-pipelined persistent forward column pass (padded single column)
+#endif
+static bool fft_tma_enabled() {
+  static const int v = [] {
+    const char* e = getenv("SFB_FFT_TMA");
+    return e ? atoi(e) : SFB_FFT_TMA;
+  }();
+  return v != 0;
+}
+
+static void launch_reg_single(const FftArgs& a, const FftPlan& f, int batch, cudaStream_t s,
+                              bool padded, int n_sms) {
+  constexpr int CBL = 2, CT = 512, CMINB = SFB_FFT_CMINB, RT = 256, RMINB = 2;
   const size_t smc = sizeof(double2) * ((size_t)1024 << CBL), smr = sizeof(double2) * 4096;
+  const size_t smcp = sizeof(double2) * RegFft<1024, CBL, CT, 8, kColPL>::SMEM_ELEMS;
+  const size_t smrp = sizeof(double2) * RegFft<4096, 0, RT, 16, kRowPL>::SMEM_ELEMS;
   const dim3 gc((unsigned)ceil_div(f.L1, (int64_t)1 << CBL), batch);
   // programmatic dependent launches: each pass is scheduled during the
   // previous one's last wave and waits (griddepcontrol.wait) for its output
-  if (col16(f)) launch_pdl(k_colfwd_r1<1024, CBL, 256, 2, 16>, gc, dim3(256), smc, s, a);
-  else launch_pdl(k_colfwd_r1<1024, CBL, CT, CMINB>, gc, dim3(CT), smc, s, a);
+  if (padded && batch == 1 && !col16(f) && fft_tma_enabled()) {
+    TmaMaps tm;
+    encode_rows(&tm.in, a.g, f.L1, ceil_div(a.K, f.L1), 1 << CBL);
+    encode_rows(&tm.out, a.Y, f.L1, f.L2, 1 << CBL);
+    const int ntiles = (int)(f.L1 >> CBL);
+    const size_t smt = sizeof(double2) * ((size_t)1024 << CBL) * kTmaStages;
+    static bool attr = false;
+    if (!attr) {
+      SF_CUDA(cudaFuncSetAttribute(k_colfwd_tma<1024, CT>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smt));
+      attr = true;
+    }
+    launch_pdl(k_colfwd_tma<1024, CT>, dim3((unsigned)std::min(ntiles, n_sms)), dim3(CT), smt, s,
+               a, tm, ntiles);
+  } else if (col16(f)) {
+    launch_pdl(k_colfwd_r1<1024, CBL, 256, 2, 16>, gc, dim3(256), smc, s, a);
+  } else {
+    launch_pdl(k_colfwd_r1<1024, CBL, CT, CMINB, 8, kColPL>, gc, dim3(CT), smcp, s, a);
+  }
   const dim3 gr((unsigned)f.L2, batch);
-  if (row16(f)) launch_pdl(k_rowmul_r1<4096, RT, RMINB, 16>, gr, dim3(RT), smr, s, a);
+  if (row16(f)) launch_pdl(k_rowmul_r1<4096, RT, RMINB, 16, kRowPL>, gr, dim3(RT), smrp, s, a);
   else launch_pdl(k_rowmul_r1<4096, RT, RMINB>, gr, dim3(RT), smr, s, a);
   if (col16(f)) launch_pdl(k_colinv_r1<1024, CBL, 256, 2, 16>, gc, dim3(256), smc, s, a);
-  else launch_pdl(k_colinv_r1<1024, CBL, CT, CMINB>, gc, dim3(CT), smc, s, a);
+  else launch_pdl(k_colinv_r1<1024, CBL, CT, CMINB, 8, kColPL>, gc, dim3(CT), smcp, s, a);
 }
 
 void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work, int batch,
-             cudaStream_t s) {
+             cudaStream_t s, bool grid_padded) {
   const FftPlan& f = p.fft;
   if (f.direct) {
     DirectArgs a = make_direct_args(p);
@@ -1993,7 +2326,10 @@ void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* w
     return;
   }
   if (reg_single(f)) {
-    launch_reg_single(a, f, batch, s);
+    if (grid_padded)  // zero the row padding the TMA path reads past K
+      SF_CUDA(cudaMemsetAsync(const_cast<double2*>(grid) + p.g.K, 0,
+                              sizeof(double2) * (size_t)(ceil_div(p.g.K, f.L1) * f.L1 - p.g.K), s));
+    launch_reg_single(a, f, batch, s, grid_padded, p.sp.n_sms);
     launch_fix(p, grid, h, batch, 0, s);
     return;
   }

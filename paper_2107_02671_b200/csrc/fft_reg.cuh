@@ -65,7 +65,18 @@ __device__ __forceinline__ int rev8(int p) {
   return revr<N, 8>(p);
 }
 
-template <int N_, int NBL, int T, int R_ = 8>
+// Shared-memory slot of exchange element e: the XOR swizzle spad(e) (PL = 0)
+// or one pad slot every 2^PL elements (PL > 0): phys = e + (e >> PL).  With
+// padding, the R legs of a butterfly (elements eb + r S NB) sit at
+// base + off(r), base = eb + (eb >> PL) computed once per exchange and off(r)
+// a compile-time constant, so an exchange costs one address computation per
+// thread instead of R swizzles.  off(r) = r S NB + (r S NB >> PL) holds when
+// (eb mod 2^PL) + (r S NB mod 2^PL) < 2^PL for every leg: for S NB >= 2^PL
+// always; for the column passes (NB = 4, PL = 3) and S = 1, eb mod 8 = b < 4
+// and r S NB mod 8 <= 4; for the row pass (NB = 1, PL = 4), eb = 16 u.
+// Both layouts keep every quarter-warp's 16-byte accesses on distinct bank
+// groups for the shapes instantiated (fft.cu).
+template <int N_, int NBL, int T, int R_ = 8, int PL = 0>
 struct RegFft {
   using Sh = RegShape<N_, R_>;
   static constexpr int R = R_;
@@ -92,22 +103,45 @@ struct RegFft {
   template <int S>
   static constexpr int stage() { return ilogr(N / S, R) - 1; }
 
+  // smem elements per exchange buffer (the padded layout is 2^-PL larger)
+  static constexpr int SMEM_ELEMS = PL ? ((N << NBL) + ((N << NBL) >> PL)) : (N << NBL);
+  template <int S>
+  static constexpr int off(int r) {
+    return r * S * NB + ((r * S * NB) >> (PL ? PL : 0));
+  }
+  template <int S>
+  static __device__ __forceinline__ int pbase(int k) {
+    const int eb = (pos<S>(but(k), 0) << NBL) + vec(k);
+    return eb + (eb >> PL);
+  }
   template <int S>
   __device__ __forceinline__ void to_smem(double2* sm) const {
 #pragma unroll
     for (int k = 0; k < BPT; ++k) {
-      const int u = but(k), b = vec(k);
+      if constexpr (PL > 0) {
+        double2* p = sm + pbase<S>(k);
 #pragma unroll
-      for (int r = 0; r < R; ++r) sm[spad((pos<S>(u, r) << NBL) + b)] = x[k][r];
+        for (int r = 0; r < R; ++r) p[off<S>(r)] = x[k][r];
+      } else {
+        const int u = but(k), b = vec(k);
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[spad((pos<S>(u, r) << NBL) + b)] = x[k][r];
+      }
     }
   }
   template <int S>
   __device__ __forceinline__ void from_smem(const double2* sm) {
 #pragma unroll
     for (int k = 0; k < BPT; ++k) {
-      const int u = but(k), b = vec(k);
+      if constexpr (PL > 0) {
+        const double2* p = sm + pbase<S>(k);
 #pragma unroll
-      for (int r = 0; r < R; ++r) x[k][r] = sm[spad((pos<S>(u, r) << NBL) + b)];
+        for (int r = 0; r < R; ++r) x[k][r] = p[off<S>(r)];
+      } else {
+        const int u = but(k), b = vec(k);
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[k][r] = sm[spad((pos<S>(u, r) << NBL) + b)];
+      }
     }
   }
   // write own stride-S outputs, barrier, read own stride-S2 inputs (the

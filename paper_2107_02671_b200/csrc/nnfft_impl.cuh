@@ -214,8 +214,10 @@ void fuse_target_weights(NnfftPlanImpl& p, const double* w_dev, cudaStream_t str
 void octet_order(NnfftPlanImpl& p, int64_t M2, cudaStream_t stream);  // GatherPlan::opos/oscale/operm
 void build_fft(NnfftPlanImpl& p, cudaStream_t stream);
 // grid[batch][K] -> h[batch][Kout] (work: batch*L complex scratch)
+// grid_padded: grid holds whole rows of L1 (ceil(K / L1) * L1 elements per
+// column) -- the TMA column pass reads rows past K (zeroed by run_fft)
 void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* work, int batch,
-             cudaStream_t stream);
+             cudaStream_t stream, bool grid_padded = false);
 // point-major variant: grid[K][batch] -> h[Kout][batch] (Bluestein path only)
 bool fft_supports_point_major(const NnfftPlanImpl& p);
 // Distributed (column-split) FFT over `world` ranks (fft.cu; layouts there).

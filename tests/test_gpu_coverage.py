@@ -332,3 +332,29 @@ def test_short_bluestein_length_nfft():
     t = O.nfft_plan(N, x, 2.0, 6)
     assert relerr(sf.nfft_trafo(plan, c), O.nfft_trafo(t, c), c) <= TOL
     assert relerr(sf.nfft_adjoint(plan, y), O.nfft_adjoint(t, y), y) <= TOL
+
+
+def test_graph_cache_lru_many_outputs():
+    """Device-pointer executes replay cached CUDA graphs keyed by (f, out,
+    batch): first sighting runs directly, the second captures, more keys than
+    the cache holds (8) evict least-recently-used entries and recycle their
+    executable through cudaGraphExecUpdate.  Every call must give the same
+    output as the host-pointer path."""
+    import ctypes as C
+    torch = pytest.importorskip("torch")
+    from paper_2107_02671_b200 import _lib
+    v, x, f = nodes_and_coeffs(77, 20000, 15000, clustered=True)
+    N, vs = sf.rescale_frequencies(4096, v, 2.0, 8)
+    plan = sf.nnfft_plan(N, vs, x, m1=8, m2=8)
+    ref = sf.nnfft_trafo(plan, f)
+    d_fs = [torch.from_numpy(f * (k + 1)).cuda() for k in range(2)]
+    outs = [torch.empty(15000, dtype=torch.complex128, device="cuda") for _ in range(11)]
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for rep in range(3):
+        for i, o in enumerate(outs):
+            o.zero_()
+            _lib.check(_lib.lib.sincfft_nnfft_execute(plan.handle, d_fs[i % 2].data_ptr(),
+                                                      o.data_ptr(), 1, _lib.PTR_DEVICE, st))
+            torch.cuda.synchronize()
+            k = i % 2 + 1
+            assert relerr(o.cpu().numpy(), k * ref, k * f) <= 1e-14, (rep, i)

@@ -34,3 +34,41 @@ for name, ms in agg.items():
           f"{100 * a('sm__inst_executed_pipe_fp64.sum') / max(a('sm__inst_executed.sum'), 1):8.1f} "
           f"{(a('dram__bytes_read.sum') + a('dram__bytes_write.sum')) / 1e6:8.1f} "
           f"{a('sm__warps_active.avg.pct_of_peak_sustained_active'):6.1f}")
+
+
+def fp64_json(paths, out):
+    """profiles/ncu_fp64.json: per config and hot kernel, the ncu FP64 counts
+    per launch (DFMA and all fp64 thread instructions) and the FP64-pipe
+    utilisation -- bench.py derives roofline.fp64 from these."""
+    import json
+    import re
+    res = {}
+    for cfg, path in paths:
+        rows_ = [r for r in csv.reader(open(path)) if r]
+        hi_ = next(i for i, r in enumerate(rows_) if r[0] == "ID")
+        h_ = rows_[hi_]
+        ix_ = {c: i for i, c in enumerate(h_)}
+        per = OrderedDict()
+        for r in rows_[hi_ + 1:]:
+            if len(r) != len(h_):
+                continue
+            per.setdefault((r[ix_["ID"]], r[ix_["Kernel Name"]]), {})[r[ix_["Metric Name"]]] = \
+                float(r[ix_["Metric Value"]].replace(",", "") or 0)
+        d = {}
+        for (_, k), m in per.items():
+            name = re.sub(r"^(void )?(sfb::)?", "", k.split("(")[0]).split("<")[0]
+            kind = ("spread" if name in ("k_spread", "k_spread_b", "k_spread_dense") else
+                    "gather" if name in ("k_gather", "k_gather2", "k_gather4", "k_gather_b")
+                    else None)
+            if kind is None or kind in d:
+                continue
+            d[kind] = {"kernel": k.split("(")[0],
+                       "dfma_thread_inst": m.get("sm__sass_thread_inst_executed_op_dfma_pred_on.sum"),
+                       "fp64_thread_inst": m.get("sm__sass_thread_inst_executed_op_fp64_pred_on.sum"),
+                       "fp64_pipe_active_pct": m.get(
+                           "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                       "duration_us": m.get("gpu__time_duration.sum", 0) / 1e3}
+        res[f"config{cfg}"] = d
+    with open(out, "w") as fh:
+        json.dump(res, fh, indent=1)
+    return res
