@@ -307,6 +307,9 @@ __global__ void k_pad_targets(double* pos, double* scale, int* perm, int64_t n, 
 // consecutive t).  Balanced residues give every octet one target per residue;
 // dense groups (few distinct cells) give octets whose equal residues share a
 // cell, i.e. one broadcast address.  A partial last group is left sorted.
+#ifndef SFB_GATHER_PAIRS
+#define SFB_GATHER_PAIRS 1  // k_octet_pairs (same-cell pairs per thread) instead of k_octet_order
+#endif
 __global__ void k_octet_order(const double* pos, const double* scale, const int* perm,
                               int64_t M2, double* opos, double* oscale, int* operm) {
   constexpr int G = kGatherGroup, T = kGatherThreads;
@@ -332,6 +335,94 @@ __global__ void k_octet_order(const double* pos, const double* scale, const int*
   opos[n] = pos[j];
   oscale[n] = scale[j];
   operm[n] = perm[j];
+}
+
+// Pair-and-octet order of one full gather group (one thread per group):
+// targets of one cell are paired (consecutive in the sorted group) and a pair
+// goes to ONE thread as its two targets, which then read one h window (the
+// second target's loads are predicated off, window_dot2 `same`).  Octets
+// (quarter-warps: 8 consecutive threads) are filled first with 8 pairs of
+// pairwise distinct window residues mod 8 -- no bank conflict and no second
+// load in the whole octet -- then the remaining units (leftover pairs, and
+// single targets dealt alternately to the two target sets so both sets stay
+// residue-sorted) fill the other octets by the residue transpose of
+// k_octet_order.  Thread t takes records t (set 0) and t + T (set 1).
+__global__ void k_octet_pairs(const double* pos, const double* scale, const int* perm, int64_t M2,
+                              int64_t ngroups, double* opos, double* oscale, int* operm) {
+  constexpr int G = kGatherGroup, T = kGatherThreads, NOCT = T / 8;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ngroups) return;
+  const int64_t j0 = g * G;
+  if (j0 + G > M2) {  // partial group: copy
+    for (int64_t j = j0; j < M2; ++j) opos[j] = pos[j], oscale[j] = scale[j], operm[j] = perm[j];
+    return;
+  }
+  const double base = floor(pos[j0]);
+  // units: (set-0 index, set-1 index); a pair has equal cells
+  short ua[T], ub[T];
+  unsigned char ures[T], upair[T];
+  int nu = 0;
+  short singles[G];
+  int ns = 0;
+  for (int i = 0; i < G;) {
+    const double ci = floor(pos[j0 + i]);
+    if (i + 1 < G && floor(pos[j0 + i + 1]) == ci) {
+      ua[nu] = (short)i, ub[nu] = (short)(i + 1);
+      ures[nu] = (unsigned char)((int64_t)(ci - base) & 7), upair[nu] = 1;
+      ++nu;
+      i += 2;
+    } else {
+      singles[ns++] = (short)i;
+      ++i;
+    }
+  }
+  // singles by residue (stable), dealt alternately to set 0 and set 1
+  short sres[G];
+  for (int k = 0; k < ns; ++k) sres[k] = (short)((int64_t)(floor(pos[j0 + singles[k]]) - base) & 7);
+  for (int k = 1; k < ns; ++k) {  // insertion sort by residue (stable)
+    const short v = singles[k], r = sres[k];
+    int m = k - 1;
+    while (m >= 0 && sres[m] > r) { singles[m + 1] = singles[m], sres[m + 1] = sres[m]; --m; }
+    singles[m + 1] = v, sres[m + 1] = r;
+  }
+  for (int k = 0; k + 1 < ns; k += 2) {
+    ua[nu] = singles[k], ub[nu] = singles[k + 1];
+    ures[nu] = (unsigned char)sres[k], upair[nu] = 0;
+    ++nu;
+  }
+  // nu == T: pairs + singles / 2 = (G - ns) / 2 + ns / 2
+  short slot_of[T];   // unit placed at thread slot
+  bool used[T];
+  for (int k = 0; k < T; ++k) used[k] = false;
+  int oct = 0;
+  // pure pair octets: one pair of each residue
+  while (oct < NOCT) {
+    int pick[8];
+    bool ok = true;
+    for (int r = 0; r < 8 && ok; ++r) {
+      pick[r] = -1;
+      for (int k = 0; k < nu; ++k)
+        if (!used[k] && upair[k] && ures[k] == r) { pick[r] = k; break; }
+      ok = pick[r] >= 0;
+    }
+    if (!ok) break;
+    for (int r = 0; r < 8; ++r) slot_of[oct * 8 + r] = (short)pick[r], used[pick[r]] = true;
+    ++oct;
+  }
+  // the rest: residue-sorted, transposed over the remaining octets
+  short rest[T];
+  int nr = 0;
+  for (int r = 0; r < 8; ++r)
+    for (int k = 0; k < nu; ++k)
+      if (!used[k] && ures[k] == r) rest[nr++] = (short)k;
+  const int om = NOCT - oct;  // nr == 8 * om
+  for (int k = 0; k < nr; ++k) slot_of[(oct + k % om) * 8 + k / om] = rest[k];
+  for (int t = 0; t < T; ++t) {
+    const int a = ua[slot_of[t]], b = ub[slot_of[t]];
+    opos[j0 + t] = pos[j0 + a], oscale[j0 + t] = scale[j0 + a], operm[j0 + t] = perm[j0 + a];
+    opos[j0 + T + t] = pos[j0 + b], oscale[j0 + T + t] = scale[j0 + b],
+                  operm[j0 + T + t] = perm[j0 + b];
+  }
 }
 
 __global__ void k_gather_spans(const double* pos, int64_t n, int64_t nblk, int m2, int64_t s_lo,
@@ -668,7 +759,11 @@ void octet_order(NnfftPlanImpl& p, int64_t M2, cudaStream_t s) {
                             cudaMemcpyDeviceToDevice, s));
   }
   const int64_t ngroups = ceil_div(M2, (int64_t)kGatherGroup);
-  if (ngroups > 0)
+  if (ngroups > 0 && SFB_GATHER_PAIRS)
+    k_octet_pairs<<<(unsigned)ceil_div(ngroups, (int64_t)64), 64, 0, s>>>(
+        p.gp.pos.p, p.gp.scale.p, p.gp.perm.p, M2, ngroups, p.gp.opos.p, p.gp.oscale.p,
+        p.gp.operm.p);
+  else if (ngroups > 0)
     k_octet_order<<<(unsigned)ngroups, kGatherGroup, 0, s>>>(p.gp.pos.p, p.gp.scale.p, p.gp.perm.p,
                                                             M2, p.gp.opos.p, p.gp.oscale.p,
                                                             p.gp.operm.p);

@@ -207,7 +207,7 @@ __device__ __forceinline__ void window_accumulate2(const WinCoef& C, double d0, 
 template <int M>
 __device__ __forceinline__ void window_dot2(const WinCoef& C, double d0, double d1,
                                             const double2* h0, const double2* h1, double2& s0,
-                                            double2& s1) {
+                                            double2& s1, bool same = false) {
   constexpr int P = window_degree(M);
   constexpr int NE = P / 2 + 1;
   constexpr int NO = (P + 1) / 2;
@@ -225,7 +225,11 @@ __device__ __forceinline__ void window_dot2(const WinCoef& C, double d0, double 
     if (q == M - 1) {
       hi0 *= sh0, lo0 *= sl0, hi1 *= sh1, lo1 *= sl1;
     }
-    const double2 a0 = h0[ih], b0 = h0[il], a1 = h1[ih], b1 = h1[il];
+    // same: both targets read one window (h1 == h0) -- the second pair of
+    // loads is predicated off, so a quarter-warp of such threads costs no
+    // shared-memory wavefront for it
+    const double2 a0 = h0[ih], b0 = h0[il];
+    const double2 a1 = same ? a0 : h1[ih], b1 = same ? b0 : h1[il];
     s0.x = fma(a0.x, hi0, fma(b0.x, lo0, s0.x));
     s0.y = fma(a0.y, hi0, fma(b0.y, lo0, s0.y));
     s1.x = fma(a1.x, hi1, fma(b1.x, lo1, s1.x));
