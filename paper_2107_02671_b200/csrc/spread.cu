@@ -47,6 +47,9 @@ struct SpreadArgs {
 static_assert(kChunk == 4, "slot records assume 4 sources per chunk");
 static_assert(kBlockChunks == 32, "one chunk per lane");
 
+#ifndef SFB_SPREAD_F64B
+#define SFB_SPREAD_F64B 1  // f gather with the .L2::64B fill size
+#endif
 constexpr int kDescStages = 3;  // descriptor ring depth (blocks)
 constexpr int kFStages = 2;     // f ring depth (blocks)
 
@@ -91,7 +94,11 @@ __device__ __forceinline__ void issue_f(const SpreadArgs& a, W& S, bool live, in
       } else {
         const double2* fp =
             static_cast<const double2*>(a.f) + (s < cnt ? (int64_t)src[s] * a.batch + col : 0);
+#if SFB_SPREAD_F64B
+        cp_async16z_l2_64(&S.f[st_f][s][lane], fp, s < cnt ? 16 : 0);
+#else
         cp_async16z(&S.f[st_f][s][lane], fp, s < cnt ? 16 : 0);
+#endif
       }
     }
   }
