@@ -206,6 +206,32 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned pha
       : "memory");
 }
 
+// ---- L2 eviction-priority hints on plain loads / stores (createpolicy):
+// tables read once per pass stream through (evict_first), intermediates the
+// next kernel reads stay (evict_last)
+__device__ __forceinline__ unsigned long long l2_policy_first() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_last() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld_hint(const double2* p, unsigned long long pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(double2* p, double2 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+               "l"(pol)
+               : "memory");
+}
+
 // ---- cp.async (global -> shared without registers); src_bytes < size zero-fills
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);

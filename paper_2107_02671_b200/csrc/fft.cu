@@ -57,6 +57,36 @@ constexpr int kTwSplit = 4096;        // two-level W_L table split
 #ifndef SFB_FFT_ABL
 #define SFB_FFT_ABL 0  // timing ablations of k_colfwd_r1 (wrong results): 1 no loads, 2 no stores
 #endif
+#ifndef SFB_FFT_L2HINT
+#define SFB_FFT_L2HINT 1  // register passes: tables evict-first, intermediates evict-last
+#endif
+#if SFB_FFT_L2HINT
+#define FFT_LD_TABLE(p) ld_hint((p), l2_policy_first())
+#define FFT_LD_ONCE(p) ld_hint((p), l2_policy_first())
+#define FFT_ST_KEEP(p, v) st_hint((p), (v), l2_policy_last())
+#else
+#define FFT_LD_TABLE(p) __ldg(p)
+#define FFT_LD_ONCE(p) (*(p))
+#define FFT_ST_KEEP(p, v) (*(p) = (v))
+#endif
+#ifndef SFB_FFT_ROWHINT
+#define SFB_FFT_ROWHINT 2  // row pass hint bits: 1 row load, 2 B-hat load, 4 row store
+#endif
+#if SFB_FFT_L2HINT && (SFB_FFT_ROWHINT & 1)
+#define FFT_ROW_LD(p) FFT_LD_ONCE(p)
+#else
+#define FFT_ROW_LD(p) (*(p))
+#endif
+#if SFB_FFT_L2HINT && (SFB_FFT_ROWHINT & 2)
+#define FFT_ROW_TAB(p) FFT_LD_TABLE(p)
+#else
+#define FFT_ROW_TAB(p) __ldg(p)
+#endif
+#if SFB_FFT_L2HINT && (SFB_FFT_ROWHINT & 4)
+#define FFT_ROW_ST(p, v) FFT_ST_KEEP(p, v)
+#else
+#define FFT_ROW_ST(p, v) (*(p) = (v))
+#endif
 #ifndef SFB_FFT_CPL
 #define SFB_FFT_CPL 0  // register column passes: exchange layout padded every 8 slots
 #endif
@@ -793,7 +823,7 @@ __global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
       if (n1 < a.L1 && n < a.K) {
         double2 gv = __ldg(g + n);
         if (a.conj_in) gv.y = -gv.y;
-        f.x[k][r] = cmul(gv, __ldg(a.P + n));
+        f.x[k][r] = cmul(gv, FFT_LD_TABLE(a.P + n));
       }
     }
   }
@@ -834,7 +864,7 @@ __global__ void __launch_bounds__(T, MINB) k_colfwd_r1(FftArgs a) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int p = R * u + r;
-      Y[n1 + a.L1 * (int64_t)p] = cmul(f.x[k][r], wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(p)));
+      FFT_ST_KEEP(Y + n1 + a.L1 * (int64_t)p, cmul(f.x[k][r], wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(p))));
     }
   }
 #endif
@@ -1005,7 +1035,7 @@ __global__ void __launch_bounds__(T, MINB) k_rowmul_r1(FftArgs a) {
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
 #pragma unroll
-    for (int r = 0; r < R; ++r) f.x[k][r] = row[F::template pos<S0>(u, r)];
+    for (int r = 0; r < R; ++r) f.x[k][r] = FFT_ROW_LD(row + F::template pos<S0>(u, r));
   }
 #endif
   f.dif(sm, R == 16 ? a.st1x : a.st1, R == 16 ? a.tw1x : a.tw1);
@@ -1014,14 +1044,14 @@ __global__ void __launch_bounds__(T, MINB) k_rowmul_r1(FftArgs a) {
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
 #pragma unroll
-    for (int r = 0; r < R; ++r) f.x[k][r] = cconj(cmul(f.x[k][r], __ldg(Bh + R * u + r)));
+    for (int r = 0; r < R; ++r) f.x[k][r] = cconj(cmul(f.x[k][r], FFT_ROW_TAB(Bh + R * u + r)));
   }
   f.dit(sm, R == 16 ? a.st1x : a.st1, R == 16 ? a.tw1x : a.tw1);
 #pragma unroll
   for (int k = 0; k < F::BPT; ++k) {
     const int u = F::but(k);
 #pragma unroll
-    for (int r = 0; r < R; ++r) row[F::template pos<S0>(u, r)] = cconj(f.x[k][r]);
+    for (int r = 0; r < R; ++r) FFT_ROW_ST(row + F::template pos<S0>(u, r), cconj(f.x[k][r]));
   }
 }
 
@@ -1067,7 +1097,7 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_r1(FftArgs a) {
       const int p = R * u + r;
       f.x[k][r] = make_double2(0.0, 0.0);
       if (n1 < a.L1)
-        f.x[k][r] = cmul(cconj(Y[n1 + a.L1 * (int64_t)p]),
+        f.x[k][r] = cmul(cconj(FFT_LD_ONCE(Y + n1 + a.L1 * (int64_t)p)),
                          wbig(a.tw_lo, a.tw_hi, n1 * (int64_t)revr<N, R>(p)));
     }
   }
@@ -1108,7 +1138,7 @@ __global__ void __launch_bounds__(T, MINB) k_colinv_r1(FftArgs a) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int64_t kk = n1 + a.L1 * (int64_t)F::template pos<S0>(u, r);
-      if (kk < a.Kout) h[kk] = cmul(cconj(f.x[k][r]), __ldg(a.Q + kk));
+      if (kk < a.Kout) FFT_ST_KEEP(h + kk, cmul(cconj(f.x[k][r]), FFT_LD_TABLE(a.Q + kk)));
     }
   }
 #endif
