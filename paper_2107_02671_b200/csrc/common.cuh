@@ -249,6 +249,19 @@ __device__ __forceinline__ void cp_async16z_l2_64(void* smem, const void* gmem, 
   asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
                "r"(src_bytes));
 }
+// cp.async with an L2 cache-policy operand (createpolicy) and the 64-byte fill
+__device__ __forceinline__ void cp_async16z_pol(void* smem, const void* gmem, int src_bytes,
+                                                unsigned long long pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint.L2::64B [%0], [%1], 16, %2, %3;\n" ::"r"(sa),
+               "l"(gmem), "r"(src_bytes), "l"(pol));
+}
+__device__ __forceinline__ void cp_async16_pol(void* smem, const void* gmem,
+                                               unsigned long long pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa),
+               "l"(gmem), "l"(pol));
+}
 __device__ __forceinline__ void cp_async8z(void* smem, const void* gmem, int src_bytes) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),

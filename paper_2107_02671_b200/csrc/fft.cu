@@ -2356,6 +2356,7 @@ void run_fft(const NnfftPlanImpl& p, const double2* grid, double2* h, double2* w
     return;
   }
   if (reg_single(f)) {
+    grid_padded = grid_padded && batch == 1 && !col16(f) && fft_tma_enabled();
     if (grid_padded)  // zero the row padding the TMA path reads past K
       SF_CUDA(cudaMemsetAsync(const_cast<double2*>(grid) + p.g.K, 0,
                               sizeof(double2) * (size_t)(ceil_div(p.g.K, f.L1) * f.L1 - p.g.K), s));

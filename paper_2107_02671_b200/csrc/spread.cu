@@ -47,6 +47,9 @@ struct SpreadArgs {
 static_assert(kChunk == 4, "slot records assume 4 sources per chunk");
 static_assert(kBlockChunks == 32, "one chunk per lane");
 
+#ifndef SFB_SPREAD_HINT
+#define SFB_SPREAD_HINT 0  // L2 hint bits: 1 descriptors evict-first, 2 f evict-last, 4 f evict-first
+#endif
 #ifndef SFB_SPREAD_F64B
 #define SFB_SPREAD_F64B 1  // f gather with the .L2::64B fill size
 #endif
@@ -71,9 +74,16 @@ __device__ __forceinline__ void issue_desc(const SpreadArgs& a, W& S, int64_t b,
                                            int st, int lane) {
   if (b < b1) {
     const int64_t ci = b * kBlockChunks + lane;
+#if SFB_SPREAD_HINT & 1  // streaming descriptors: evict-first
+    const unsigned long long pol = l2_policy_first();
+    cp_async16_pol(&S.pos[st][0][lane], a.pos + ci * kChunk, pol);
+    cp_async16_pol(&S.pos[st][1][lane], a.pos + ci * kChunk + 2, pol);
+    cp_async16_pol(&S.perm[st][lane], a.perm + ci * kChunk, pol);
+#else
     cp_async16(&S.pos[st][0][lane], a.pos + ci * kChunk);
     cp_async16(&S.pos[st][1][lane], a.pos + ci * kChunk + 2);
     cp_async16(&S.perm[st][lane], a.perm + ci * kChunk);
+#endif
     cp_async4(&S.info[st][lane], a.info + ci);
   }
   cp_async_commit();
@@ -94,7 +104,11 @@ __device__ __forceinline__ void issue_f(const SpreadArgs& a, W& S, bool live, in
       } else {
         const double2* fp =
             static_cast<const double2*>(a.f) + (s < cnt ? (int64_t)src[s] * a.batch + col : 0);
-#if SFB_SPREAD_F64B
+#if SFB_SPREAD_HINT & 2  // f: evict-last (its 64-byte neighbours are other sources)
+        cp_async16z_pol(&S.f[st_f][s][lane], fp, s < cnt ? 16 : 0, l2_policy_last());
+#elif SFB_SPREAD_HINT & 4
+        cp_async16z_pol(&S.f[st_f][s][lane], fp, s < cnt ? 16 : 0, l2_policy_first());
+#elif SFB_SPREAD_F64B
         cp_async16z_l2_64(&S.f[st_f][s][lane], fp, s < cnt ? 16 : 0);
 #else
         cp_async16z(&S.f[st_f][s][lane], fp, s < cnt ? 16 : 0);
