@@ -110,3 +110,69 @@ def _coll_worker(rank, world, port, result_dir):
 def test_distributed_fft_collectives_gloo(tmp_path, world):
     mp.spawn(_coll_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     assert all((tmp_path / f"ok{r}.npy").exists() for r in range(world))
+
+
+def _native_worker(rank, world, port, result_dir):
+    """The collective layer of the default N > 1 path (sparse distributed FFT)
+    on CPU: TorchCollectives' native calls -- the exact reduce_scatter_tensor /
+    all_to_all_single / all_gather_into_tensor / uneven all_to_all_single
+    calls NCCL executes on the GPUs -- forced on (gloo runs them on CPU
+    tensors), against its CPU-staging fallback and against the data movement
+    they must perform."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2107_02671_b200.sharding import SparseRows, TorchCollectives, _all_to_all_v
+        res = {}
+        for native in (True, False):
+            c = TorchCollectives()
+            c.nccl = native  # the NCCL-path calls (CPU tensors over gloo) or the staging path
+            n = 6
+            send = torch.complex(torch.arange(world * n, dtype=torch.float64) + 1000 * rank,
+                                 -torch.arange(world * n, dtype=torch.float64))
+            # (clones: on CPU tensors the staging path's .cpu() aliases its input)
+            res[f"rs{native}"] = c.reduce_scatter(send.clone()).numpy()
+            res[f"a2a{native}"] = c.all_to_all(send.clone()).numpy()
+            res[f"ag{native}"] = c.all_gather(send[:n].clone()).numpy()
+            # uneven splits as the sparse exchange produces them: rank q sends
+            # (q + 1) * (p + 2) elements to rank p
+            ins = [(rank + 1) * (p + 2) for p in range(world)]
+            outs = [(q + 1) * (rank + 2) for q in range(world)]
+            sv = torch.complex(torch.arange(sum(ins), dtype=torch.float64) + 100 * rank,
+                               torch.full((sum(ins),), float(rank), dtype=torch.float64))
+            res[f"a2av{native}"] = _all_to_all_v(c, sv, ins, outs).numpy()
+        # SparseRows bookkeeping: what a rank sends to q is what q expects from it
+        sup = [[1000 * r + 7, 1000 * r + 900, 500 * r, 500 * r + 1300] for r in range(world)]
+        rows = SparseRows(sup, 64, 5, 3)
+        ok = all(rows.grid_send_splits(a)[b] == rows.grid_recv_splits(b)[a] and
+                 rows.h_send_splits(a)[b] == rows.h_recv_splits(b)[a]
+                 for a in range(world) for b in range(world))
+        res["splits_ok"] = np.array([ok])
+        np.savez(os.path.join(result_dir, f"coll{rank}.npz"), **res)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_collective_layer_native_calls(tmp_path, world):
+    mp.spawn(_native_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    d = [np.load(tmp_path / f"coll{r}.npz") for r in range(world)]
+    n = 6
+    sends = [np.arange(world * n) + 1000 * r - 1j * np.arange(world * n) for r in range(world)]
+    for r in range(world):
+        assert bool(d[r]["splits_ok"][0])
+        for native in (True, False):
+            np.testing.assert_array_equal(d[r][f"rs{native}"],
+                                          sum(s[r * n:(r + 1) * n] for s in sends))
+            np.testing.assert_array_equal(d[r][f"a2a{native}"],
+                                          np.concatenate([s[r * n:(r + 1) * n] for s in sends]))
+            np.testing.assert_array_equal(d[r][f"ag{native}"],
+                                          np.concatenate([s[:n] for s in sends]))
+            exp = []
+            for q in range(world):
+                ins = [(q + 1) * (p + 2) for p in range(world)]
+                off = sum(ins[:r])
+                sv = np.arange(sum(ins)) + 100 * q + 1j * q
+                exp.append(sv[off:off + ins[r]])
+            np.testing.assert_array_equal(d[r][f"a2av{native}"], np.concatenate(exp))
