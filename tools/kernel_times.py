@@ -33,12 +33,14 @@ if cfg.get("sinc"):
 else:
     n_star, vs = sf.rescale_frequencies(cfg["N"], v, 2.0, cfg["m"])
     plan = sf.nnfft_plan(n_star, vs, x, m1=cfg["m"], m2=cfg["m"], device=0)
-    d_f = torch.from_numpy(f).to(dev)
-    d_out = torch.empty(cfg["M2"], dtype=torch.complex128, device=dev)
+    d_f = torch.from_numpy(np.ascontiguousarray(f)).to(dev)
+    B = max(cfg["batch"], 1)
+    d_out = torch.empty((cfg["M2"],) + ((B,) if cfg["batch"] else ()), dtype=torch.complex128,
+                        device=dev)
 
     def step():
         _lib.check(_lib.lib.sincfft_nnfft_execute(plan.handle, d_f.data_ptr(), d_out.data_ptr(),
-                                                  1, _lib.PTR_DEVICE, s))
+                                                  B, _lib.PTR_DEVICE, s))
 for _ in range(5):
     step()
 torch.cuda.synchronize()
