@@ -343,10 +343,10 @@ __global__ void k_octet_order(const double* pos, const double* scale, const int*
 // second target's loads are predicated off, window_dot2 `same`).  Octets
 // (quarter-warps: 8 consecutive threads) are filled first with 8 pairs of
 // pairwise distinct window residues mod 8 -- no bank conflict and no second
-// load in the whole octet -- then the remaining units (leftover pairs, and
-// single targets dealt alternately to the two target sets so both sets stay
-// residue-sorted) fill the other octets by the residue transpose of
-// k_octet_order.  Thread t takes records t (set 0) and t + T (set 1).
+// load in the whole octet -- then lane l of every other octet takes a
+// leftover pair of residue l or two single targets of residue l (one per
+// target set), falling back to the fullest residue bucket.  Thread t takes
+// records t (set 0) and t + T (set 1).
 __global__ void k_octet_pairs(const double* pos, const double* scale, const int* perm, int64_t M2,
                               int64_t ngroups, double* opos, double* oscale, int* operm) {
   constexpr int G = kGatherGroup, T = kGatherThreads, NOCT = T / 8;
@@ -359,8 +359,8 @@ __global__ void k_octet_pairs(const double* pos, const double* scale, const int*
   }
   const double base = floor(pos[j0]);
   // units: (set-0 index, set-1 index); a pair has equal cells
-  short ua[T], ub[T];
-  unsigned char ures[T], upair[T];
+  short ua[2 * T], ub[2 * T];
+  unsigned char ures[2 * T], upair[2 * T];
   int nu = 0;
   short singles[G];
   int ns = 0;
@@ -376,21 +376,13 @@ __global__ void k_octet_pairs(const double* pos, const double* scale, const int*
       ++i;
     }
   }
-  // singles by residue (stable), dealt alternately to set 0 and set 1
-  short sres[G];
-  for (int k = 0; k < ns; ++k) sres[k] = (short)((int64_t)(floor(pos[j0 + singles[k]]) - base) & 7);
-  for (int k = 1; k < ns; ++k) {  // insertion sort by residue (stable)
-    const short v = singles[k], r = sres[k];
-    int m = k - 1;
-    while (m >= 0 && sres[m] > r) { singles[m + 1] = singles[m], sres[m + 1] = sres[m]; --m; }
-    singles[m + 1] = v, sres[m + 1] = r;
+  // residue buckets of the single targets (position order inside a bucket)
+  short sb_[8][G];
+  int sn[8] = {0, 0, 0, 0, 0, 0, 0, 0}, shead[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int k = 0; k < ns; ++k) {
+    const int r = (int)((int64_t)(floor(pos[j0 + singles[k]]) - base) & 7);
+    sb_[r][sn[r]++] = singles[k];
   }
-  for (int k = 0; k + 1 < ns; k += 2) {
-    ua[nu] = singles[k], ub[nu] = singles[k + 1];
-    ures[nu] = (unsigned char)sres[k], upair[nu] = 0;
-    ++nu;
-  }
-  // nu == T: pairs + singles / 2 = (G - ns) / 2 + ns / 2
   short slot_of[T];   // unit placed at thread slot
   bool used[T];
   for (int k = 0; k < T; ++k) used[k] = false;
@@ -409,14 +401,43 @@ __global__ void k_octet_pairs(const double* pos, const double* scale, const int*
     for (int r = 0; r < 8; ++r) slot_of[oct * 8 + r] = (short)pick[r], used[pick[r]] = true;
     ++oct;
   }
-  // the rest: residue-sorted, transposed over the remaining octets
-  short rest[T];
-  int nr = 0;
-  for (int r = 0; r < 8; ++r)
-    for (int k = 0; k < nu; ++k)
-      if (!used[k] && ures[k] == r) rest[nr++] = (short)k;
-  const int om = NOCT - oct;  // nr == 8 * om
-  for (int k = 0; k < nr; ++k) slot_of[(oct + k % om) * 8 + k / om] = rest[k];
+  // mixed octets: lane l prefers residue l in both target sets -- a leftover
+  // pair of residue l, else two singles of residue l -- and falls back to the
+  // fullest bucket, so a quarter-warp repeats a residue only when a bucket
+  // runs dry
+  auto take_single = [&](int r) -> int {
+    if (shead[r] >= sn[r]) {
+      int best = -1;
+      for (int q = 0; q < 8; ++q)
+        if (shead[q] < sn[q] && (best < 0 || sn[q] - shead[q] > sn[best] - shead[best])) best = q;
+      if (best < 0) return -1;
+      r = best;
+    }
+    return sb_[r][shead[r]++];
+  };
+  int nu2 = nu;
+  for (int t = oct * 8; t < T; ++t) {
+    const int l = t & 7;
+    int pk = -1;
+    for (int k = 0; k < nu && pk < 0; ++k)
+      if (!used[k] && upair[k] && ures[k] == l) pk = k;
+    int sa = -1, sbb = -1;
+    if (pk < 0) {
+      sa = take_single(l);
+      if (sa >= 0) sbb = take_single(l);
+    }
+    if (pk < 0 && (sa < 0 || sbb < 0)) {  // no singles left: any leftover pair
+      for (int k = 0; k < nu && pk < 0; ++k)
+        if (!used[k] && upair[k]) pk = k;
+    }
+    if (pk >= 0) {
+      used[pk] = true;
+      slot_of[t] = (short)pk;
+    } else {  // a new unit of two singles
+      ua[nu2] = (short)sa, ub[nu2] = (short)sbb;
+      slot_of[t] = (short)nu2++;
+    }
+  }
   for (int t = 0; t < T; ++t) {
     const int a = ua[slot_of[t]], b = ub[slot_of[t]];
     opos[j0 + t] = pos[j0 + a], oscale[j0 + t] = scale[j0 + a], operm[j0 + t] = perm[j0 + a];
