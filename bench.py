@@ -804,6 +804,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="3")
+    ap.add_argument("--m", type=int, default=None,
+                    help="window cut-off m1 = m2 (config 2 is BASELINE's sweep over "
+                         "m in {2, 4, 6, 8, 10}; default: the config's own m)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--e2e-streams", type=int, default=4,
                     help="host-buffer pipeline depth of the e2e leg (streams in flight)")
@@ -828,6 +831,9 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
+    if args.m is not None:
+        cfg = dict(cfg, m=args.m, desc=cfg["desc"].replace(f"m1=m2={cfg['m']}",
+                                                           f"m1=m2={args.m}"))
     world = int(os.environ.get("WORLD_SIZE", "0"))
     if args.impl != "reference":
         if args.gpus > 1 and world == 0:

@@ -87,6 +87,9 @@ constexpr int kTwSplit = 4096;        // two-level W_L table split
 #else
 #define FFT_ROW_ST(p, v) (*(p) = (v))
 #endif
+#ifndef SFB_DIRECT_PARMIN
+#define SFB_DIRECT_PARMIN 32
+#endif
 #ifndef SFB_FFT_CPL
 #define SFB_FFT_CPL 0  // register column passes: exchange layout padded every 8 slots
 #endif
@@ -1817,6 +1820,13 @@ int64_t primitive_root(int64_t P) {
   return 0;
 }
 
+static double direct_par_min() {
+  static const double v = [] {
+    const char* e = getenv("SFB_DIRECT_PARMIN");
+    return e ? atof(e) : (double)SFB_DIRECT_PARMIN;
+  }();
+  return v;
+}
 // pick N2 = A * P for the direct path; false if no split fits.  best_out is
 // the model cost per point (stage costs + ~1 unit per byte of HBM traffic)
 bool choose_direct(int64_t N2, DirectFft& d, double* best_out = nullptr) {
@@ -1834,10 +1844,14 @@ bool choose_direct(int64_t N2, DirectFft& d, double* best_out = nullptr) {
     int C = 8;
     while (C > 1 && C * A > kDirectSmem) C >>= 1;
     if (C < 2) continue;
+    // these sizes are launch/latency bound: a split with few step-2 rows (A)
+    // or few step-1 CTAs (P / C) leaves most SMs idle (N2 = 16464 split as
+    // 3 x 5488 took 43 us, twice its neighbours)
+    const double par = std::min((double)A, (double)P / C);
     const double cst = (stage_cost(A) + (ps ? stage_cost(P)
                                           : 2.0 * stage_cost(LP) * (double)LP / (double)P) +
                         48.0) *
-                       (C < 4 ? 1.15 : 1.0);
+                       (C < 4 ? 1.15 : 1.0) * (par < direct_par_min() ? direct_par_min() / par : 1.0);
     if (cst < best) {
       best = cst, found = true;
       d.A = A, d.P = P, d.LP = LP, d.p_smooth = ps, d.C = C, d.rader = rader;
@@ -2035,7 +2049,9 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
       gbest = std::min(gbest, (double)(L1 * L2) / (double)g.N2 *
                                   (2.0 * stage_cost(L1) + 2.0 * stage_cost(L2) + 144.0));
     }
-    use_direct = g.N2 <= 65536 || dcost < gbest;
+    // (a direct split left with little parallelism competes on cost)
+    const bool par_ok = std::min((double)f.d.A, (double)f.d.P / f.d.C) >= direct_par_min() / 2;
+    use_direct = (g.N2 <= 65536 && par_ok) || dcost < gbest;
   }
   if (use_direct) {
     f.direct = true;
