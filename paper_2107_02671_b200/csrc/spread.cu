@@ -446,6 +446,9 @@ constexpr int kDenseLanes = SFB_DENSE_LANES;  // lanes per unit
 #ifndef SFB_DENSE_G
 #define SFB_DENSE_G 2
 #endif
+#ifndef SFB_DENSE_FAST_SQRT
+#define SFB_DENSE_FAST_SQRT 1  // edge-tap square roots from the rsqrt seed + one step (window.cuh)
+#endif
 
 template <int M, bool REAL>
 #ifndef SFB_DENSE_MINB
@@ -512,7 +515,8 @@ __global__ void __launch_bounds__(256, SFB_DENSE_MINB) k_spread_dense(DenseArgs 
         const double pos = pv[i], fv = fr[i];
         const double d = pos - floor(pos);
         const double u = 2.0 * d - 1.0;
-        const double fb = fv * sqrt(d), fc = fv * sqrt(1.0 - d);
+        const double fb = fv * edge_sqrt<M, SFB_DENSE_FAST_SQRT != 0>(d),
+                     fc = fv * edge_sqrt<M, SFB_DENSE_FAST_SQRT != 0>(1.0 - d);
         double pw = 1.0;
 #pragma unroll
         for (int j = 0; j <= P; ++j) {

@@ -87,6 +87,27 @@ __host__ __device__ __forceinline__ double poly(const double* c, const VPow& w) 
 #endif
 }
 
+// sqrt(d), d in [0, 1], for the two edge taps of the moment spread.  For m >= 4
+// the edge taps are small (|g| <= sinh(beta sqrt(2/m)) / sinh(beta) < 7e-3 at
+// m = 4, < 7e-9 at m = 8), so the square root needs far less than full
+// precision: the hardware reciprocal-square-root seed (MUFU.RSQ64H, relative
+// error 2^-22) and ONE Goldschmidt step (1.5 eps^2 ~ 9e-14 relative, < 6e-16
+// absolute on the tap) instead of the IEEE routine's seed + 2 steps + fix-up +
+// slow-path branch.  d = 0 gives exactly 0 (the clamped seed is finite).
+// Measured and NOT used in the per-node window passes below: freed of the
+// IEEE routine's slow-path call, ptxas interleaves many more tap pairs there
+// and spills (config-3 spread 385 -> 650 us, gather 256 -> 263 us).
+template <int M, bool FAST>
+__device__ __forceinline__ double edge_sqrt(double d) {
+  if constexpr (M >= 4 && FAST) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(fmax(d, 1e-300)));
+    const double g = d * y, h = 0.5 * y;
+    return fma(g, fma(-g, h, 0.5), g);
+  }
+  return sqrt(d);
+}
+
 // All 2M tap values w[i] = g_{i+1-M}(d) for one node.  Host and device use
 // the same instruction sequence (host validation emulates the kernel).
 template <int M>

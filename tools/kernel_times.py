@@ -22,6 +22,14 @@ cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "5"]
 dev = torch.device("cuda", 0)
 s = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 v, x, f = bench.make_inputs(cfg)
+# ablation: KT_SORT=v / x / vx presents the sources / targets already sorted by
+# position, so the spread's f gather / the gather's output scatter are sequential
+srt = os.environ.get("KT_SORT", "")
+if "v" in srt:
+    o = np.argsort(v, kind="stable")
+    v, f = v[o], f[o]
+if "x" in srt:
+    x = np.sort(x)
 if cfg.get("sinc"):
     plan = sf.sinc_plan(cfg["N"], v, x, m1=cfg["m"], m2=cfg["m"], device=0)
     d_c = torch.from_numpy(np.ascontiguousarray(f.real)).to(dev)
