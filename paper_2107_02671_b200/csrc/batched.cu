@@ -20,6 +20,8 @@
 // stage still runs per column, with tiled transposes around it.
 #include "nnfft_impl.cuh"
 
+#include <atomic>
+
 namespace sfb {
 
 constexpr int kTileB = 128;   // cells per spread CTA
@@ -135,6 +137,222 @@ __global__ void __launch_bounds__(kThreadsB, SFB_SPREADB_MINB) k_spread_b(Spread
   while (ccur < cend - 1) spread_flush<M>(a, r, ccur, cell0, cend, col, colok);
 #pragma unroll
   for (int i = 0; i < 2 * M; ++i) spread_flush<M>(a, r, ccur, cell0, cend, col, colok);
+}
+
+// ----------------------------------------------- warp-specialised spread
+// k_spread_bw: the same tile / column decomposition as k_spread_b, rebuilt
+// around the TMA engine and static register slots.
+//   * one PRODUCER warp per CTA: 32 sources at a time, every lane evaluates
+//     one source's window (the next 32 positions / permutation entries are
+//     already in flight); then, stage by stage (kWsSrc sources), it writes
+//     taps and cells to shared memory and issues one bulk copy (cp.async.bulk,
+//     2 KiB = 128 columns) per source row of F into a kWsStages-deep ring,
+//     completing on the stage's `full` mbarrier -- no registers hold loads in
+//     flight;
+//   * four CONSUMER warps (lane = column): the 2m grid points of the current
+//     cell live in 2m STATIC register slots, slot(point) = point mod 2m.  The
+//     cell loop is unrolled over one period of 2m cells, so every tap
+//     addresses its slot at compile time (k_spread_b's shifting window was
+//     compiled to ~50 register moves per source: IMAD.MOV 42 % of its
+//     instructions); the sources of a cell are an inner loop over the ring.
+//     When a cell is finished its lowest point is final and is stored.
+// Stage release: each consumer warp arrives on the stage's `empty` mbarrier.
+// Measured (config 4, 1.57 ms for k_spread_b): 1.13 ms with 3 stages of 8
+// rows, 1.27 ms with 4, 1.51 ms with 6 (2 CTAs per SM); windows evaluated by
+// the consumer warps instead (a free-running copy producer): 1.54-1.71 ms.
+#ifndef SFB_SPREADB_SRC
+#define SFB_SPREADB_SRC 8
+#endif
+constexpr int kWsSrc = SFB_SPREADB_SRC;  // source rows per stage (2 KiB each)
+#ifndef SFB_SPREADB_STAGES
+#define SFB_SPREADB_STAGES 3
+#endif
+#ifndef SFB_SPREADBW_ABL
+#define SFB_SPREADBW_ABL 0  // timing ablations (wrong results): 1 no tap FMAs, 2 no bulk copies
+#endif
+constexpr int kWsStages = SFB_SPREADB_STAGES;
+constexpr int kWsConsumers = kThreadsB / 32;
+static_assert(32 % kWsSrc == 0, "a producer batch is a whole number of stages");
+
+template <int M>
+struct __align__(128) SpreadBwSmem {
+  double2 f[kWsStages][kWsSrc][kThreadsB];
+  double w[kWsStages][kWsSrc][2 * M];
+  int cell[kWsStages][kWsSrc];
+  unsigned long long full[kWsStages], empty[kWsStages];
+};
+
+// resident CTAs per SM: the 4 m accumulator registers leave room for 3 CTAs up to m = 6
+#ifndef SFB_SPREADBW_MINB
+#define SFB_SPREADBW_MINB(M) ((M) <= 6 ? 3 : 2)
+#endif
+template <int M>
+__global__ void __launch_bounds__(kThreadsB + 32, SFB_SPREADBW_MINB(M))
+    k_spread_bw(SpreadBArgs a, WinCoef C) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto& S = *reinterpret_cast<SpreadBwSmem<M>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int col0 = blockIdx.y * kThreadsB;
+  const int ncol = min(kThreadsB, a.B - col0);
+  const int cell0 = (int)((int64_t)blockIdx.x * kTileB);
+  const int cend = (int)min((int64_t)cell0 + kTileB, a.K);
+  const int s0 = a.tile[blockIdx.x], s1 = a.tile[blockIdx.x + 1];
+  const int nst = (s1 - s0 + kWsSrc - 1) / kWsSrc;
+  if (tid == 0) {
+    for (int i = 0; i < kWsStages; ++i) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], kWsConsumers);
+    }
+  }
+  __syncthreads();
+  if (warp == kWsConsumers) {
+    // ------------------------------------------------------------ producer
+    const int64_t halfK = a.K / 2;
+    const int nsrc = s1 - s0;
+    double pos_n = 0.5;
+    int src_n = 0;
+    if (lane < nsrc) {
+      pos_n = __ldg(a.pos + s0 + lane);
+      src_n = __ldg(a.perm + s0 + lane);
+    }
+    for (int jb = 0; jb < nst; jb += 32 / kWsSrc) {
+      const double pos = pos_n;
+      const int src = src_n;
+      const int sb = s0 + jb * kWsSrc;  // first source of this batch
+      if (sb + 32 + lane < s1) {
+        pos_n = __ldg(a.pos + sb + 32 + lane);
+        src_n = __ldg(a.perm + sb + 32 + lane);
+      }
+      const double fl = floor(pos);
+      double w[2 * M];
+      window_taps<M>(C, pos - fl, w);
+      const int cl = (int)((int64_t)fl + halfK);
+#pragma unroll
+      for (int g = 0; g < 32 / kWsSrc; ++g) {
+        const int j = jb + g;
+        if (j < nst) {  // warp-uniform
+          const int st = j % kWsStages;
+          if (j >= kWsStages) mbar_wait(&S.empty[st], (unsigned)((j / kWsStages - 1) & 1));
+          const int n = min(kWsSrc, s1 - (s0 + j * kWsSrc));
+          const int l = lane - g * kWsSrc;
+          const bool mine = l >= 0 && l < n;
+          if (mine) {
+#pragma unroll
+            for (int i = 0; i < 2 * M; ++i) S.w[st][l][i] = w[i];
+            S.cell[st][l] = cl;
+          }
+          __syncwarp();
+#if SFB_SPREADBW_ABL & 2
+          if (lane == 0) mbar_arrive(&S.full[st]);
+#else
+          if (lane == 0) mbar_expect_tx(&S.full[st], (unsigned)(n * ncol * (int)sizeof(double2)));
+          __syncwarp();
+          if (mine)
+            bulk_g2s_tx(&S.f[st][l][0], a.f + (int64_t)src * a.B + col0,
+                        (unsigned)(ncol * (int)sizeof(double2)), &S.full[st]);
+#endif
+        }
+      }
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  const bool colok = tid < ncol;
+  double2 r[2 * M];
+#pragma unroll
+  for (int i = 0; i < 2 * M; ++i) r[i] = make_double2(0.0, 0.0);
+  // Position in the source stream: source i of the tile, row k = i % kWsSrc
+  // of ring slot st (running shared-memory addresses fp / wp / cp, so the
+  // inner loop has no index arithmetic); cs = cell of the current, not yet
+  // consumed source (INT_MAX when the tile is exhausted).
+  const int nsrc = s1 - s0;
+  int i = 0, st = 0, cs = 0x7fffffff;
+  unsigned par = 0;  // phase parity of slot st's `full` barrier
+  const unsigned f0 = smem_u32(&S.f[0][0][tid]), w0 = smem_u32(&S.w[0][0][0]),
+                 c0 = smem_u32(&S.cell[0][0]);
+  unsigned fp = f0, wp = w0, cp = c0;
+  constexpr unsigned kFRow = sizeof(double2) * kThreadsB, kWRow = sizeof(double) * 2 * M;
+  auto lds_i = [](unsigned addr) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+  };
+  auto lds_d2 = [](unsigned addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+  };
+  if (nsrc > 0) {
+    mbar_wait(&S.full[0], 0u);
+    cs = lds_i(cp);
+  }
+  auto next = [&]() {
+    ++i;
+    fp += kFRow, wp += kWRow, cp += 4;
+    if ((i % kWsSrc) != 0 && i < nsrc) {
+      cs = lds_i(cp);
+      return;
+    }
+    __syncwarp();  // every lane has read this stage
+    if (lane == 0) mbar_arrive(&S.empty[st]);
+    if (i < nsrc) {
+      if (++st == kWsStages) {
+        st = 0, par ^= 1u;
+        fp = f0, wp = w0, cp = c0;
+      }
+      mbar_wait(&S.full[st], par);
+      cs = lds_i(cp);
+    } else {
+      cs = 0x7fffffff;
+    }
+  };
+  // cells cell0 .. cend-1, then 2M-1 source-free steps that retire the
+  // points still in the slots.  Step ci retires point cell0 + ci + 1 - M:
+  // inside the grid for ci in [ci_lo, ci_hi), interior to this tile (plain
+  // store) for ci in [2M-1, ncell), shared with a neighbour tile otherwise.
+  const int ncell = cend - cell0;
+  const int total = ncell + 2 * M - 1;
+  const int ci_lo = max(0, M - 1 - cell0);
+  const int ci_hi = (int)min((int64_t)total, a.K - cell0 - 1 + M);
+  double2* gp = a.grid + ((int64_t)cell0 + 1 - M) * a.B + (col0 + tid);
+  for (int base = 0; base < total; base += 2 * M) {
+#pragma unroll
+    for (int p = 0; p < 2 * M; ++p) {
+      const int ci = base + p;
+      if (ci < total) {  // warp-uniform
+        const int c = cell0 + ci;
+        while (cs == c) {
+#if !(SFB_SPREADBW_ABL & 1)
+          const double2 fv = lds_d2(fp);
+#pragma unroll
+          for (int t = 0; t < M; ++t) {
+            const double2 ww = lds_d2(wp + 16 * t);  // taps 2t, 2t+1 (broadcast)
+            double2& ra = r[(2 * t + p) % (2 * M)];
+            double2& rb = r[(2 * t + 1 + p) % (2 * M)];
+            ra.x = fma(fv.x, ww.x, ra.x);
+            ra.y = fma(fv.y, ww.x, ra.y);
+            rb.x = fma(fv.x, ww.y, rb.x);
+            rb.y = fma(fv.y, ww.y, rb.y);
+          }
+#endif
+          next();
+        }
+        // point cell0 + ci + 1 - M (slot p) is final
+        if (colok && ci >= ci_lo && ci < ci_hi) {
+          if (ci >= 2 * M - 1 && ci < ncell) {
+            *gp = r[p];  // interior: only this tile touches it
+          } else if (r[p].x != 0.0 || r[p].y != 0.0) {
+            atomicAdd(&gp->x, r[p].x);
+            atomicAdd(&gp->y, r[p].y);
+          }
+        }
+        gp += a.B;
+        r[p] = make_double2(0.0, 0.0);
+      }
+    }
+  }
 }
 
 // zero the grid rows shared by two tiles (touched with atomics)
@@ -265,6 +483,15 @@ static void transpose(const double2* in, double2* out, int64_t R, int64_t Cc, cu
 }
 
 // --------------------------------------------------------------- drivers
+// SFB_SPREADB_WS=0 selects the round-1 kernel (k_spread_b)
+static bool spread_b_ws() {
+  static const bool v = [] {
+    const char* e = getenv("SFB_SPREADB_WS");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 template <int M>
 static void spread_b_m(const NnfftPlanImpl& p, const double2* f, double2* grid, int B,
                        cudaStream_t s) {
@@ -272,6 +499,20 @@ static void spread_b_m(const NnfftPlanImpl& p, const double2* f, double2* grid, 
   k_zero_halo<<<(unsigned)(ntile + 1), dim3(32, 8), 0, s>>>(grid, p.g.K, B, M, ntile);
   SF_LAUNCH_CHECK();
   SpreadBArgs a{p.sp.bpos.p, p.sp.bperm.p, p.sp.btile.p, f, grid, p.g.K, B};
+  if (spread_b_ws()) {
+    const size_t smem = sizeof(SpreadBwSmem<M>);
+    static std::atomic<unsigned long long> attr_set{0};  // per template instance, per device
+    const unsigned long long bit = 1ull << (p.device & 63);
+    if (!(attr_set.load() & bit)) {
+      SF_CUDA(cudaFuncSetAttribute(k_spread_bw<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      attr_set.fetch_or(bit);
+    }
+    k_spread_bw<M><<<dim3((unsigned)ntile, (unsigned)ceil_div(B, kThreadsB)), kThreadsB + 32, smem,
+                     s>>>(a, p.c1);
+    SF_LAUNCH_CHECK();
+    return;
+  }
   const int threads = (int)std::min<int64_t>(kThreadsB, ceil_div(B, 32) * 32);
   const size_t smem = sizeof(double) * (2 * M + 1) * 32 * (threads / 32);
   k_spread_b<M><<<dim3((unsigned)ntile, (unsigned)ceil_div(B, threads)), threads, smem, s>>>(a,
