@@ -366,6 +366,12 @@ __global__ void k_zero_halo(double2* grid, int64_t K, int B, int m, int64_t ntil
 }
 
 // ------------------------------------------------------------------ gather
+// (A warp-specialised form in the shape of k_spread_bw -- h rows streamed by
+// bulk copies into an mbarrier ring, window tables from a second producer
+// warp, 2m static row slots in the consumers -- was measured at config 4:
+// 1.61-2.34 ms against 1.10 ms for this kernel, whatever the ring depth, CTAs
+// per SM (1-3) or columns per thread (1-2): with one output row per target
+// the consumer's per-target chain, not the h traffic, is what binds.  Dropped.)
 struct GatherBArgs {
   const double* pos;   // sorted target positions fl(N2 xs)
   const int* perm;

@@ -12,6 +12,8 @@
 
 #include "nnfft_impl.cuh"
 
+#include <cstdio>
+
 #ifndef SFB_SPREAD_CTAS
 #define SFB_SPREAD_CTAS 2  // persistent spread CTAs per SM (matches SFB_SPREAD_MINB)
 #endif
@@ -220,7 +222,10 @@ __global__ void k_block_emit(const int* nb, const int* boff, int64_t ntile, int*
 // (spread.cu): window pairs (4 units each for the lane that needs the most)
 // plus accumulator rounds (1 unit each; a single-cell block is one butterfly).
 // One warp per block.
-__global__ void k_block_cost(const int* info, int64_t nblk, long long* cost) {
+struct CostW {
+  int pair, round, base, same;
+};
+__global__ void k_block_cost(const int* info, int64_t nblk, long long* cost, CostW cw) {
   const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (b >= nblk) return;
@@ -230,8 +235,8 @@ __global__ void k_block_cost(const int* info, int64_t nblk, long long* cost) {
   int same = 0;
   __match_all_sync(0xffffffffu, cnt > 0 ? lc : -1 - lane, &same);
   const unsigned peers = __match_any_sync(0xffffffffu, cnt > 0 ? lc : -1 - lane);
-  const int rounds = same ? 2 : __reduce_max_sync(0xffffffffu, __popc(peers));
-  if (lane == 0) cost[b] = 4 * pairs + rounds;
+  const int rounds = same ? cw.same : __reduce_max_sync(0xffffffffu, __popc(peers));
+  if (lane == 0) cost[b] = cw.pair * pairs + cw.round * rounds + cw.base;
 }
 
 // first block of warp w: the first b with prefix cost[0..b] > w * total / W
@@ -675,7 +680,11 @@ void build_sources(NnfftPlanImpl& p, const double* v, int64_t M1, double N1, int
       p.sp.wstart.alloc(W + 1);
       if (nblk > 0) {
         Scratch cost(sizeof(long long) * nblk, s), incl(sizeof(long long) * nblk, s);
-        k_block_cost<<<blocks(nblk * 32), 256, 0, s>>>(p.sp.info.p, nblk, cost.as<long long>());
+        CostW cw{4, 1, 0, 2};  // tuning: SFB_SPREAD_COST="pair,round,base,same"
+        if (const char* e = getenv("SFB_SPREAD_COST"))
+          sscanf(e, "%d,%d,%d,%d", &cw.pair, &cw.round, &cw.base, &cw.same);
+        k_block_cost<<<blocks(nblk * 32), 256, 0, s>>>(p.sp.info.p, nblk, cost.as<long long>(),
+                                                       cw);
         SF_LAUNCH_CHECK();
         size_t tb3 = 0;
         SF_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb3, cost.as<long long>(),
