@@ -230,8 +230,10 @@ SINCFFT_API int sincfft_nnfft_dist_colinv_peer(sincfft_nnfft_plan plan, int32_t 
 
 /* Observability: one execute with DEVICE pointers and CUDA events recorded
  * on `stream` between the stages; returns after synchronizing the stream
- * with stage_ms[0..3] = spread (incl. grid zeroing), FFT (deconvolution +
- * pruned Bluestein), gather, whole call, in milliseconds. */
+ * with stage_ms[0..3] = spread kernel (single column: the grid memset runs
+ * before the first event; batched: the halo-row zeroing is included), FFT
+ * (deconvolution + pruned Bluestein), gather, whole call (grid zeroing
+ * included), in milliseconds. */
 SINCFFT_API int sincfft_nnfft_execute_profiled(sincfft_nnfft_plan plan, const double *f,
                                                double *out, int64_t batch, void *stream,
                                                double *stage_ms);

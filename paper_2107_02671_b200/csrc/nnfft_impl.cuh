@@ -279,6 +279,9 @@ void run_fft_point_major(const NnfftPlanImpl& p, const double2* grid, double2* h
 // f: (M1, batch) row-major; grid[batch][K] is zeroed and accumulated.
 void run_spread(const NnfftPlanImpl& p, const double2* f, double2* grid, int batch,
                 cudaStream_t stream);
+void run_spread_zero(const NnfftPlanImpl& p, double2* grid, int batch, cudaStream_t s);
+void run_spread_kernel(const NnfftPlanImpl& p, const double2* f, double2* grid, int batch,
+                       cudaStream_t s);
 // real-valued coefficients (fast sinc input), batch 1
 void run_spread_real(const NnfftPlanImpl& p, const double* f, double2* grid, cudaStream_t stream);
 // out: (M2, batch) row-major, original target order.

@@ -621,8 +621,8 @@ static void launch_spread_m(const NnfftPlanImpl& p, const void* f, double2* grid
 
 template <bool REAL>
 static void launch_spread(const NnfftPlanImpl& p, const void* f, double2* grid, int batch,
-                          cudaStream_t s) {
-  SF_CUDA(cudaMemsetAsync(grid, 0, sizeof(double2) * (size_t)p.g.K * batch, s));
+                          cudaStream_t s, bool zero = true) {
+  if (zero) SF_CUDA(cudaMemsetAsync(grid, 0, sizeof(double2) * (size_t)p.g.K * batch, s));
   switch (p.g.m1) {
 #define SF_CASE(MM) \
   case MM:          \
@@ -637,6 +637,16 @@ static void launch_spread(const NnfftPlanImpl& p, const void* f, double2* grid, 
 void run_spread(const NnfftPlanImpl& p, const double2* f, double2* grid, int batch,
                 cudaStream_t s) {
   launch_spread<false>(p, f, grid, batch, s);
+}
+
+// the two halves of run_spread, for per-kernel timing (capi.cu: the profiled
+// execute records its first event between them)
+void run_spread_zero(const NnfftPlanImpl& p, double2* grid, int batch, cudaStream_t s) {
+  SF_CUDA(cudaMemsetAsync(grid, 0, sizeof(double2) * (size_t)p.g.K * batch, s));
+}
+void run_spread_kernel(const NnfftPlanImpl& p, const double2* f, double2* grid, int batch,
+                       cudaStream_t s) {
+  launch_spread<false>(p, f, grid, batch, s, false);
 }
 
 void run_spread_real(const NnfftPlanImpl& p, const double* f, double2* grid, cudaStream_t s) {

@@ -52,7 +52,7 @@ def main():
     data[f"config{cfg}"] = {k: int(v) for k, v in per.items()}
     data["source"] = ("ncu --set full --clock-control none per kernel (dram__bytes_read.sum + "
                       "dram__bytes_write.sum per launch; fft = sum of its passes); reports "
-                      "summarised in profiles/r01g_ncu_summary.txt")
+                      "summarised in profiles/r02/r02w_ncu_summary_config*.txt")
     with open(path, "w") as fh:
         json.dump(data, fh, indent=1)
     print(json.dumps(data[f"config{cfg}"]))

@@ -57,7 +57,7 @@ def fp64_json(paths, out):
         d = {}
         for (_, k), m in per.items():
             name = re.sub(r"^(void )?(sfb::)?", "", k.split("(")[0]).split("<")[0]
-            kind = ("spread" if name in ("k_spread", "k_spread_b", "k_spread_dense") else
+            kind = ("spread" if name in ("k_spread", "k_spread_b", "k_spread_bw", "k_spread_dense") else
                     "gather" if name in ("k_gather", "k_gather2", "k_gather4", "k_gather_b")
                     else None)
             if kind is None or kind in d:
