@@ -255,7 +255,8 @@ def test_config5_full_size_vs_oracle():
 
 
 @pytest.mark.parametrize("B,m,clustered", [(16, 6, False), (40, 3, True), (64, 8, True),
-                                           (300, 5, False)])
+                                           (300, 5, False), (130, 10, True), (17, 16, False),
+                                           (256, 2, True), (129, 13, False)])
 def test_column_vectorised_batch_path(B, m, clustered):
     """B >= 16 columns run the column-vectorised kernels (csrc/batched.cu);
     every column must match the oracle applied to that column."""
@@ -268,6 +269,20 @@ def test_column_vectorised_batch_path(B, m, clustered):
         assert relerr(out[:, b], O.trafo(tab, f[:, b]), f[:, b]) <= TOL, b
     one = sf.nnfft_trafo(plan, np.ascontiguousarray(f[:, 5]))
     assert relerr(out[:, 5], one, f[:, 5]) <= 1e-14
+
+
+@pytest.mark.parametrize("M1,M2,m", [(3, 40, 6), (9, 7, 4), (33, 300, 8), (700, 5, 12)])
+def test_batched_few_nodes(M1, M2, m):
+    """The warp-specialised batched spread (k_spread_bw) with almost every
+    tile empty, fewer sources than one ring stage, and partial last stages."""
+    B = 48
+    v, x, f = nodes_and_coeffs(900 + M1, M1, M2, batch=B)
+    N, vs = sf.rescale_frequencies(512, v, 2.0, m)
+    plan = sf.nnfft_plan(N, vs, x, m1=m, m2=m)
+    out = sf.nnfft_trafo(plan, f)
+    tab = O.plan(N, vs, x, m1=m, m2=m)
+    for b in (0, 31, 32, B - 1):
+        assert relerr(out[:, b], O.trafo(tab, f[:, b]), f[:, b]) <= TOL, b
 
 
 def test_pipelined_host_async_two_streams():
