@@ -708,6 +708,26 @@ def run_b200(args, cfg):
             fp64_peak, fp64_note = float(json.load(fh)["fp64_dfma_tflops"]), \
                 "measured: tools/fp64_peak.cu (DFMA microbenchmark on this pool's B200)"
 
+    # the same three figures for every stage (the north star asks for each of
+    # spread / FFT / interpolate against the HBM roofline): algorithmic bytes
+    # over the live stage time, the committed ncu DRAM bytes and FP64 counts
+    traffic_all = {}
+    if world == 1 and os.path.exists(tf):
+        with open(tf) as fh:
+            traffic_all = json.load(fh).get(f"config{args.config}", {})
+    stages_roof = {}
+    for i, n in enumerate(names):
+        t_s = stage[i] * 1e-3
+        if t_s <= 0:
+            continue
+        stages_roof[n] = {"launch_ms": float(stage[i]), "alg_bytes_per_launch": alg[n],
+                          "achieved": alg[n] / t_s / 1e9, "frac": alg[n] / t_s / 1e9 / peak,
+                          "traffic": traffic_all.get(n),
+                          "dram_frac": (traffic_all[n] / t_s / 1e9 / peak
+                                        if traffic_all.get(n) else None),
+                          "fp64_frac": (None if flops.get(n) is None else
+                                        flops[n] / t_s / 1e12 / fp64_peak)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample_rate(cfg)
@@ -755,6 +775,7 @@ def run_b200(args, cfg):
                              "counts_from": fp64_node[dom][3],
                              "peak_note": fp64_note}},
             "stage_ms": {n: float(stage[i]) for i, n in enumerate(names)},
+            "roofline_stages": stages_roof,
             "plan_ms": plan_ms,
             "e2e": {"value": e2e_val, "unit": "nodes/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
