@@ -66,7 +66,7 @@ __device__ __forceinline__ void spread_flush(const SpreadBArgs& a, double2* r, i
 #endif
 template <int M>
 __global__ void __launch_bounds__(kThreadsB, SFB_SPREADB_MINB) k_spread_b(SpreadBArgs a, WinCoef C) {
-  extern __shared__ double wsm[];
+  extern __shared__ __align__(16) double wsm[];
   constexpr int WS = 2 * M + 1;  // padded row
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -385,8 +385,8 @@ struct GatherBArgs {
 
 template <int M>
 __global__ void __launch_bounds__(kThreadsB, 4) k_gather_b(GatherBArgs a, WinCoef C) {
-  extern __shared__ double wsm[];
-  constexpr int WS = 2 * M + 1;
+  extern __shared__ __align__(16) double wsm[];
+  constexpr int WS = 2 * M + 2;  // even: a row is 16-byte aligned, taps read in pairs
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   double* wl = wsm + warp * 32 * WS;
@@ -449,15 +449,18 @@ __global__ void __launch_bounds__(kThreadsB, 4) k_gather_b(GatherBArgs a, WinCoe
       for (int s = s0; s < s1; ++s) {
       const int d = __shfl_sync(0xffffffffu, dst, s);
       const double scs = __shfl_sync(0xffffffffu, sc, s);
-      const double* wr = wl + s * WS;
-      double2 acc = make_double2(0.0, 0.0);
+      const double2* wr = reinterpret_cast<const double2*>(wl + s * WS);
+      double2 acc = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int i = 0; i < 2 * M; ++i) {
-        const double wi = wr[i];
-        acc.x = fma(hr[i].x, wi, acc.x);
-        acc.y = fma(hr[i].y, wi, acc.y);
+      for (int i = 0; i < M; ++i) {
+        const double2 ww = wr[i];  // taps 2i, 2i+1 (broadcast LDS.128)
+        acc.x = fma(hr[2 * i].x, ww.x, acc.x);
+        acc.y = fma(hr[2 * i].y, ww.x, acc.y);
+        acc1.x = fma(hr[2 * i + 1].x, ww.y, acc1.x);
+        acc1.y = fma(hr[2 * i + 1].y, ww.y, acc1.y);
       }
-      if (colok) ocol[(int64_t)d * a.B] = make_double2(acc.x * scs, acc.y * scs);
+      if (colok)
+        ocol[(int64_t)d * a.B] = make_double2((acc.x + acc1.x) * scs, (acc.y + acc1.y) * scs);
       }
     }
     __syncwarp();
@@ -533,7 +536,7 @@ static void gather_b_m(const NnfftPlanImpl& p, const double2* h, double2* out, i
   GatherBArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, h, out, p.g.M2, p.fft.Kout, p.g.N2,
                 p.fft.s_lo, B, per_cta};
   const int threads = (int)std::min<int64_t>(kThreadsB, ceil_div(B, 32) * 32);
-  const size_t smem = sizeof(double) * (2 * M + 1) * 32 * (threads / 32);
+  const size_t smem = sizeof(double) * (2 * M + 2) * 32 * (threads / 32);
   k_gather_b<M><<<dim3((unsigned)ceil_div(p.g.M2, per_cta), (unsigned)ceil_div(B, threads)),
                   threads, smem, s>>>(a, p.c2);
   SF_LAUNCH_CHECK();
