@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(kThreadsB + 32, SFB_SPREADBW_MINB(M))
 #else
           if (lane == 0) mbar_expect_tx(&S.full[st], (unsigned)(n * ncol * (int)sizeof(double2)));
           __syncwarp();
+          SF_BOUNDS(!mine || (src >= 0 && cl >= cell0 && cl < cend));
           if (mine)
             bulk_g2s_tx(&S.f[st][l][0], a.f + (int64_t)src * a.B + col0,
                         (unsigned)(ncol * (int)sizeof(double2)), &S.full[st]);
@@ -324,6 +325,8 @@ __global__ void __launch_bounds__(kThreadsB + 32, SFB_SPREADBW_MINB(M))
       if (ci < total) {  // warp-uniform
         const int c = cell0 + ci;
         while (cs == c) {
+          SF_BOUNDS(i < nsrc && fp >= f0 && fp < f0 + kWsStages * kWsSrc * kFRow &&
+                    wp >= w0 && wp < w0 + kWsStages * kWsSrc * kWRow);
 #if !(SFB_SPREADBW_ABL & 1)
           const double2 fv = lds_d2(fp);
 #pragma unroll
@@ -341,6 +344,7 @@ __global__ void __launch_bounds__(kThreadsB + 32, SFB_SPREADBW_MINB(M))
         }
         // point cell0 + ci + 1 - M (slot p) is final
         if (colok && ci >= ci_lo && ci < ci_hi) {
+          SF_BOUNDS(gp >= a.grid && gp < a.grid + a.K * a.B);
           if (ci >= 2 * M - 1 && ci < ncell) {
             *gp = r[p];  // interior: only this tile touches it
           } else if (r[p].x != 0.0 || r[p].y != 0.0) {
@@ -405,6 +409,7 @@ __global__ void __launch_bounds__(kThreadsB, 4) k_gather_b(GatherBArgs a, WinCoe
       kk %= (int)a.N2;
       if (kk < 0) kk += (int)a.N2;
     }
+    SF_BOUNDS(kk >= 0 && kk < Kout);
     return __ldg(hcol + (int64_t)kk * a.B);
   };
   for (int64_t jb = j0; jb < j1; jb += 32) {

@@ -7,6 +7,22 @@
 #include <stdexcept>
 #include <string>
 
+// Bounds-checked build (make EXTRA=-DSFB_BOUNDS=1): device-side asserts on the
+// indices of every shared-memory accumulator / staging buffer and of the
+// table-driven global accesses of the hot kernels.  compute-sanitizer is
+// closed on this project's GPU pool, so this build, run over the GPU test
+// suite and tools/sanitize_cases.py, is the memcheck substitute
+// (profiles/r02/r02x_bounds_checked.log).  Off in the shipped library.
+#ifndef SFB_BOUNDS
+#define SFB_BOUNDS 0
+#endif
+#if SFB_BOUNDS
+#include <cassert>
+#define SF_BOUNDS(cond) assert(cond)
+#else
+#define SF_BOUNDS(cond) ((void)0)
+#endif
+
 namespace sfb {
 
 // Error carrying one of the SINCFFT_* status codes (see include/sincfft_b200.h).

@@ -125,7 +125,10 @@ struct RegFft {
       } else {
         const int u = but(k), b = vec(k);
 #pragma unroll
-        for (int r = 0; r < R; ++r) sm[spad((pos<S>(u, r) << NBL) + b)] = x[k][r];
+        for (int r = 0; r < R; ++r) {
+          SF_BOUNDS(spad((pos<S>(u, r) << NBL) + b) < SMEM_ELEMS);
+          sm[spad((pos<S>(u, r) << NBL) + b)] = x[k][r];
+        }
       }
     }
   }
@@ -140,7 +143,10 @@ struct RegFft {
       } else {
         const int u = but(k), b = vec(k);
 #pragma unroll
-        for (int r = 0; r < R; ++r) x[k][r] = sm[spad((pos<S>(u, r) << NBL) + b)];
+        for (int r = 0; r < R; ++r) {
+          SF_BOUNDS(spad((pos<S>(u, r) << NBL) + b) < SMEM_ELEMS);
+          x[k][r] = sm[spad((pos<S>(u, r) << NBL) + b)];
+        }
       }
     }
   }

@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(Ga
         s1.x += h1[t].x * p1, s1.y += h1[t].y * p1;
       }
 #else
+      SF_BOUNDS(k0 >= klo && k0 + 2 * M - 1 <= khi && k1 >= klo && k1 + 2 * M - 1 <= khi);
       window_dot2<M>(C, p0 - c0, p1 - c1, hs + (k0 - klo), hs + (k1 - klo), s0, s1, k0 == k1);
 #endif
     } else {

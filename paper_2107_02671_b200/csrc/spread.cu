@@ -95,6 +95,7 @@ __device__ __forceinline__ void issue_f(const SpreadArgs& a, W& S, bool live, in
   if (live) {
     const int cnt = S.info[st_d][lane] & 255;
     const int4 pm = S.perm[st_d][lane];
+    SF_BOUNDS(cnt <= kChunk && pm.x >= 0 && pm.y >= 0 && pm.z >= 0 && pm.w >= 0);
     const int src[kChunk] = {pm.x, pm.y, pm.z, pm.w};
 #pragma unroll
     for (int s = 0; s < kChunk; ++s) {
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(kSpreadWarps * 32, SFB_SPREAD_MINB) k_spread(S
     issue_f<REAL>(a, S, b + 1 < b1, (i + 1) % kDescStages, (i + 1) & 1, col, lane);
     const int btile = next_tile;
     if (b + 1 < b1) next_tile = __ldg(a.blk_tile + b + 1);
+    SF_BOUNDS(btile >= 0 && (int64_t)btile * kTile < a.K + kTile);
     if (btile != tile) {
       if (tile >= 0) flush_tile<M>(a, S, tile, col, lane);
       tile = btile;
@@ -326,6 +328,7 @@ __global__ void __launch_bounds__(kSpreadWarps * 32, SFB_SPREAD_MINB) k_spread(S
         }
       }
       if (lane == 0) {
+        SF_BOUNDS(lcell >= 0 && lcell + 2 * M - 1 < W::SPAN);
 #pragma unroll
         for (int k = 0; k < 2 * M; ++k) {
           double2 t = S.acc[lcell + k];
@@ -345,6 +348,7 @@ __global__ void __launch_bounds__(kSpreadWarps * 32, SFB_SPREAD_MINB) k_spread(S
 #pragma unroll
       for (int k = 0; k < 2 * M; ++k) {
         if (leader) {
+          SF_BOUNDS(lcell >= 0 && lcell + k < W::SPAN);
           double2 t = S.acc[lcell + k];
           t.x += r[k].x;
           t.y += r[k].y;

@@ -1,6 +1,7 @@
-"""GPU box, under compute-sanitizer (one --tool per gpurun call): small
-invocations that launch every hot kernel once, each checked against the
-oracle so a silent corruption also fails the run.
+"""GPU box, under compute-sanitizer (one --tool per gpurun call) or with the
+bounds-checked library (make EXTRA=-DSFB_BOUNDS=1, SINCFFT_B200_LIB=...):
+small invocations that launch every hot kernel once, each checked against
+the oracle so a silent corruption also fails the run.
 
     compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize_cases.py
 
@@ -9,7 +10,7 @@ forced with SFB_SPREAD_DENSE=1), k_spread_small, the register FFT passes of
 the config-3 shape (k_colfwd_r1 / k_rowmul_r1 / k_colinv_r1 + k_bluestein_fix:
 N = 2^20 gives the 4096 x 1024 Bluestein regardless of the node count),
 k_gather2 (TMA-staged span), the batched path of the config-4 shape
-(k_spread_b, k_*_rb, k_gather_b), and the fast sinc transform."""
+(k_spread_bw, k_*_rb, k_gather_b), and the fast sinc transform."""
 import os
 import sys
 
