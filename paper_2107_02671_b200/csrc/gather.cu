@@ -142,6 +142,9 @@ __device__ __forceinline__ double2 gather_one(const GatherArgs& a, const double2
 #ifndef SFB_GATHER_PF
 #define SFB_GATHER_PF 0  // L2 prefetch distance in CTAs (0: off)
 #endif
+#ifndef SFB_GATHER_ALLSAME
+#define SFB_GATHER_ALLSAME 1  // warps whose 32 threads all hold a same-window pair: no second loads
+#endif
 #ifndef SFB_GATHER_TMA
 #define SFB_GATHER_TMA 1  // the h span staged by one TMA bulk copy
 #endif
@@ -288,6 +291,11 @@ __global__ void __launch_bounds__(kGatherThreads, SFB_GATHER2_MINB) k_gather2(Ga
       }
 #else
       SF_BOUNDS(k0 >= klo && k0 + 2 * M - 1 <= khi && k1 >= klo && k1 + 2 * M - 1 <= khi);
+#if SFB_GATHER_ALLSAME
+      if (__all_sync(__activemask(), k0 == k1))  // (lanes past M2 have left)
+        window_dot2<M, true>(C, p0 - c0, p1 - c1, hs + (k0 - klo), hs + (k1 - klo), s0, s1, true);
+      else
+#endif
       window_dot2<M>(C, p0 - c0, p1 - c1, hs + (k0 - klo), hs + (k1 - klo), s0, s1, k0 == k1);
 #endif
     } else {

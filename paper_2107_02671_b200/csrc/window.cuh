@@ -225,7 +225,10 @@ __device__ __forceinline__ void window_accumulate2(const WinCoef& C, double d0, 
 // Gather form of window_accumulate2: two targets (d0 over h0[0..2M), d1 over
 // h1[0..2M)) interpolated together, every coefficient feeding both Horner
 // chains and each tap pair consumed as soon as it is formed (no tap arrays).
-template <int M>
+// ALLSAME: every lane of the warp has both targets on one window (h1 == h0,
+// checked with a warp vote by the caller): the second target reuses the first
+// one's loaded values with no second loads and no register copies.
+template <int M, bool ALLSAME = false>
 __device__ __forceinline__ void window_dot2(const WinCoef& C, double d0, double d1,
                                             const double2* h0, const double2* h1, double2& s0,
                                             double2& s1, bool same = false) {
@@ -250,11 +253,18 @@ __device__ __forceinline__ void window_dot2(const WinCoef& C, double d0, double 
     // loads is predicated off, so a quarter-warp of such threads costs no
     // shared-memory wavefront for it
     const double2 a0 = h0[ih], b0 = h0[il];
-    const double2 a1 = same ? a0 : h1[ih], b1 = same ? b0 : h1[il];
-    s0.x = fma(a0.x, hi0, fma(b0.x, lo0, s0.x));
-    s0.y = fma(a0.y, hi0, fma(b0.y, lo0, s0.y));
-    s1.x = fma(a1.x, hi1, fma(b1.x, lo1, s1.x));
-    s1.y = fma(a1.y, hi1, fma(b1.y, lo1, s1.y));
+    if constexpr (ALLSAME) {
+      s0.x = fma(a0.x, hi0, fma(b0.x, lo0, s0.x));
+      s0.y = fma(a0.y, hi0, fma(b0.y, lo0, s0.y));
+      s1.x = fma(a0.x, hi1, fma(b0.x, lo1, s1.x));
+      s1.y = fma(a0.y, hi1, fma(b0.y, lo1, s1.y));
+    } else {
+      const double2 a1 = same ? a0 : h1[ih], b1 = same ? b0 : h1[il];
+      s0.x = fma(a0.x, hi0, fma(b0.x, lo0, s0.x));
+      s0.y = fma(a0.y, hi0, fma(b0.y, lo0, s0.y));
+      s1.x = fma(a1.x, hi1, fma(b1.x, lo1, s1.x));
+      s1.y = fma(a1.y, hi1, fma(b1.y, lo1, s1.y));
+    }
   }
 }
 
