@@ -51,6 +51,7 @@ struct sincfft_sinc_plan_s {
   std::unique_ptr<sfb::NfftPlanImpl> nf1, nf3;  // NFFT trafo / adjoint stages (grid sets)
   int64_t N = 0, n_star = 0, L1 = 0, L2 = 0, n = 0;
   int device = 0, mode = 0;
+  GraphCache graphs;  // device-pointer executes, keyed on (c, out, c_is_real)
 };
 
 struct sincfft_nfft_plan_s {
@@ -301,9 +302,9 @@ bool use_graph(const sfb::NnfftPlanImpl& p, int64_t batch) {
 // (LRU); a new key reuses the least recently used exec through
 // cudaGraphExecUpdate (same topology, new pointers) instead of instantiating.
 // Returns false when the caller should launch directly (first sighting).
-bool launch_graph(sincfft_nnfft_plan plan, const double2* f, double2* out, int64_t batch,
-                  cudaStream_t s) {
-  GraphCache& gc = plan->graphs;
+template <class Capture>
+bool launch_graph(GraphCache& gc, const void* f, void* out, int64_t batch, cudaStream_t s,
+                  Capture&& capture) {
   std::lock_guard<std::mutex> lk(gc.mu);
   cudaGraphExec_t exec = nullptr;
   for (size_t i = 0; i < gc.entries.size(); ++i) {
@@ -334,7 +335,7 @@ bool launch_graph(sincfft_nnfft_plan plan, const double2* f, double2* out, int64
     cudaGraph_t graph = nullptr;
     try {
       SF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      sfb::run_execute(plan->impl, f, out, (int)batch, cs);
+      capture(cs);
       SF_CUDA(cudaStreamEndCapture(cs, &graph));
       if (gc.entries.size() == GraphCache::kMax) {
         cudaGraphExec_t lru = gc.entries.front().exec;
@@ -463,7 +464,9 @@ int sincfft_nnfft_execute(sincfft_nnfft_plan plan, const double* f, double* out,
     const size_t ob = sizeof(double2) * (size_t)p.g.M2 * batch;
     InBuf fin(f, fb, ptr_kind, s);
     if (ptr_kind == SINCFFT_PTR_DEVICE && use_graph(p, batch) &&
-        launch_graph(plan, (const double2*)f, (double2*)out, batch, s)) {
+        launch_graph(plan->graphs, f, out, batch, s, [&](cudaStream_t cs) {
+          sfb::run_execute(plan->impl, (const double2*)f, (double2*)out, (int)batch, cs);
+        })) {
     } else if (ptr_kind == SINCFFT_PTR_DEVICE) {
       sfb::run_execute(p, (const double2*)fin.ptr, (double2*)out, (int)batch, s);
     } else {
@@ -977,6 +980,16 @@ int sincfft_sinc_execute(sincfft_sinc_plan plan, const double* c, int32_t c_is_r
     set_device(plan->device);
     cudaStream_t s = as_stream(stream);
     const size_t cb = (c_is_real ? sizeof(double) : sizeof(double2)) * (size_t)plan->L1;
+    // device pointers: the ~13 launches of the two stages replayed as one CUDA
+    // graph (captured on the second execute with the same buffers)
+    static const bool no_graphs = getenv("SINCFFT_NO_GRAPHS") != nullptr;
+    if (ptr_kind == SINCFFT_PTR_DEVICE && !no_graphs &&
+        launch_graph(plan->graphs, c, out, c_is_real ? 1 : 0, s, [&](cudaStream_t cs) {
+          sfb::Scratch a2(sizeof(double2) * (size_t)(plan->n + 1), cs);
+          sinc_stage1(plan, c, c_is_real, a2.as<double2>(), cs);
+          sinc_stage3(plan, a2.as<double2>(), out, SINCFFT_PTR_DEVICE, cs);
+        }))
+      return;
     InBuf cin(c, cb, ptr_kind, s);
     sfb::Scratch alpha(sizeof(double2) * (size_t)(plan->n + 1), s);
     sinc_stage1(plan, cin.ptr, c_is_real, alpha.as<double2>(), s);
