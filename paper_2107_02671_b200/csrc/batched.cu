@@ -537,7 +537,10 @@ static void spread_b_m(const NnfftPlanImpl& p, const double2* f, double2* grid, 
 template <int M>
 static void gather_b_m(const NnfftPlanImpl& p, const double2* h, double2* out, int B,
                        cudaStream_t s) {
-  const int per_cta = 64;
+  static const int per_cta = [] {  // targets per CTA (tuning: SFB_GATHERB_PER_CTA)
+    const char* e = getenv("SFB_GATHERB_PER_CTA");
+    return e ? std::max(32, atoi(e) / 32 * 32) : 64;
+  }();
   GatherBArgs a{p.gp.pos.p, p.gp.perm.p, p.gp.scale.p, h, out, p.g.M2, p.fft.Kout, p.g.N2,
                 p.fft.s_lo, B, per_cta};
   const int threads = (int)std::min<int64_t>(kThreadsB, ceil_div(B, 32) * 32);
