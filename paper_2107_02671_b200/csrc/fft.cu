@@ -2018,6 +2018,7 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
   set_smem(k_rowmul_b<512, 3>, smem_bytes(kColElemsB));
   set_smem(k_colinv_b<512, 3>, smem_bytes(kColElemsB));
   set_reg_smem<2, 256, 4>();
+  set_reg_smem<2, 128, 4>();
   set_smem(k_colfwd_r1<1024, 2, 512, SFB_FFT_CMINB, 8, kColPL>,
            sizeof(double2) * RegFft<1024, 2, 512, 8, kColPL>::SMEM_ELEMS);
   set_smem(k_colinv_r1<1024, 2, 512, SFB_FFT_CMINB, 8, kColPL>,
@@ -2181,7 +2182,8 @@ bool fft_supports_point_major(const NnfftPlanImpl& p) {
 }
 
 // Register-resident passes for this plan's point-major shape (512 x 512,
-// config 4): 4 columns x 256 threads, 64 registers, 4 CTAs/SM.  Measured
+// config 4): 4 columns x 256 threads, 64 registers, 4 CTAs/SM (the row pass:
+// 4 columns x 128 threads x 2 butterflies, see launch_reg_point_major).  Measured
 // alternatives: 8 columns x 256 (2 butterflies per thread: spills), 8 x 512,
 // 4 x 256 at 3 CTAs/SM -- 1.89-2.75 ms against 1.77 ms; the shared-memory
 // kernels k_*_b (SFB_FFT_REG=0) 2.20 ms.
@@ -2191,17 +2193,33 @@ static bool reg_point_major(const FftPlan& f) {
   return !(e && atoi(e) == 0);
 }
 
-static void launch_reg_point_major(const FftBArgs& x, int64_t L1, int64_t L2, cudaStream_t s) {
-  constexpr int NBL = 2, T = 256, MINB = 4;
+template <int NBL, int T, int MINB>
+static void launch_reg_point_major_t(const FftBArgs& x, int64_t L1, int64_t L2, cudaStream_t s,
+                                     int which) {
   const size_t sm = sizeof(double2) * ((size_t)512 << NBL);
   const dim3 gc((unsigned)ceil_div(x.B, 1 << NBL), (unsigned)L1);  // column groups fastest
   const dim3 gr((unsigned)ceil_div(x.B, 1 << NBL), (unsigned)L2);
-  k_colfwd_rb<512, NBL, T, MINB><<<gc, T, sm, s>>>(x);
+  if (which == 0) k_colfwd_rb<512, NBL, T, MINB><<<gc, T, sm, s>>>(x);
+  if (which == 1) k_rowmul_rb<512, NBL, T, MINB><<<gr, T, sm, s>>>(x);
+  if (which == 2) k_colinv_rb<512, NBL, T, MINB><<<gc, T, sm, s>>>(x);
   SF_LAUNCH_CHECK();
-  k_rowmul_rb<512, NBL, T, MINB><<<gr, T, sm, s>>>(x);
-  SF_LAUNCH_CHECK();
-  k_colinv_rb<512, NBL, T, MINB><<<gc, T, sm, s>>>(x);
-  SF_LAUNCH_CHECK();
+}
+
+static void launch_reg_point_major(const FftBArgs& x, int64_t L1, int64_t L2, cudaStream_t s) {
+  // SFB_FFT_RB_T128: bit p set -> pass p (0 colfwd, 1 rowmul, 2 colinv) runs
+  // with 128 threads and TWO butterflies per thread (128 registers, 4 CTAs per
+  // SM) instead of 256 threads and one.  Measured at config 4: rowmul 616 ->
+  // 585 us (the fused forward-multiply-inverse pass has the longest dependent
+  // chain per thread and gains from the second butterfly's ILP); colfwd 524 ->
+  // 612, colinv 625 -> 967 (spills).  Default: rowmul only.
+  static const int t128 = [] {
+    const char* e = getenv("SFB_FFT_RB_T128");
+    return e ? atoi(e) : 2;
+  }();
+  for (int w = 0; w < 3; ++w) {
+    if (t128 >> w & 1) launch_reg_point_major_t<2, 128, 4>(x, L1, L2, s, w);
+    else launch_reg_point_major_t<2, 256, 4>(x, L1, L2, s, w);
+  }
 }
 
 // Columns can be transformed in groups of G (SFB_FFT_GROUP): the group's work array Y (L x G
