@@ -158,29 +158,44 @@ def pin_one_core():
         os.sched_setaffinity(0, {core})
 
 
-def cpu_sample_rate(cfg, steps=1, warmup=0, sample_nodes=1 << 22):
+def cpu_sample_rate(cfg, steps=1, warmup=0, sample_nodes=1 << 22, budget_s=None):
     """Time the CPU oracle's trafo (single-threaded numpy/scipy, like the
     reference) pinned to one core: the workload's geometry (N, m) with
     sample_nodes sources and targets drawn the same way (the full workload
-    when sample_nodes >= M1, with the workload's own seed)."""
+    when sample_nodes >= M1, with the workload's own seed).  With budget_s the
+    run is bounded in wall time on a slow host: warm-ups stop (after one) at a
+    quarter of the budget, timed steps (after two) at the budget; the counts
+    actually run are reported."""
     from oracle import sincfft_oracle as O
     pin_one_core()
     M = min(sample_nodes, cfg["M1"])
     full = M == cfg["M1"]
     sub = dict(cfg, M1=M, M2=M, batch=0)
+    t_start = time.perf_counter()
     v, x, f = make_inputs(sub, seed=0 if full else 1)
     n_star, vs = O.rescale_frequencies(cfg["N"], v, 2.0, cfg["m"])
     t0 = time.perf_counter()
     tab = O.plan(n_star, vs, x, m1=cfg["m"], m2=cfg["m"])
     t_plan = time.perf_counter() - t0
+
+    def spent(frac):
+        return budget_s is not None and time.perf_counter() - t_start > frac * budget_s
+
+    warm_run = 0
     for _ in range(warmup):
+        if warm_run >= 1 and spent(0.25):
+            break
         O.trafo(tab, f)
+        warm_run += 1
     ts = []
     for _ in range(steps):
+        if len(ts) >= 2 and spent(1.0):
+            break
         t0 = time.perf_counter()
         O.trafo(tab, f)
         ts.append(time.perf_counter() - t0)
     t = statistics.median(ts)
+    steps, warmup = len(ts), warm_run
     info = cpu_info()
     return {"value": 2 * M / t, "unit": "nodes/s", "cores": 1, "kind": "port",
             "sample": (f"oracle trafo (restatement of the reference's nnfft_trafo, pinned to "
@@ -198,7 +213,9 @@ def run_reference(args, cfg):
         return
     # the reference's own CPU path on the same workload as the B200 arm: the
     # full configuration (config 3: ~45 s of plan, ~17 s per trafo on one core)
-    base = cpu_sample_rate(cfg, steps=args.steps, warmup=args.warmup, sample_nodes=cfg["M1"])
+    # (bounded at ~4 minutes of wall time on a slow host: fewer steps, same workload)
+    base = cpu_sample_rate(cfg, steps=args.steps, warmup=args.warmup, sample_nodes=cfg["M1"],
+                           budget_s=args.ref_budget_s)
     line = {"metric": METRIC, "value": base["value"], "unit": "nodes/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": base["seconds_per_step"] * 1e3, "higher_is_better": True,
@@ -829,6 +846,9 @@ def main():
                     help="window cut-off m1 = m2 (config 2 is BASELINE's sweep over "
                          "m in {2, 4, 6, 8, 10}; default: the config's own m)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--ref-budget-s", type=float, default=240.0,
+                    help="--impl reference: wall-time bound (s) after which warm-ups / timed "
+                         "steps stop early (never below 1 / 2)")
     ap.add_argument("--e2e-streams", type=int, default=4,
                     help="host-buffer pipeline depth of the e2e leg (streams in flight)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],

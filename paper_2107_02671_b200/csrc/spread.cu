@@ -142,6 +142,9 @@ __device__ __forceinline__ void flush_tile(const SpreadArgs& a, W& S, int tile, 
 #ifndef SFB_SPREAD_PM
 #define SFB_SPREAD_PM 0
 #endif
+#ifndef SFB_SPREAD_ABL
+#define SFB_SPREAD_ABL 0  // timing ablations (wrong results): 1 no accumulate rounds, 2 no window polynomials
+#endif
 // Pair-major form of one block (SFB_SPREAD_PM): a lane's NS (2 or 4) sources
 // are evaluated together, tap pair by tap pair -- every coefficient (a
 // uniform constant-bank load) feeds NS Horner chains instead of 2 -- and each
@@ -292,6 +295,16 @@ __global__ void __launch_bounds__(kSpreadWarps * 32, SFB_SPREAD_MINB) k_spread(S
     double2 r[2 * M];
 #pragma unroll
     for (int k = 0; k < 2 * M; ++k) r[k] = make_double2(0.0, 0.0);
+#if SFB_SPREAD_ABL & 2  // timing ablation: f values as taps, no polynomials
+    if (cnt > 0 && !REAL) {
+      const double2* fs = reinterpret_cast<const double2*>(&S.f[sf][0][0]);
+#pragma unroll
+      for (int k = 0; k < 2 * M; ++k) {
+        r[k].x = fs[lane + 32 * (k & 3)].x * p01.x;
+        r[k].y = fs[lane + 32 * (k & 3)].y * p23.y;
+      }
+    } else
+#endif
     if (cnt > 0) {
       if (REAL) {
         const double* fs = reinterpret_cast<const double*>(&S.f[sf][0][0]);
@@ -316,6 +329,14 @@ __global__ void __launch_bounds__(kSpreadWarps * 32, SFB_SPREAD_MINB) k_spread(S
     // sources in one cell) is summed across lanes first (butterfly) and added
     // once; otherwise equal cells in one block would race, so leaders of each
     // cell group go first, round by round (rarely more than one round)
+#if SFB_SPREAD_ABL & 1  // timing ablation (wrong results): plain stores, no rounds
+    if (cnt > 0) {
+#pragma unroll
+      for (int k = 0; k < 2 * M; ++k) S.acc[lcell + k] = r[k];
+    }
+    __syncwarp();
+    continue;
+#endif
     int same = 0;
     __match_all_sync(0xffffffffu, cnt > 0 ? lcell : -1 - lane, &same);
     if (same) {

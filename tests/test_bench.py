@@ -53,3 +53,17 @@ def test_reference_arm_line():
     assert line["impl"] == "reference" and line["config"]["same_config"] is True
     assert line["cpu_baseline"]["cores"] == 1 and line["cpu_baseline"]["nproc"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["value"] > 0
+
+
+def test_reference_arm_wall_time_bound():
+    """A tiny budget stops the arm after one warm-up and two timed steps; the
+    line says how many ran."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--config", "1", "--steps", "20", "--warmup", "5",
+                        "--ref-budget-s", "1e-9"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["steps"] == 20 and line["warmup"] == 5  # as asked, for the driver's match
+    assert "median of 2 after 1 warm-up" in line["cpu_baseline"]["sample"]
+    assert line["config"]["same_config"] is True and line["value"] > 0
