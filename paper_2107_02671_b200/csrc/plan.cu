@@ -12,6 +12,8 @@
 
 #include "nnfft_impl.cuh"
 
+#include <chrono>
+
 #include <cstdio>
 
 #ifndef SFB_SPREAD_CTAS
@@ -800,8 +802,28 @@ void octet_order(NnfftPlanImpl& p, int64_t M2, cudaStream_t s) {
   SF_LAUNCH_CHECK();
 }
 
+// SFB_PLAN_TIMING=1: wall time of every plan stage (stream synchronised), on stderr
+struct PlanLaps {
+  cudaStream_t s;
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  explicit PlanLaps(cudaStream_t st) : s(st), on(getenv("SFB_PLAN_TIMING") != nullptr) {
+    if (on) cudaStreamSynchronize(s);
+    t0 = std::chrono::steady_clock::now();
+  }
+  void lap(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[plan] %-28s %8.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cudaStream_t s) {
   const Geometry& g = p.g;
+  PlanLaps laps(s);
   // --- domain checks and clipping (nnfft.py:162-170)
   const double vlim = 0.5 / g.a;
   const double vmax = device_absmax(v_dev, g.M1, s);
@@ -820,10 +842,12 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
   k_clip<<<blocks(g.M1), 256, 0, s>>>(v_dev, p.v_clip.p, g.M1, vlim);
   k_clip<<<blocks(g.M2), 256, 0, s>>>(x_dev, p.x_clip.p, g.M2, 0.5);
   SF_LAUNCH_CHECK();
+  laps.lap("domain checks + clip");
 
   // --- window polynomials (window.cu); sigma of window 2 is N2/K (nnfft.py:173)
   p.c1 = fit_window(g.m1, g.beta1);
   p.c2 = fit_window(g.m2, g.beta2);
+  laps.lap("window polynomial fits");
 
   // --- phi_hat_2 at l - K/2 (nnfft.py:180-183)
   p.hat2.alloc(g.K);
@@ -837,8 +861,10 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
       fail(2, "nnfft_plan: phi_hat_2 must be strictly positive on the coarse grid");
   }
 
+  laps.lap("phi_hat_2 table");
   // --- sources: sort by cell, chunk, tile into blocks
   build_sources(p, p.v_clip.p, g.M1, (double)g.N1, g.K, s);
+  laps.lap("build_sources");
 
   // --- targets: sort by (original-index slice, fine-grid cell), 1/phi_hat_1,
   //     and the output window [s_lo, s_hi] the gather reads
@@ -857,10 +883,12 @@ void build_plan(NnfftPlanImpl& p, const double* v_dev, const double* x_dev, cuda
   }
   build_targets(p, p.x_clip.p, g.M2, (double)g.N / (double)g.N1, (double)g.N2, g.N2, g.m2, ts, s,
                 fs_lo, fkout);
+  laps.lap("build_targets");
 
   p.fft.in_scale = 1.0 / ((double)g.N1 * (double)g.N2);
   build_fft(p, s);
   SF_CUDA(cudaStreamSynchronize(s));
+  laps.lap("build_fft");
 }
 
 // Grid indices the spread can touch, [c + K/2 + 1 - m1, c + K/2 + m1] for the

@@ -160,8 +160,11 @@ class NnfftPlan:
         self.geometry = geometry
         self.window1 = window1
         self.window2 = window2
-        self.v = v
-        self.x = x
+        # host copies of the clipped nodes (the reference's plan.v / plan.x):
+        # numpy inputs are clipped on first access (the device clips its own
+        # copy), so a plan does not pay two M-sized host passes it may never use
+        self._v, self._x = v, x
+        self._vlim = None
         self.device = device
         self._tables = None
         g = _lib.Geometry()
@@ -177,6 +180,22 @@ class NnfftPlan:
     @property
     def handle(self):
         return self._h
+
+    def _clip_host(self):
+        if self._vlim is not None:
+            self._v = np.clip(self._v, -self._vlim, self._vlim)
+            self._x = np.clip(self._x, -0.5, 0.5)
+            self._vlim = None
+
+    @property
+    def v(self):
+        self._clip_host()
+        return self._v
+
+    @property
+    def x(self):
+        self._clip_host()
+        return self._x
 
     def _export(self):
         if self._tables is None:
@@ -229,14 +248,13 @@ def nnfft_plan(N, v, x, *, sigma1=2.0, sigma2=2.0, m1=4, m2=4,
     geo = NnfftGeometry.from_parameters(N, v.size, x.size, float(sigma1), float(sigma2),
                                         int(m1), int(m2))
     vmax = 0.5 / geo.a
-    if np.max(np.abs(v)) > vmax + _DOMAIN_TOL:
+    # max |.| without an M-sized temporary (same NaN behaviour as np.max(np.abs(.)))
+    if _absmax(v) > vmax + _DOMAIN_TOL:
         raise ParameterError(
             "nnfft_plan: frequencies exceed 1/(2a) = {:.6g}; apply "
             "rescale_frequencies to map [-1/2, 1/2] data into the band".format(vmax))
-    v = np.clip(v, -vmax, vmax)
-    if np.max(np.abs(x)) > 0.5 + _DOMAIN_TOL:
+    if _absmax(x) > 0.5 + _DOMAIN_TOL:
         raise ParameterError("nnfft_plan: spatial nodes must lie in [-1/2, 1/2]")
-    x = np.clip(x, -0.5, 0.5)
     w1 = WindowSpec(window1, geo.m1, geo.sigma1, geo.N1)
     w2 = WindowSpec(window2, geo.m2, geo.sigma2, geo.N2)
     dev = _default_device(device)
@@ -244,7 +262,14 @@ def nnfft_plan(N, v, x, *, sigma1=2.0, sigma2=2.0, m1=4, m2=4,
     _lib.check(_lib.lib.sincfft_nnfft_plan_create_ex(
         C.byref(h), geo.N, geo.M1, geo.M2, float(sigma1), float(sigma2), geo.m1, geo.m2,
         _vp(v), _vp(x), _lib.PTR_HOST, dev, flags, None))
-    return NnfftPlan(h, geo, w1, w2, v, x, dev)
+    plan = NnfftPlan(h, geo, w1, w2, v, x, dev)
+    plan._vlim = vmax  # host copies clipped lazily (NnfftPlan.v / .x)
+    return plan
+
+
+def _absmax(a):
+    hi, lo = a.max(), a.min()
+    return hi if hi != hi or lo != lo or hi >= -lo else -lo
 
 
 def _default_device(device):

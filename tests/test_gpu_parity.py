@@ -141,3 +141,20 @@ def test_single_wave_known_answer():
     plan = sf.nnfft_plan(32, v, x, m1=6, m2=6)
     out = sf.nnfft_trafo(plan, np.array([1.0 + 0j]))
     assert np.max(np.abs(out - np.exp(-2j * np.pi * 32 * v[0] * x))) < 1e-9
+
+
+def test_host_node_copies_are_clipped_lazily():
+    """plan.v / plan.x are the reference's clipped nodes (nnfft.py:168-170);
+    numpy inputs within the 1e-12 domain tolerance are clipped on first access,
+    the device plan clips its own copy."""
+    vlim = 0.5 / sf.NnfftGeometry.from_parameters(32, 3, 4, 2.0, 2.0, 4, 4).a
+    v = np.array([-vlim - 5e-13, 0.1, vlim + 5e-13])
+    x = np.array([-0.5 - 5e-13, 0.0, 0.25, 0.5 + 5e-13])
+    plan = sf.nnfft_plan(32, v, x, m1=4, m2=4)
+    out = sf.nnfft_trafo(plan, np.ones(3, complex))
+    assert np.all(np.isfinite(out))
+    assert plan.v.max() == vlim and plan.v.min() == -vlim
+    assert plan.x.max() == 0.5 and plan.x.min() == -0.5
+    ref = sf.nnfft_trafo(sf.nnfft_plan(32, np.clip(v, -vlim, vlim), np.clip(x, -0.5, 0.5),
+                                       m1=4, m2=4), np.ones(3, complex))
+    assert np.array_equal(out, ref)
