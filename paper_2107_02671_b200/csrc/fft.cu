@@ -2073,7 +2073,12 @@ void build_fft(NnfftPlanImpl& p, cudaStream_t s) {
     double best = 1e300;
     // L may fall short of K + Kout - 1 by D <= Dmax slots (fixed afterwards
     // by k_bluestein_fix at ~D^2 cost), which admits much smoother lengths
-    const int64_t Dmax = getenv("SFB_FFT_NO_SHORT_L") ? 0 : std::min<int64_t>(kFixMax, Lmin / 8);
+    // (D <= Kout - 1 keeps L >= K: the K inputs themselves must not wrap -- a
+    // plan whose targets sit in a few cells has Kout of a few dozen)
+    const int64_t Dmax = getenv("SFB_FFT_NO_SHORT_L")
+                             ? 0
+                             : std::max<int64_t>(
+                                   0, std::min<int64_t>({kFixMax, Lmin / 8, f.Kout - 1}));
     for (int64_t L2 = 2; L2 <= 2048; ++L2) {
       if (!smooth7(L2)) continue;
       for (int pass = 0; pass < 2; ++pass) {

@@ -336,6 +336,31 @@ def test_short_bluestein_length_fix(N, M, m, B):
         assert relerr(ob, O.trafo(tab, fb), fb) <= TOL, b
 
 
+@pytest.mark.parametrize("N,m,B", [(32822, 4, 0), (32768, 4, 16), (65536, 6, 3)])
+def test_narrow_output_window_keeps_inputs_inside_the_fft(N, m, B):
+    """Targets confined to a few fine-grid cells give an output window Kout of
+    a few dozen slots.  The Bluestein length may then fall short of
+    K + Kout - 1 by at most Kout - 1 slots: a shorter L would wrap the K inputs
+    themselves (found by tools/fuzz_parity.py: L = 65536 < K = 65652 gave a
+    1.7e-2 error)."""
+    rng = np.random.default_rng(N + m)
+    M1, M2 = 1000, 65
+    v = rng.uniform(-0.5, 0.5, M1)
+    x = 0.3 + 1e-3 * (rng.random(M2) - 0.5)
+    shape = (M1, B) if B else (M1,)
+    f = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    n, vs = sf.rescale_frequencies(N, v, 2.0, m)
+    plan = sf.nnfft_plan(n, vs, x, m1=m, m2=m)
+    g = plan.backend_geometry
+    assert g["Kout"] < 200 and g["L"] >= g["K"], g
+    out = sf.nnfft_trafo(plan, f)
+    tab = O.plan(n, vs, x, m1=m, m2=m)
+    for b in ([None] if not B else [0, B - 1]):
+        fb = f if b is None else f[:, b]
+        ob = out if b is None else out[:, b]
+        assert relerr(ob, O.trafo(tab, fb), fb) <= TOL, b
+
+
 def test_short_bluestein_length_nfft():
     """The same fix under the NFFT trafo's conjugated input (nfft.cu)."""
     rng = np.random.default_rng(77)
