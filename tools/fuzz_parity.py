@@ -66,7 +66,7 @@ rejected = 0
 def one_case(c):
     N = int(rng.choice([8, 12, 30, 64, 100, 254, 256, 1000, 1024, 2 * 1031, 4096, 6 * 1001,
                         10000, 16384, 2 * 16411, 65536, 100000]))
-    m1, m2 = int(rng.integers(2, 13)), int(rng.integers(2, 13))
+    m1, m2 = int(rng.integers(2, 17)), int(rng.integers(2, 17))  # kMaxM = 16
     s1, s2 = float(rng.choice([1.25, 1.5, 2.0])), float(rng.choice([1.25, 1.5, 2.0]))
     M1 = int(rng.choice([1, 2, 31, 33, 100, 257, 1000, 4097, 20000, 100000]))
     M2 = int(rng.choice([1, 3, 64, 65, 999, 5000, 30000, 100000]))

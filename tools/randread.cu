@@ -54,6 +54,13 @@ __global__ void k_red(double* g, const int* __restrict__ idx, int n, int K) {
 }
 
 int main() {
+  // L2G=32|64|128: cudaLimitMaxL2FetchGranularity before the context does any work
+  if (const char* e = getenv("L2G")) {
+    cudaError_t rc = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
+    printf("L2 fetch granularity: asked %s, rc %d, now %zu\n", e, (int)rc, got);
+  }
   const int n = 1 << 24;
   std::vector<int> h(n);
   double2* f;
