@@ -87,7 +87,20 @@ def one_case(c):
         tab = O.plan(n, vs, x, sigma1=s1, sigma2=s2, m1=m1, m2=m2)
         shape = (M1, B) if B else (M1,)
         f = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
-        out = sf.nnfft_trafo(plan, f)
+        if rng.integers(0, 3) == 0:
+            # device pointers: plan from CUDA tensors, the execute captured into a CUDA
+            # graph on the first call and replayed on the second (capi.cu launch_graph)
+            import torch
+            plan = sf.nnfft_plan(n, torch.from_numpy(vs).cuda(), torch.from_numpy(x).cuda(),
+                                 sigma1=s1, sigma2=s2, m1=m1, m2=m2)
+            df = torch.from_numpy(f).cuda()
+            first = sf.nnfft_trafo(plan, df).cpu().numpy()
+            out = sf.nnfft_trafo(plan, df).cpu().numpy()
+            rep = float(np.max(np.abs(out - first)) / np.sum(np.abs(f)) * max(B, 1))
+            note("graph_replay", rep, desc, 1e-15)
+            desc += " device"
+        else:
+            out = sf.nnfft_trafo(plan, f)
         cols = sorted({0, B - 1}) if B else [None]
         err = 0.0
         for b in cols:

@@ -9,7 +9,7 @@ MET=gpu__time_duration.sum,sm__inst_executed_pipe_fp64.sum,sm__pipe_fp64_cycles_
 for c in ${CONFIGS:-3 4 5}; do
   cmd="python bench.py --config $c --no-cpu --steps 2 --warmup 3"
   $cmd > $OUT/plain_config$c.log 2>&1 || { echo "plain run config $c failed"; exit 1; }
-  ncu --metrics $MET --clock-control none -k regex:"${KREGEX:-k_}" -s ${SKIP:-0} -c ${COUNT:-60} --csv \
+  ncu --metrics $MET --clock-control none -k regex:"${KREGEX:-k_}" -s ${SKIP:-0} -c ${COUNT:-160} --csv \
       --log-file $OUT/pipes_config$c.csv $cmd > $OUT/ncu_config$c.log 2>&1
 done
 ls -la $OUT
