@@ -791,6 +791,15 @@ def run_b200(args, cfg):
                          "launch_ms": t_dom * 1e3,
                          "random_gather_floor_ms": gather_floor_ms
                          if dom == "spread" else None,
+                         "bound_note": (
+                             "single-column spread: f is read through the cell-sort permutation, "
+                             "2^24 random 16-byte reads at config 3; HBM serves ~59 G random "
+                             "sectors/s whatever the fill size (tools/randread.cu: 0.285 ms alone; "
+                             "torch's f[perm] = random_gather_floor_ms), and a timing-only build "
+                             "with no window arithmetic and no accumulation still takes 0.351 of "
+                             "the kernel's 0.388 ms (DESIGN.md, SFB_SPREAD_ABL), so frac against "
+                             "the sequential-copy peak understates how close the kernel is to "
+                             "its loads") if dom == "spread" and B == 1 else None,
                          "fp64": None if flops[dom] is None else {
                              "achieved_tflops": flops[dom] / t_dom / 1e12,
                              "peak_tflops": fp64_peak,
